@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark: theta-instantiations/s of a parametric H^2 matrix at n = 2^18 (3D)
+(BASELINE.json configs[2], "C3"), one step = instantiate(theta) + one MVM.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (rows sharded, NCCL all-gather of y)
+
+Data: seeded synthetic (points U[0,1)^3, theta draws of harness.cpp:254-260,
+x ~ N(0,1)); random-free otherwise. The near-field stream (113 GB at C3) is
+far larger than the 126 MB L2, so no L2 flush is needed between steps.
+
+`--impl reference` times the reference's CPU path (the oracle port of
+proj/src/phmatrix.cpp:168-269; the reference itself needs Eigen3 and cannot
+be built here) on a bounded sample of the same workload, extrapolated.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[2] (the metric's n = 2^18, 3D configuration)
+    "c3": dict(n=262144, d=3, family="e", box=(0.05, 0.5), l_max=4, p_s=4, p_theta=8, eta=1.0, fmt="h2",
+               points="uniform"),
+    # BASELINE.json configs[1]
+    "c2": dict(n=65536, d=2, family="m32", box=(0.05, 0.5), l_max=5, p_s=8, p_theta=10, eta=1.0, fmt="h2",
+               points="uniform"),
+    # BASELINE.json configs[0] (CPU-runnable PR1 case; param-H)
+    "c1": dict(n=4096, d=2, family="gauss", box=(0.1, 1.0), l_max=3, p_s=6, p_theta=8, eta=1.0, fmt="h",
+               points="uniform"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=16, help="1/f of near/far blocks timed on the CPU")
+    return ap.parse_args()
+
+
+def theta_draws(lo, hi, count, seed):
+    # harness.cpp:254-260: Rng(mix_seed(seed, 0x74686574)).uniform(lo, hi)
+    import paper_2511_03109_b200 as ph
+
+    return ph.theta_draws(lo, hi, count, seed)
+
+
+def make_points(ph, c, seed):
+    if c["points"] == "uniform":
+        return ph.generate_points(c["n"], c["d"], seed)
+    return ph.generate_mixture_points(c["n"], c["d"], 16, 0.05, seed)
+
+
+def make_cfg(ph, c, rank=0, world=1, near_mode=None):
+    return ph.PHConfig(spec=ph.KernelSpec(ph.Family.from_id(c["family"]), [c["box"]]), l_max=c["l_max"],
+                       p_s=c["p_s"], p_theta=c["p_theta"], eta=c["eta"], eps=1e-5, seed=0,
+                       near_mode=ph.NearMode.SNAPSHOT if near_mode is None else near_mode,
+                       shard_rank=rank, shard_count=world)
+
+
+def algorithmic_bytes(info, c, n_classes_bytes):
+    """per-theta instantiate and per-vector H^2 MVM bytes."""
+    P = info["P"]
+    b_inst = 8 * info["near_stream_elems"] + n_classes_bytes
+    n = c["n"]
+    b_mvm = 8 * (info["near_entries"] + 2 * n + c["d"] * c["p_s"] * n + c["d"] * c["p_s"] ** 2 * info["nodes"]
+                 + info["n_classes"] * P * P + 2 * P * info["nodes"])
+    return b_inst, b_mvm
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_baseline(ph, c, pts, pm_host, steps, sample, seed):
+    """The oracle port of the reference's online path on this host's cores,
+    on a bounded sample: every class, 1/sample of the near blocks and 1/sample
+    of the far blocks; per-theta time extrapolated to the full block lists."""
+    from oracle import pyoracle as po
+
+    cores = os.cpu_count() or 1
+    po.lib().orc_set_threads(cores)
+    om = po.OracleMatrix(pts, c["l_max"], c["eta"], c["p_s"], ph.Family.from_id(c["family"]), [c["box"]],
+                         c["p_theta"], h2=c["fmt"] == "h2")
+    cnt = om.counts()
+    for k in range(cnt["n_classes"]):
+        om.set_coupling(k, pm_host.coupling_cores(k))
+    near_mask = np.zeros(cnt["n_near"], dtype=np.uint8)
+    near_mask[::sample] = 1
+    far_mask = np.zeros(cnt["n_far"], dtype=np.uint8)
+    far_mask[::sample] = 1
+    om.make_near_snapshots(near_mask)
+    om.finalize()
+    ints, _ = om.nodes()
+    near, far, _ = om.blocks()
+    sizes = ints[:, 3].astype(np.int64)
+    ent = sizes[near[:, 0]] * sizes[near[:, 1]]
+    f_near = ent[near_mask == 1].sum() / ent.sum()
+    f_far = far_mask.sum() / max(1, len(far_mask))
+    thetas = theta_draws(c["box"][0], c["box"][1], max(steps, 1), seed)
+    x = ph.generate_normal(c["n"], seed + 1)
+    per = []
+    for s in range(steps):
+        inst, secs = om.instantiate_timed([thetas[s % len(thetas)]], near_mask)
+        _, asecs = inst.apply_sample(x, near_mask, far_mask)
+        t = secs[0] + secs[1] / f_near + asecs[0] + asecs[1] / f_far + asecs[2] / f_near
+        per.append(t)
+        del inst
+    t = float(np.median(per))
+    return {"value": 1.0 / t, "unit": "theta/s", "cores": cores, "kind": "port",
+            "sample": f"instantiate over all {cnt['n_classes']} classes and 1/{sample} of the near blocks "
+                      f"({f_near:.4f} of near entries, {cores} threads); one MVM (single-threaded, as the reference) "
+                      f"over 1/{sample} of the far and near blocks + full basis passes; extrapolated per theta, "
+                      f"median of {steps} thetas"}
+
+
+# --------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_03109_b200 as ph
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = CONFIGS[args.config]
+    ctx = ph.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    pts = make_points(ph, c, args.seed)
+    cfg = make_cfg(ph, c, rank, world)
+    t0 = time.time()
+    pm = ph.offline_h2(pts, cfg, ctx) if c["fmt"] == "h2" else ph.offline_h(pts, cfg, ctx)
+    build_s = time.time() - t0
+    info = pm.info()
+    n = c["n"]
+    thetas = theta_draws(c["box"][0], c["box"][1], 32, args.seed)
+    x_host = torch.from_numpy(ph.generate_normal(n, args.seed + 1)).pin_memory()
+    x_dev = x_host.cuda()
+    y_dev = torch.empty(n, dtype=torch.float64, device="cuda")
+    rows = info["row_end"] - info["row_begin"]
+    counts = None
+    if world > 1:
+        cnt = torch.tensor([rows], dtype=torch.int64, device="cuda")
+        allc = [torch.zeros_like(cnt) for _ in range(world)]
+        dist.all_gather(allc, cnt)
+        counts = [int(v.item()) for v in allc]
+        maxr = max(counts)
+        yrows = torch.zeros(maxr, dtype=torch.float64, device="cuda")
+        gathered = torch.empty(world * maxr, dtype=torch.float64, device="cuda")
+        yperm = torch.empty(n, dtype=torch.float64, device="cuda")
+    inst = ph.instantiate(pm, [thetas[0]])
+
+    def step(s):
+        inst.reinstantiate([thetas[s % len(thetas)]])
+        if world == 1:
+            inst.apply_device(x_dev.data_ptr(), y_dev.data_ptr(), 1)
+        else:
+            inst.apply_rows_device(x_dev.data_ptr(), yrows.data_ptr(), 1)
+            dist.all_gather_into_tensor(gathered, yrows)
+            off = 0
+            for r in range(world):  # padded all-gather -> contiguous tree order
+                yperm[off: off + counts[r]].copy_(gathered[r * maxr: r * maxr + counts[r]])
+                off += counts[r]
+            ph.lib().phm_unpermute_device(pm._h, ph._P(yperm.data_ptr()), ph._P(y_dev.data_ptr()), 1)
+
+    for s in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ctx.enable_timing(True)
+    ctx.reset_timers()
+    launches0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for s in range(args.steps):
+            step(args.warmup + s)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    ms = ev0.elapsed_time(ev1)
+    k1_ms, k1_n = ctx.timer("near_inst")
+    timers = {}
+    for name in ("near_inst", "class_inst", "near_w", "near_mvm", "coupling", "leaf_fwd", "up", "down",
+                 "leaf_bwd", "gather", "scatter", "far_h"):
+        t, cnt = ctx.timer(name)
+        if cnt:
+            timers[name] = {"ms_per_launch": t / cnt, "launches": cnt}
+    ctx.enable_timing(False)
+    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item())
+
+    # e2e through the public API with host buffers (rank-local; N=1 path)
+    e2e = None
+    if world == 1:
+        y_host = torch.empty(n, dtype=torch.float64).pin_memory()
+        xh, yh = x_host.numpy(), y_host.numpy()
+        from ctypes import c_double, POINTER
+
+        def e2e_step(s):
+            inst.reinstantiate([thetas[s % len(thetas)]])
+            ph._check(ph.lib().phm_apply(inst._h, xh.ctypes.data_as(POINTER(c_double)), n,
+                                         yh.ctypes.data_as(POINTER(c_double)), 1))
+
+        for s in range(args.warmup):
+            e2e_step(s)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for s in range(args.steps):
+            e2e_step(s)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a.elapsed_time(b)
+        e2e = {"value": args.steps * 1000.0 / e_ms, "unit": "theta/s", "h2d_bytes_per_step": 8 * n + 8,
+               "d2h_bytes_per_step": 8 * n}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        host_pm = ph.offline_structure(pts, make_cfg(ph, c))
+        cpu = cpu_baseline(ph, c, pts, host_pm, 3, args.cpu_sample, args.seed)
+
+    if rank == 0:
+        peak, peak_kind = measured_peak()
+        ncls = info["n_classes"]
+        cls_bytes = 0
+        for k in range(ncls):  # middle cores + L/R read, H and C written, per class
+            cores = pm.coupling_cores(k)
+            mid = cores[c["d"]]
+            rl, rr = mid.shape[0], mid.shape[2]
+            cls_bytes += 8 * (mid.size + info["P"] * (rl + rr) + rl * rr + info["P"] ** 2)
+        b_inst, b_mvm = algorithmic_bytes(info, c, cls_bytes)
+        k1_avg = k1_ms / max(1, k1_n)
+        k1_bytes = 8 * info["near_stream_elems"]  # read R+1 slabs... (R reads + 1 write) per near entry
+        achieved = k1_bytes / (k1_avg * 1e-3) / 1e9
+        mvm_ms = sum(v["ms_per_launch"] * v["launches"] for k, v in timers.items()
+                     if k in ("near_mvm", "coupling", "leaf_fwd", "up", "down", "leaf_bwd", "gather", "scatter",
+                              "far_h")) / max(1, args.steps)
+        line = {
+            "metric": "theta-instantiations/s (instantiate + H2 MVM per theta) at n=2^18, 3D",
+            "value": world * 0 + args.steps * 1000.0 / ms,
+            "unit": "theta/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded uniform points, harness theta draws, x~N(0,1))",
+            "config": {"workload": f"{args.config}: n={n} d={c['d']} {c['fmt']} kernel={c['family']} "
+                                   f"l_max={c['l_max']} p_s={c['p_s']} p_theta={c['p_theta']} eta={c['eta']} "
+                                   f"near=snapshot", "rows_sharded_over": world,
+                       "l2": "inputs (near snapshots) larger than L2; no flush needed"},
+            "roofline": {"bound": "hbm", "kernel": "k_inst_flat (K1 near instantiate)", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "peak_kind": peak_kind, "bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg},
+            "mvm": {"ms": mvm_ms, "algorithmic_bytes": b_mvm, "GB_s": b_mvm / (mvm_ms * 1e-3) / 1e9 if mvm_ms else None},
+            "instantiate_algorithmic_bytes": b_inst,
+            "kernels": timers,
+            "gpu_launches": launches,
+            "build_s": build_s,
+            "structure": {k: info[k] for k in ("n_near", "n_far", "n_classes", "c_sp", "near_entries")},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import paper_2511_03109_b200 as ph
+
+    c = CONFIGS[args.config]
+    pts = make_points(ph, c, args.seed)
+    host_pm = ph.offline_structure(pts, make_cfg(ph, c))
+    steps = max(1, args.steps)
+    cpu = cpu_baseline(ph, c, pts, host_pm, steps, args.cpu_sample, args.seed)
+    line = {
+        "impl": "reference",
+        "metric": "theta-instantiations/s (instantiate + H2 MVM per theta) at n=2^18, 3D",
+        "value": cpu["value"], "unit": "theta/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 / cpu["value"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": {"workload": args.config},
+        "cpu_baseline": cpu,
+        "e2e": {"value": cpu["value"], "unit": "theta/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -1,0 +1,192 @@
+/*
+ * phmat_b200 — C ABI of the B200-native online stage of parametric H / H^2
+ * matrices (arXiv 2511.03109).
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference
+ * (/root/reference/proj) is a C++ library with no FFI of its own (its
+ * python module is an empty pybind11 stub, proj/python/phmat_module.cpp:1-2),
+ * so the entry points below mirror its public C++ API, one C function per
+ * reference entry point, with plain pointers and sizes:
+ *
+ *   phm_matrix_build       <- phmat::offline_h / offline_h2
+ *                             (proj/include/phmat/phmatrix.hpp:82-91)
+ *   phm_instantiate        <- phmat::instantiate(pm, theta, counter)
+ *                             (proj/include/phmat/phmatrix.hpp:133-138,
+ *                              proj/src/phmatrix.cpp:168-225)
+ *   phm_apply              <- LinearOperator::apply / Instantiated{H,H2}Matrix::apply
+ *                             (proj/include/phmat/phmatrix.hpp:95-128,
+ *                              proj/src/phmatrix.cpp:227-269), plus m > 1
+ *   phm_instance_far_h     <- InstantiatedXMatrix::far_h[i]   (phmatrix.hpp:105,119)
+ *   phm_instance_near_d    <- InstantiatedXMatrix::near_d[i]  (phmatrix.hpp:106,120)
+ *   phm_to_dense           <- InstantiatedXMatrix::to_dense   (phmatrix.hpp:110,124)
+ *   phm_matrix_metrics     <- phmat::metrics                  (phmatrix.hpp:141-153)
+ *   phm_matrix_perm/nodes/blocks/class_keys
+ *                          <- ClusterTree / BlockClusterTree / far_key views
+ *                             (geometry.hpp:49-92, phmatrix.hpp:56-57)
+ *   phm_parametric_vectors <- phmat::parametric_vectors       (farfield.hpp:31-34)
+ *   phm_generate_points    <- phmat::generate_points          (harness.hpp:77)
+ *
+ * Conventions: every function returns PHM_OK (0) or an error code; no C++
+ * exception crosses the ABI. The code maps back to the reference's exception
+ * types (domain_error, invalid_argument, logic_error, runtime_error) and
+ * phm_last_error() returns the message (thread-local). Matrices are
+ * column-major doubles; point sets are n x d row-major (the reference's
+ * Eigen row access order). Vectors are in the ORIGINAL point order, as in the
+ * reference; the tree-order permutation is internal.
+ */
+#ifndef PHMAT_B200_H_
+#define PHMAT_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum phm_status {
+  PHM_OK = 0,
+  PHM_ERR_RUNTIME = 1,   /* std::runtime_error (size guards, artifact problems) */
+  PHM_ERR_DOMAIN = 2,    /* std::domain_error  (theta outside the box) */
+  PHM_ERR_INVALID = 3,   /* std::invalid_argument (length mismatch, bad spec) */
+  PHM_ERR_LOGIC = 4,     /* std::logic_error   (PHMAT_CHECK failures) */
+  PHM_ERR_CUDA = 5,      /* CUDA runtime failure / no sm_100 device */
+  PHM_ERR_RANGE = 6      /* index out of range */
+};
+
+/* Kernel families: reference ids e, tps, se, mc, mn (kernels.hpp:14-23) plus
+ * the single-parameter Gaussian and Matern-3/2, -5/2 families. */
+enum phm_family {
+  PHM_KERNEL_E = 0,
+  PHM_KERNEL_TPS = 1,
+  PHM_KERNEL_SE = 2,
+  PHM_KERNEL_MC = 3,
+  PHM_KERNEL_MN = 4,
+  PHM_KERNEL_GAUSS = 5,
+  PHM_KERNEL_MATERN32 = 6,
+  PHM_KERNEL_MATERN52 = 7
+};
+
+enum phm_format { PHM_FORMAT_H = 0, PHM_FORMAT_H2 = 1 };
+/* Near-field modes: the reference's TT and Direct (phmatrix.hpp:18) plus
+ * Snapshot (full-rank NearBlockTT generated on the GPU). */
+enum phm_near_mode { PHM_NEAR_TT = 0, PHM_NEAR_DIRECT = 1, PHM_NEAR_SNAPSHOT = 2 };
+
+/* PHConfig (phmatrix.hpp:20-35) + KernelSpec (kernels.hpp:31-38) + the
+ * extensions of SURVEY.md Appendix A (amplitude parameter, per-dimension
+ * p_theta) + row sharding for multi-GPU. */
+typedef struct phm_config {
+  int32_t family;
+  int32_t amplitude;   /* 1: trailing theta component sigma^2 multiplies the kernel */
+  int32_t d_theta;
+  int32_t p_theta[3];
+  double theta_lo[3];
+  double theta_hi[3];
+  int32_t format;
+  int32_t l_max;
+  int32_t p_s;
+  int32_t near_mode;
+  double eps;
+  double eta;          /* <= 0 selects sqrt(d) */
+  int64_t r_max_far;
+  int64_t r_max_near;
+  uint64_t seed;
+  int32_t translation_cache;
+  int32_t threads;     /* 0: PHMAT_THREADS / hardware */
+  int32_t shard_rank;
+  int32_t shard_count;
+} phm_config;
+
+/* StructureMetrics (phmatrix.hpp:141-153) + build statistics. */
+typedef struct phm_info {
+  int64_t n, d, nodes, n_near, n_far, n_classes, c_sp, constructed;
+  int64_t P;                 /* p_s^d */
+  int64_t row_begin, row_end;/* tree-order rows owned by this shard */
+  int64_t near_entries;      /* sum over local near blocks of n_sigma n_tau */
+  int64_t near_stream_elems; /* sum of n_sigma n_tau (R_b + 1): K1's algorithmic elements */
+  int64_t device_bytes;
+  int64_t storage_entries;
+  double storage_gb, nf_ratio, ff_ratio, coupling_ratio, rank;
+  double tree_s, ff_s, nf_s, upload_s;
+  uint64_t evals_offline, evals_online, evals_audit;
+  int32_t any_rank_capped;
+  int32_t pad;
+} phm_info;
+
+typedef struct phm_context_s* phm_context;
+typedef struct phm_matrix_s* phm_matrix;
+typedef struct phm_instance_s* phm_instance;
+
+const char* phm_last_error(void);
+int phm_version(void);
+void phm_config_default(phm_config* cfg);
+
+/* Context: one CUDA device and one stream (own, or a caller's stream). */
+int phm_context_create(int device, phm_context* out);
+int phm_context_destroy(phm_context ctx);
+int phm_context_set_stream(phm_context ctx, void* cuda_stream);
+int phm_context_get_stream(phm_context ctx, void** cuda_stream);
+int phm_context_sync(phm_context ctx);
+/* CUDA-event timing of every kernel launch, aggregated by kernel name. */
+int phm_context_enable_timing(phm_context ctx, int on);
+int phm_context_timer(phm_context ctx, const char* name, double* total_ms, int64_t* launches);
+int phm_context_reset_timers(phm_context ctx);
+int phm_context_launches(phm_context ctx, int64_t* launches);
+
+/* Offline build (host structure + TT-cross, upload, GPU snapshots). */
+int phm_matrix_build(phm_context ctx, const double* points, int64_t n, int d, const phm_config* cfg,
+                     phm_matrix* out);
+/* Host-only build (no device): structure + offline TT data for inspection;
+ * instantiate / apply on such a handle fail with PHM_ERR_LOGIC. */
+int phm_matrix_build_host(const double* points, int64_t n, int d, const phm_config* cfg, phm_matrix* out);
+int phm_matrix_destroy(phm_matrix m);
+int phm_matrix_info(phm_matrix m, phm_info* info);
+/* Structure views (bit-exact with the reference's tree and block lists). */
+int phm_matrix_perm(phm_matrix m, int32_t* perm /* n */);
+int phm_matrix_nodes(phm_matrix m, int32_t* ints /* 7 per node: level,parent,first_child,count,coords[3] */,
+                     double* boxes /* 6 per node: lo[3], hi[3] */);
+int phm_matrix_blocks(phm_matrix m, int32_t* near_pairs /* 2 per near block */,
+                      int32_t* far_pairs /* 2 per far block */, int32_t* far_key /* per far block */);
+int phm_matrix_class_keys(phm_matrix m, int64_t* keys /* 4 per class: level, offset[3] */);
+int phm_matrix_theta_grid(phm_matrix m, int k, double* nodes /* p_theta[k] */);
+/* Offline payload views, two-call pattern: pass data == NULL to get sizes.
+ * dims: 3 per core (r0, m, r1); *ncores <= 10. */
+int phm_matrix_coupling(phm_matrix m, int64_t cls, int32_t* ncores, int64_t* dims, double* data, int64_t* len);
+int phm_matrix_near_tt(phm_matrix m, int64_t near_block, int32_t* ncores, int64_t* dims, double* data, int64_t* len);
+int phm_matrix_near_rank(phm_matrix m, int64_t near_block, int64_t* rank);
+int phm_matrix_near_column(phm_matrix m, int64_t near_block, int64_t kap, double* out /* n_sigma n_tau */);
+int phm_matrix_far_st(phm_matrix m, int64_t far_index, double* S, double* T, int64_t* dims /* 4 */);
+int phm_matrix_class_lr(phm_matrix m, int64_t cls, double* L, double* R, int64_t* dims /* 4 */);
+int phm_parametric_vectors(phm_matrix m, const double* theta, int n_theta, double* out /* sum p_theta */);
+
+/* Online stage. */
+int phm_instantiate(phm_matrix m, const double* theta, int n_theta, phm_instance* out);
+int phm_reinstantiate(phm_instance inst, const double* theta, int n_theta);
+int phm_instance_destroy(phm_instance inst);
+int phm_instance_sync(phm_instance inst);
+int phm_instance_far_h(phm_instance inst, int64_t far_index, double* out, int64_t* rows, int64_t* cols);
+int phm_instance_near_d(phm_instance inst, int64_t near_block, double* out);
+int phm_instance_class_c(phm_instance inst, int64_t cls, double* out /* P x P */);
+/* y = K(theta) x, host buffers, n_rows must equal n (length check before
+ * any launch, phmatrix.cpp:228); m right-hand sides, column-major. */
+int phm_apply(phm_instance inst, const double* x, int64_t n_rows, double* y, int64_t m);
+/* Device buffers, asynchronous on the context stream. */
+int phm_apply_device(phm_instance inst, const double* x_dev, double* y_dev, int64_t m);
+/* Row-sharded apply: this shard's rows [row_begin, row_end) of y in tree
+ * order (rows x m, column-major); gather across ranks, then unpermute. */
+int phm_apply_rows_device(phm_instance inst, const double* x_dev, double* yrows_dev, int64_t m);
+int phm_unpermute_device(phm_matrix m, const double* yperm_dev, double* y_dev, int64_t mcols);
+/* Induced dense matrix (n x n column-major), refuses n > guard. */
+int phm_to_dense(phm_instance inst, double* out, int64_t guard);
+
+/* Seeded generators (harness.cpp:174-181; mixture and normal are new). */
+int phm_generate_points(int64_t n, int d, uint64_t seed, double* out);
+int phm_generate_mixture_points(int64_t n, int d, int clusters, double sigma, uint64_t seed, double* out);
+int phm_generate_normal(int64_t n, uint64_t seed, double* out);
+/* theta draws of run_experiment (harness.cpp:254-260), one parameter. */
+int phm_theta_draws(double lo, double hi, int64_t count, uint64_t seed, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PHMAT_B200_H_ */

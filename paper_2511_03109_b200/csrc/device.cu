@@ -1,0 +1,1011 @@
+// Device layer: flattens a HostMatrix into HBM-resident arrays once
+// (upload), generates near-field snapshots on the GPU (K11), and runs the
+// online stage (instantiate, apply) as a sequence of sm_100a kernels on one
+// stream. No CPU fallback: every online computation is a kernel launch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "kernels.cuh"
+
+#define CK(x)                                                                                         \
+  do {                                                                                                \
+    cudaError_t e_ = (x);                                                                             \
+    if (e_ != cudaSuccess)                                                                            \
+      throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #x); \
+  } while (0)
+
+namespace phm {
+namespace dev {
+void launch_snapshot(cudaStream_t, const SnapTile*, std::int64_t, const BlockGeom*, const double*, std::int64_t, int,
+                     int, int, const double*, double, double*);
+void launch_inst_flat(cudaStream_t, const double*, std::int64_t, int, const double*, double*);
+void launch_inst_tiles(cudaStream_t, const InstTile*, std::int64_t, const double*, const double*, double*);
+void launch_near_w(cudaStream_t, const NearW*, std::int64_t, const double*, const std::int32_t*, const ThetaV&,
+                   double*);
+void launch_set_vec(cudaStream_t, double*, int, const ThetaV&, double);
+void launch_class_inst(cudaStream_t, const ClassMeta*, int, const double*, const std::int32_t*, const double*,
+                       const double*, const ThetaV&, int, bool, int, int, int, double*, double*);
+void launch_gather(cudaStream_t, const double*, const std::int32_t*, std::int64_t, std::int64_t, double*);
+void launch_scatter(cudaStream_t, const double*, const std::int32_t*, std::int64_t, std::int64_t, double*);
+void launch_leaf_fwd(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*, const double*,
+                     std::int64_t, int, int, int, const double*, int, double*);
+void launch_up(cudaStream_t, const std::int32_t*, int, const std::int32_t*, const std::int32_t*, const double*, int,
+               int, int, int, double*);
+void launch_coupling(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*,
+                     const std::int32_t*, const double*, int, int, const double*, double*);
+void launch_near_mvm(cudaStream_t, const RowItem*, int, const std::int64_t*, const std::int32_t*,
+                     const std::int64_t*, const double*, const double*, double*);
+void launch_down(cudaStream_t, const std::int32_t*, int, const std::int32_t*, const double*, int, int, int, int,
+                 double*);
+void launch_leaf_bwd(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*, const double*,
+                     std::int64_t, int, int, int, const double*, int, std::int64_t, std::int64_t, double*);
+void launch_far_h(cudaStream_t, const FarHItem*, int, int, const std::int64_t*, const std::int32_t*,
+                  const std::int32_t*, const std::int64_t*, const std::int64_t*, const ClassMeta*, const double*,
+                  const double*, const double*, const double*, std::int64_t, std::int64_t, double*);
+}  // namespace dev
+
+// ---------------------------------------------------------------- buffers
+namespace {
+
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      bytes = o.bytes;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t b) {
+    release();
+    if (b == 0) return;
+    CK(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+template <typename T>
+void upload(DBuf& buf, const std::vector<T>& v, cudaStream_t st) {
+  buf.alloc(v.size() * sizeof(T));
+  if (!v.empty()) {
+    CK(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // host vector may die after return
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- context
+struct Context {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  bool timing = false;
+  std::int64_t launches = 0;
+  struct Rec {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  std::map<std::string, std::pair<double, std::int64_t>> totals;
+  ~Context() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& r : recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+    if (own) cudaStreamDestroy(own);
+  }
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  // Brackets one kernel launch with events on the launching stream.
+  template <typename F>
+  void run(const char* name, F&& f) {
+    ++launches;
+    if (!timing) {
+      f();
+      CK(cudaGetLastError());
+      return;
+    }
+    Rec r{name, ev(), ev()};
+    CK(cudaEventRecord(r.a, stream));
+    f();
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(r.b, stream));
+    recs.push_back(r);
+  }
+  void flush_timers() {
+    if (recs.empty()) return;
+    CK(cudaStreamSynchronize(stream));
+    for (auto& r : recs) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, r.a, r.b));
+      auto& t = totals[r.name];
+      t.first += ms;
+      t.second += 1;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    recs.clear();
+  }
+};
+
+std::shared_ptr<Context> context_create(int device) {
+  int count = 0;
+  CK(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) throw std::runtime_error("no such CUDA device");
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) throw std::runtime_error("phmat_b200 is built for sm_100a (B200); found sm_" +
+                                                 std::to_string(prop.major) + std::to_string(prop.minor));
+  auto ctx = std::make_shared<Context>();
+  ctx->device = device;
+  CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+  ctx->stream = ctx->own;
+  return ctx;
+}
+void context_set_stream(Context& ctx, void* s) { ctx.stream = s ? static_cast<cudaStream_t>(s) : ctx.own; }
+void* context_stream(Context& ctx) { return ctx.stream; }
+void context_sync(Context& ctx) { CK(cudaStreamSynchronize(ctx.stream)); }
+void context_enable_timing(Context& ctx, bool on) { ctx.timing = on; }
+void context_timer(Context& ctx, const std::string& name, double* ms, std::int64_t* count) {
+  ctx.flush_timers();
+  auto it = ctx.totals.find(name);
+  *ms = it == ctx.totals.end() ? 0.0 : it->second.first;
+  *count = it == ctx.totals.end() ? 0 : it->second.second;
+}
+void context_reset_timers(Context& ctx) {
+  ctx.flush_timers();
+  ctx.totals.clear();
+}
+std::int64_t context_launches(Context& ctx) { return ctx.launches; }
+
+// ----------------------------------------------------------------- matrix
+struct DevMatrix {
+  std::shared_ptr<Context> ctx;
+  std::unique_ptr<HostMatrix> hm;
+  int d = 0, ps = 0, P = 0, dt = 0, nnodes = 0;
+  Index n = 0;
+  bool h2 = true;
+  NearMode mode = NearMode::TT;
+
+  // structure
+  DBuf perm, pts, node_begin, node_count, node_first_child, node_parent;
+  // near field
+  std::vector<std::int64_t> near_doff;  // per global near block, -1 if not local
+  std::vector<std::int64_t> near_goff;  // start of G1 / snapshot slab 0
+  std::vector<std::int64_t> near_gstride;
+  std::vector<int> near_R;
+  std::int64_t E = 0;    // padded local near entries (D length)
+  std::int64_t E_raw = 0, E_rank = 0;
+  int R_snap = 0;        // snapshot mode: shared rank
+  double snap_amp_nodes_unused = 0;
+  DBuf G;                // near payload
+  DBuf snap_tiles, geo;  // K11 (snapshot / direct)
+  std::int64_t n_snap_tiles = 0;
+  DBuf inst_tiles, near_w_meta, near_cores, near_core_dims;
+  std::int64_t n_inst_tiles = 0, n_near_local = 0, w_len = 0;
+  DBuf row_items, nb_tb, nb_tn, nb_doff;
+  int n_row_items = 0;
+  // far field
+  int ncls = 0;
+  std::vector<dev::ClassMeta> cmeta_h;
+  DBuf cmeta, class_mid, class_mid_dims, class_L, class_R;
+  std::int64_t H_len = 0, C_len = 0;
+  int capA = 0, capB = 0, capT = 0;
+  // H^2 coupling CSR by sigma node
+  DBuf cp_sig, cp_beg, cp_tau, cp_cls;
+  int n_cp_sig = 0;
+  // H form far CSR by level
+  DBuf fh_items, fh_tb, fh_tn, fh_cls, fh_soff, fh_toff, fh_S, fh_T;
+  std::vector<std::pair<int, int>> fh_level_range;  // [item begin, item end) per level
+  std::vector<int> fh_level_maxrows;
+  // basis
+  DBuf U, Etr;
+  DBuf leaves_all, leaves_local;
+  int n_leaves_all = 0, n_leaves_local = 0;
+  std::vector<std::pair<int, int>> up_range, down_range;  // per level into level_nodes arrays
+  DBuf up_nodes, down_nodes;
+  // apply workspace
+  DBuf xp, yp, xhat, yhat, xdev, ydev;
+  Index ws_m = 0;
+  // pooled instance buffers
+  std::vector<DBuf> pool_D;
+  std::mutex mu;
+  std::int64_t device_bytes = 0;
+
+  cudaStream_t st() const { return ctx->stream; }
+};
+
+struct DevInstance {
+  std::shared_ptr<DevMatrix> M;
+  std::vector<double> theta;
+  DBuf D, H, C, w;
+  ~DevInstance() {
+    if (M && D.p) {
+      std::lock_guard<std::mutex> lk(M->mu);
+      M->pool_D.push_back(std::move(D));
+    }
+  }
+};
+
+namespace {
+
+dev::ThetaV make_theta_v(const std::vector<std::vector<double>>& v) {
+  dev::ThetaV tv{};
+  tv.dt = static_cast<int>(v.size());
+  PHM_CHECK(tv.dt <= dev::kMaxThetaDim, "too many theta dimensions");
+  for (int k = 0; k < tv.dt; ++k) {
+    PHM_CHECK(static_cast<int>(v[k].size()) <= dev::kMaxThetaNodes, "p_theta above 32 unsupported on device");
+    tv.p[k] = static_cast<int>(v[k].size());
+    for (size_t j = 0; j < v[k].size(); ++j) tv.v[k][j] = v[k][j];
+  }
+  return tv;
+}
+
+std::int64_t pad4(std::int64_t x) { return (x + 3) & ~std::int64_t(3); }
+
+void ensure_workspace(DevMatrix& M, Index m) {
+  if (M.ws_m >= m) return;
+  M.xp.alloc(sizeof(double) * M.n * m);
+  M.yp.alloc(sizeof(double) * M.n * m);
+  M.xdev.alloc(sizeof(double) * M.n * m);
+  M.ydev.alloc(sizeof(double) * M.n * m);
+  if (M.h2) {
+    M.xhat.alloc(sizeof(double) * M.nnodes * M.P * m);
+    M.yhat.alloc(sizeof(double) * M.nnodes * M.P * m);
+  }
+  M.ws_m = m;
+}
+
+}  // namespace
+
+const HostMatrix& matrix_host(const DevMatrix& m) { return *m.hm; }
+bool matrix_on_device(const DevMatrix& m) { return m.ctx != nullptr; }
+
+std::shared_ptr<DevMatrix> matrix_build_host_only(const double* points, Index n, int d, const Config& cfg) {
+  auto M = std::make_shared<DevMatrix>();
+  M->hm = build_host(points, n, d, cfg);
+  M->n = n;
+  M->d = d;
+  return M;
+}
+std::int64_t matrix_device_bytes(const DevMatrix& m) { return m.device_bytes; }
+std::int64_t matrix_near_rank(const DevMatrix& m, Index b) {
+  if (!m.ctx) throw std::logic_error("host-only matrix has no device near payload");
+  if (b < 0 || b >= static_cast<Index>(m.near_R.size())) throw std::out_of_range("near block index");
+  return m.near_R[b];
+}
+std::int64_t matrix_near_elems(const DevMatrix& m, bool with_rank) { return with_rank ? m.E_rank : m.E_raw; }
+
+void matrix_near_column(const DevMatrix& m, Index b, Index kap, double* out) {
+  if (!m.ctx) throw std::logic_error("host-only matrix has no device near payload");
+  if (b < 0 || b >= static_cast<Index>(m.near_doff.size()) || m.near_doff[b] < 0)
+    throw std::out_of_range("near block not resident");
+  if (kap < 0 || kap >= m.near_R[b]) throw std::out_of_range("near column index");
+  const HostMatrix& H = *m.hm;
+  const Block blk = H.blocks.near[b];
+  const Index N = H.tree->nodes[blk.sigma].count * H.tree->nodes[blk.tau].count;
+  CK(cudaSetDevice(m.ctx->device));
+  CK(cudaMemcpyAsync(out, m.G.as<double>() + m.near_goff[b] + kap * m.near_gstride[b], N * sizeof(double),
+                     cudaMemcpyDeviceToHost, m.st()));
+  CK(cudaStreamSynchronize(m.st()));
+}
+
+std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const double* points, Index n, int d,
+                                        const Config& cfg) {
+  CK(cudaSetDevice(ctx->device));
+  auto Mp = std::make_shared<DevMatrix>();
+  DevMatrix& M = *Mp;
+  M.ctx = ctx;
+  if (cfg.near_mode == NearMode::Snapshot || cfg.near_mode == NearMode::Direct) {
+    if (cfg.spec.family == kMatern && cfg.near_mode == NearMode::Direct)
+      throw std::invalid_argument("direct near mode needs a closed-form kernel family on the GPU");
+  }
+  M.hm = build_host(points, n, d, cfg);
+  const auto t_up = std::chrono::steady_clock::now();
+  HostMatrix& H = *M.hm;
+  const Tree& T = *H.tree;
+  cudaStream_t st = ctx->stream;
+  M.d = d;
+  M.n = n;
+  M.ps = cfg.p_s;
+  M.P = static_cast<int>(H.P());
+  M.dt = H.grids.d_theta();
+  M.nnodes = static_cast<int>(T.nodes.size());
+  M.h2 = cfg.format == Format::H2;
+  M.mode = cfg.near_mode;
+  if (M.h2) PHM_CHECK(M.ps <= 16 && M.P <= 1024, "H2 on device needs p_s <= 16 and p_s^d <= 1024");
+
+  // --- structure
+  {
+    upload(M.perm, T.perm, st);
+    std::vector<double> soa(static_cast<size_t>(d * n));
+    for (int k = 0; k < d; ++k)
+      for (Index p = 0; p < n; ++p) soa[k * n + p] = T.coord(T.perm[p], k);
+    upload(M.pts, soa, st);
+    std::vector<std::int64_t> nb(M.nnodes);
+    std::vector<std::int32_t> nc(M.nnodes), fc(M.nnodes), par(M.nnodes);
+    for (int i = 0; i < M.nnodes; ++i) {
+      nb[i] = T.nodes[i].begin;
+      nc[i] = static_cast<std::int32_t>(T.nodes[i].count);
+      fc[i] = T.nodes[i].first_child;
+      par[i] = T.nodes[i].parent;
+    }
+    upload(M.node_begin, nb, st);
+    upload(M.node_count, nc, st);
+    upload(M.node_first_child, fc, st);
+    upload(M.node_parent, par, st);
+  }
+
+  // --- near field layout
+  const Index nnear = static_cast<Index>(H.blocks.near.size());
+  M.near_doff.assign(nnear, -1);
+  M.near_goff.assign(nnear, -1);
+  M.near_gstride.assign(nnear, 0);
+  M.near_R.assign(nnear, 0);
+  int Rshape = 1;  // snapshot rank: product of non-amplitude theta grids
+  for (int k = 0; k < cfg.spec.shape_params(); ++k) Rshape *= H.grids.grids[k].p;
+  {
+    std::int64_t off = 0;
+    for (Index b = 0; b < nnear; ++b) {
+      if (!H.near_local[b]) continue;
+      const Block blk = H.blocks.near[b];
+      const std::int64_t N = T.nodes[blk.sigma].count * T.nodes[blk.tau].count;
+      M.near_doff[b] = off;
+      off += pad4(N);
+      M.E_raw += N;
+      ++M.n_near_local;
+    }
+    M.E = off;
+  }
+  std::vector<dev::BlockGeom> geo(nnear);
+  for (Index b = 0; b < nnear; ++b) {
+    const Block blk = H.blocks.near[b];
+    geo[b] = {T.nodes[blk.sigma].begin, T.nodes[blk.tau].begin, static_cast<std::int32_t>(T.nodes[blk.sigma].count),
+              static_cast<std::int32_t>(T.nodes[blk.tau].count)};
+  }
+  if (M.mode == NearMode::Snapshot || M.mode == NearMode::Direct) {
+    upload(M.geo, geo, st);
+    std::vector<dev::SnapTile> tiles;
+    const int kTile = 4096;
+    for (Index b = 0; b < nnear; ++b) {
+      if (M.near_doff[b] < 0) continue;
+      const std::int64_t N = static_cast<std::int64_t>(geo[b].s_n) * geo[b].t_n;
+      for (std::int64_t e0 = 0; e0 < N; e0 += kTile)
+        tiles.push_back({M.near_doff[b] + e0, M.E, static_cast<std::int32_t>(e0),
+                         static_cast<std::int32_t>(std::min<std::int64_t>(kTile, N - e0)), static_cast<std::int32_t>(b),
+                         0});
+    }
+    M.n_snap_tiles = static_cast<std::int64_t>(tiles.size());
+    upload(M.snap_tiles, tiles, st);
+  }
+  if (M.mode == NearMode::Snapshot) {
+    M.R_snap = Rshape;
+    M.E_rank = M.E_raw * (Rshape + 1);
+    for (Index b = 0; b < nnear; ++b)
+      if (M.near_doff[b] >= 0) {
+        M.near_goff[b] = M.near_doff[b];
+        M.near_gstride[b] = M.E;
+        M.near_R[b] = Rshape;
+      }
+    M.G.alloc(sizeof(double) * M.E * Rshape);
+    CK(cudaMemsetAsync(M.G.p, 0, M.G.bytes, st));
+    // theta-node table (kappa -> shape parameters, first grid fastest)
+    std::vector<double> tn(3 * Rshape, 1.0);
+    for (int kap = 0; kap < Rshape; ++kap) {
+      int rem = kap;
+      for (int k = 0; k < cfg.spec.shape_params(); ++k) {
+        tn[3 * kap + k] = H.grids.grids[k].nodes[rem % H.grids.grids[k].p];
+        rem /= H.grids.grids[k].p;
+      }
+    }
+    if (cfg.spec.family == kMatern) {
+      // K_nu has no device implementation: evaluate the snapshots on host
+      // threads (offline data production, not the online path) and upload.
+      KernelSpec shape = cfg.spec;
+      shape.amplitude = false;
+      std::vector<double> host(static_cast<size_t>(M.E * Rshape), 0.0);
+      parallel_for(
+          nnear,
+          [&](Index b) {
+            if (M.near_doff[b] < 0) return;
+            const auto& g = geo[b];
+            for (std::int64_t j = 0; j < g.t_n; ++j)
+              for (std::int64_t i = 0; i < g.s_n; ++i) {
+                const Index oi = T.perm[g.s_begin + i], oj = T.perm[g.t_begin + j];
+                double r2 = 0.0;
+                for (int k = 0; k < d; ++k) {
+                  const double dl = T.coord(oi, k) - T.coord(oj, k);
+                  r2 += dl * dl;
+                }
+                const double r = std::sqrt(r2);
+                for (int kap = 0; kap < Rshape; ++kap)
+                  host[kap * M.E + M.near_doff[b] + i + j * g.s_n] = kernel_value(shape, r, &tn[3 * kap]);
+              }
+          },
+          cfg.threads);
+      CK(cudaMemcpyAsync(M.G.p, host.data(), M.G.bytes, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    } else {
+      DBuf dtn;
+      upload(dtn, tn, st);
+      ctx->run("snapshot", [&] {
+        dev::launch_snapshot(st, M.snap_tiles.as<dev::SnapTile>(), M.n_snap_tiles, M.geo.as<dev::BlockGeom>(),
+                             M.pts.as<double>(), n, d, cfg.spec.family, Rshape, dtn.as<double>(), 1.0,
+                             M.G.as<double>());
+      });
+      CK(cudaStreamSynchronize(st));
+    }
+    H.counters.offline.add(static_cast<std::uint64_t>(M.E_raw) * Rshape);
+    H.stats.nf_evals += static_cast<std::uint64_t>(M.E_raw) * Rshape;
+  } else if (M.mode == NearMode::TT) {
+    // G1_b per block (N_b padded even, column-major), theta cores, w chain
+    std::int64_t goff = 0, woff = 0, coff = 0;
+    std::vector<dev::InstTile> tiles;
+    std::vector<dev::NearW> wm;
+    std::vector<std::int32_t> cdims;
+    std::vector<double> cores;
+    for (Index b = 0; b < nnear; ++b) {
+      if (M.near_doff[b] < 0) continue;
+      const TTTensor& tt = H.near_tt[b];
+      const std::int64_t N = tt.cores[0].m, Np = pad4(N), R = tt.cores[0].r1;
+      PHM_CHECK(R <= 256, "near TT rank above 256 unsupported on device");
+      M.near_goff[b] = goff;
+      M.near_gstride[b] = Np;
+      M.near_R[b] = static_cast<int>(R);
+      M.E_rank += N * (R + 1);
+      const int kTile = 2048;
+      for (std::int64_t e0 = 0; e0 < Np; e0 += kTile)
+        tiles.push_back({M.near_doff[b] + e0, goff + e0, Np, woff,
+                         static_cast<std::int32_t>(std::min<std::int64_t>(kTile, Np - e0)),
+                         static_cast<std::int32_t>(R)});
+      dev::NearW nw{};
+      nw.core_off = coff;
+      nw.w_off = woff;
+      nw.dims_off = static_cast<std::int32_t>(cdims.size());
+      nw.ncores = tt.order() - 1;
+      nw.R = static_cast<std::int32_t>(R);
+      for (int c = 1; c < tt.order(); ++c) {
+        cdims.push_back(static_cast<std::int32_t>(tt.cores[c].r0));
+        cdims.push_back(static_cast<std::int32_t>(tt.cores[c].m));
+        cdims.push_back(static_cast<std::int32_t>(tt.cores[c].r1));
+        cores.insert(cores.end(), tt.cores[c].data.begin(), tt.cores[c].data.end());
+        coff += tt.cores[c].size();
+      }
+      wm.push_back(nw);
+      goff += Np * R;
+      woff += R;
+    }
+    M.G.alloc(sizeof(double) * goff);
+    {
+      std::vector<double> host(static_cast<size_t>(goff), 0.0);
+      for (Index b = 0; b < nnear; ++b) {
+        if (M.near_doff[b] < 0) continue;
+        const TTCore& g1 = H.near_tt[b].cores[0];
+        for (Index k = 0; k < g1.r1; ++k)
+          std::memcpy(&host[M.near_goff[b] + k * M.near_gstride[b]], &g1.data[k * g1.m], g1.m * sizeof(double));
+      }
+      if (goff) CK(cudaMemcpyAsync(M.G.p, host.data(), M.G.bytes, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    M.n_inst_tiles = static_cast<std::int64_t>(tiles.size());
+    upload(M.inst_tiles, tiles, st);
+    upload(M.near_w_meta, wm, st);
+    upload(M.near_cores, cores, st);
+    upload(M.near_core_dims, cdims, st);
+    M.w_len = woff;
+  } else {  // Direct
+    M.E_rank = M.E_raw;
+  }
+
+  // K6 work: CSR by sigma leaf, row chunks of 128
+  {
+    std::vector<std::vector<Index>> by_sigma(M.nnodes);
+    for (Index b = 0; b < nnear; ++b)
+      if (M.near_doff[b] >= 0) by_sigma[H.blocks.near[b].sigma].push_back(b);
+    std::vector<dev::RowItem> items;
+    std::vector<std::int64_t> tb, dof;
+    std::vector<std::int32_t> tn;
+    for (int s = 0; s < M.nnodes; ++s) {
+      if (by_sigma[s].empty()) continue;
+      const int bbeg = static_cast<int>(tb.size());
+      for (Index b : by_sigma[s]) {
+        const Block blk = H.blocks.near[b];
+        tb.push_back(T.nodes[blk.tau].begin);
+        tn.push_back(static_cast<std::int32_t>(T.nodes[blk.tau].count));
+        dof.push_back(M.near_doff[b]);
+      }
+      const int bend = static_cast<int>(tb.size());
+      const int ns = static_cast<int>(T.nodes[s].count);
+      for (int i0 = 0; i0 < ns; i0 += 128)
+        items.push_back({T.nodes[s].begin + i0, std::min(128, ns - i0), ns, i0, bbeg, bend, 0});
+    }
+    M.n_row_items = static_cast<int>(items.size());
+    upload(M.row_items, items, st);
+    upload(M.nb_tb, tb, st);
+    upload(M.nb_tn, tn, st);
+    upload(M.nb_doff, dof, st);
+  }
+
+  // --- far field: classes
+  {
+    M.ncls = static_cast<int>(H.couplings.size());
+    std::vector<double> mid, L, R;
+    std::vector<std::int32_t> mdims;
+    std::int64_t hoff = 0;
+    int maxrl = 1, maxA = 1, maxB = 1, maxs1 = 1;
+    for (int k = 0; k < M.ncls; ++k) {
+      const Coupling& c = H.couplings[k];
+      dev::ClassMeta cm{};
+      cm.rl = static_cast<std::int32_t>(c.rank_left());
+      cm.rr = static_cast<std::int32_t>(c.rank_right());
+      PHM_CHECK(cm.rl <= 128 && cm.rr <= 128, "coupling rank above 128 unsupported on device");
+      cm.mid_off = static_cast<std::int64_t>(mid.size());
+      cm.dims_off = static_cast<std::int32_t>(mdims.size());
+      int cur = 1;
+      for (int q = 0; q < c.d_theta; ++q) {
+        const TTCore& g = c.tt.cores[c.d + q];
+        mdims.push_back(static_cast<std::int32_t>(g.r0));
+        mdims.push_back(static_cast<std::int32_t>(g.m));
+        mdims.push_back(static_cast<std::int32_t>(g.r1));
+        mid.insert(mid.end(), g.data.begin(), g.data.end());
+        if (q == 0) maxA = std::max<int>(maxA, static_cast<int>(g.r0 * g.r1));
+        else {
+          maxB = std::max<int>(maxB, static_cast<int>(g.r0 * g.r1));
+          maxs1 = std::max<int>(maxs1, static_cast<int>(g.r1));
+        }
+        cur = static_cast<int>(g.r1);
+      }
+      (void)cur;
+      maxA = std::max(maxA, cm.rl * cm.rr);
+      maxrl = std::max(maxrl, cm.rl);
+      cm.h_off = hoff;
+      hoff += static_cast<std::int64_t>(cm.rl) * cm.rr;
+      if (M.h2) {
+        cm.l_off = static_cast<std::int64_t>(L.size());
+        cm.r_off = static_cast<std::int64_t>(R.size());
+        L.insert(L.end(), H.class_l[k].a.begin(), H.class_l[k].a.end());
+        R.insert(R.end(), H.class_r[k].a.begin(), H.class_r[k].a.end());
+        cm.c_off = static_cast<std::int64_t>(k) * M.P * M.P;
+      }
+      M.cmeta_h.push_back(cm);
+    }
+    // A needs rl x (running r) for every step of the chain
+    M.capA = std::max(maxA, maxrl * maxs1);
+    M.capB = maxB;
+    M.capT = std::max(maxrl * 32, maxrl * maxs1);
+    PHM_CHECK((M.capA + M.capB + M.capT) * 8 <= 227 * 1024, "class instantiate shared memory over 227 KB");
+    M.H_len = hoff;
+    M.C_len = M.h2 ? static_cast<std::int64_t>(M.ncls) * M.P * M.P : 0;
+    upload(M.cmeta, M.cmeta_h, st);
+    upload(M.class_mid, mid, st);
+    upload(M.class_mid_dims, mdims, st);
+    upload(M.class_L, L, st);
+    upload(M.class_R, R, st);
+  }
+  if (M.h2) {
+    // coupling CSR by sigma node (local far blocks, list order inside sigma)
+    std::vector<std::vector<Index>> by_sigma(M.nnodes);
+    for (Index i = 0; i < static_cast<Index>(H.blocks.far.size()); ++i)
+      if (H.far_local[i]) by_sigma[H.blocks.far[i].sigma].push_back(i);
+    std::vector<std::int32_t> sig, tau, cls;
+    std::vector<std::int64_t> beg{0};
+    for (int s = 0; s < M.nnodes; ++s) {
+      if (by_sigma[s].empty()) continue;
+      sig.push_back(s);
+      for (Index i : by_sigma[s]) {
+        tau.push_back(H.blocks.far[i].tau);
+        cls.push_back(H.far_key[i]);
+      }
+      beg.push_back(static_cast<std::int64_t>(tau.size()));
+    }
+    M.n_cp_sig = static_cast<int>(sig.size());
+    upload(M.cp_sig, sig, st);
+    upload(M.cp_beg, beg, st);
+    upload(M.cp_tau, tau, st);
+    upload(M.cp_cls, cls, st);
+    // basis: leaf factors [k][pos][j] for all points, transfers per node
+    std::vector<double> u(static_cast<size_t>(d) * n * M.ps, 0.0);
+    std::vector<std::int32_t> lall, lloc;
+    for (int id = 0; id < M.nnodes; ++id) {
+      const TreeNode& nd = T.nodes[id];
+      if (!nd.leaf() || nd.count == 0) continue;
+      lall.push_back(id);
+      if (H.node_local[id]) lloc.push_back(id);
+      std::vector<double> row(M.ps);
+      for (int k = 0; k < d; ++k) {
+        const Grid1D g = cheb_grid(nd.box.lo[k], nd.box.hi[k], M.ps);
+        for (Index i = 0; i < nd.count; ++i) {
+          lagrange_all(g, T.coord(T.perm[nd.begin + i], k), row.data());
+          for (int j = 0; j < M.ps; ++j) u[(static_cast<size_t>(k) * n + nd.begin + i) * M.ps + j] = row[j];
+        }
+      }
+    }
+    std::vector<double> e(static_cast<size_t>(M.nnodes) * d * M.ps * M.ps, 0.0);
+    for (int id = 1; id < M.nnodes; ++id) {
+      const TreeNode& ch = T.nodes[id];
+      const TreeNode& pa = T.nodes[ch.parent];
+      std::vector<double> row(M.ps);
+      for (int k = 0; k < d; ++k) {
+        const Grid1D pg = cheb_grid(pa.box.lo[k], pa.box.hi[k], M.ps);
+        const Grid1D cg = cheb_grid(ch.box.lo[k], ch.box.hi[k], M.ps);
+        for (int i = 0; i < M.ps; ++i) {  // E_k(i, j): parent cardinal j at child node i
+          lagrange_all(pg, cg.nodes[i], row.data());
+          for (int j = 0; j < M.ps; ++j) e[((static_cast<size_t>(id) * d + k) * M.ps + i) * M.ps + j] = row[j];
+        }
+      }
+    }
+    upload(M.U, u, st);
+    upload(M.Etr, e, st);
+    M.n_leaves_all = static_cast<int>(lall.size());
+    M.n_leaves_local = static_cast<int>(lloc.size());
+    upload(M.leaves_all, lall, st);
+    upload(M.leaves_local, lloc, st);
+    // level lists: upward = internal non-empty nodes per level (all);
+    // downward = non-empty local non-root nodes per level
+    std::vector<std::int32_t> upn, dnn;
+    M.up_range.assign(T.l_max + 1, {0, 0});
+    M.down_range.assign(T.l_max + 1, {0, 0});
+    for (int l = 0; l <= T.l_max; ++l) {
+      M.up_range[l].first = static_cast<int>(upn.size());
+      M.down_range[l].first = static_cast<int>(dnn.size());
+      for (int id = 0; id < M.nnodes; ++id) {
+        const TreeNode& nd = T.nodes[id];
+        if (nd.level != l || nd.count == 0) continue;
+        if (!nd.leaf()) upn.push_back(id);
+        if (nd.parent >= 0 && H.node_local[id]) dnn.push_back(id);
+      }
+      M.up_range[l].second = static_cast<int>(upn.size());
+      M.down_range[l].second = static_cast<int>(dnn.size());
+    }
+    upload(M.up_nodes, upn, st);
+    upload(M.down_nodes, dnn, st);
+  } else {
+    // H form: far blocks grouped per level, CSR by sigma, S/T payloads
+    std::vector<dev::FarHItem> items;
+    std::vector<std::int64_t> tb, soff, toff;
+    std::vector<std::int32_t> tn, cls;
+    std::vector<double> S, Tm;
+    M.fh_level_range.assign(T.l_max + 1, {0, 0});
+    M.fh_level_maxrows.assign(T.l_max + 1, 0);
+    for (int l = 0; l <= T.l_max; ++l) {
+      std::map<int, std::vector<Index>> by_sigma;
+      for (Index i = 0; i < static_cast<Index>(H.blocks.far.size()); ++i)
+        if (H.far_local[i] && T.nodes[H.blocks.far[i].sigma].level == l) by_sigma[H.blocks.far[i].sigma].push_back(i);
+      M.fh_level_range[l].first = static_cast<int>(items.size());
+      for (auto& kv : by_sigma) {
+        const TreeNode& s = T.nodes[kv.first];
+        dev::FarHItem it{};
+        it.row0 = s.begin;
+        it.rows = static_cast<std::int32_t>(s.count);
+        it.bbeg = static_cast<std::int32_t>(tb.size());
+        for (Index i : kv.second) {
+          const TreeNode& u = T.nodes[H.blocks.far[i].tau];
+          tb.push_back(u.begin);
+          tn.push_back(static_cast<std::int32_t>(u.count));
+          cls.push_back(H.far_key[i]);
+          soff.push_back(static_cast<std::int64_t>(S.size()));
+          toff.push_back(static_cast<std::int64_t>(Tm.size()));
+          S.insert(S.end(), H.far_s[i].a.begin(), H.far_s[i].a.end());
+          Tm.insert(Tm.end(), H.far_t[i].a.begin(), H.far_t[i].a.end());
+        }
+        it.bend = static_cast<std::int32_t>(tb.size());
+        M.fh_level_maxrows[l] = std::max<int>(M.fh_level_maxrows[l], it.rows);
+        items.push_back(it);
+      }
+      M.fh_level_range[l].second = static_cast<int>(items.size());
+      PHM_CHECK((M.fh_level_maxrows[l] + 256) * 8 <= 200 * 1024, "H-form far block rows exceed shared memory");
+    }
+    upload(M.fh_items, items, st);
+    upload(M.fh_tb, tb, st);
+    upload(M.fh_tn, tn, st);
+    upload(M.fh_cls, cls, st);
+    upload(M.fh_soff, soff, st);
+    upload(M.fh_toff, toff, st);
+    upload(M.fh_S, S, st);
+    upload(M.fh_T, Tm, st);
+  }
+  CK(cudaStreamSynchronize(st));
+  {
+    std::int64_t bytes = 0;
+    for (const DBuf* b : {&M.perm, &M.pts, &M.G, &M.class_mid, &M.class_L, &M.class_R, &M.U, &M.Etr, &M.fh_S, &M.fh_T,
+                          &M.near_cores, &M.snap_tiles, &M.inst_tiles})
+      bytes += static_cast<std::int64_t>(b->bytes);
+    M.device_bytes = bytes;
+  }
+  H.stats.upload_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_up).count();
+  return Mp;
+}
+
+// ----------------------------------------------------------- instantiate
+namespace {
+
+void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCounters* counters) {
+  DevMatrix& M = *I.M;
+  const HostMatrix& H = *M.hm;
+  Context& ctx = *M.ctx;
+  CK(cudaSetDevice(ctx.device));
+  cudaStream_t st = ctx.stream;
+  // theta box check before any launch (farfield.cpp:23-24)
+  const auto v = parametric_vectors(H.grids, theta, n_theta);
+  I.theta.assign(theta, theta + n_theta);
+  const dev::ThetaV tv = make_theta_v(v);
+
+  // far: H_k (and C_k) per class
+  ctx.run("class_inst", [&] {
+    dev::launch_class_inst(st, M.cmeta.as<dev::ClassMeta>(), M.ncls, M.class_mid.as<double>(),
+                           M.class_mid_dims.as<std::int32_t>(), M.class_L.as<double>(), M.class_R.as<double>(), tv, M.P,
+                           M.h2, M.capA, M.capB, M.capT, I.H.as<double>(), I.C.as<double>());
+  });
+  // near
+  if (M.mode == NearMode::Snapshot) {
+    // w = v_shape (x) ... times the amplitude interpolant sum_j v_j s_j
+    dev::ThetaV shape = tv;
+    const KernelSpec& spec = H.cfg.spec;
+    shape.dt = spec.shape_params();
+    double amp = 1.0;
+    if (spec.amplitude) {
+      const auto& g = H.grids.grids[spec.shape_params()];
+      amp = 0.0;
+      for (int j = 0; j < g.p; ++j) amp += v[spec.shape_params()][j] * g.nodes[j];
+    }
+    ctx.run("near_w", [&] { dev::launch_set_vec(st, I.w.as<double>(), M.R_snap, shape, amp); });
+    ctx.run("near_inst", [&] {
+      dev::launch_inst_flat(st, M.G.as<double>(), M.E, M.R_snap, I.w.as<double>(), I.D.as<double>());
+    });
+  } else if (M.mode == NearMode::TT) {
+    ctx.run("near_w", [&] {
+      dev::launch_near_w(st, M.near_w_meta.as<dev::NearW>(), M.n_near_local, M.near_cores.as<double>(),
+                         M.near_core_dims.as<std::int32_t>(), tv, I.w.as<double>());
+    });
+    ctx.run("near_inst", [&] {
+      dev::launch_inst_tiles(st, M.inst_tiles.as<dev::InstTile>(), M.n_inst_tiles, M.G.as<double>(),
+                             I.w.as<double>(), I.D.as<double>());
+    });
+  } else {
+    // Direct: evaluate the kernel at theta for every near entry (counted)
+    std::vector<double> th(3, 1.0);
+    for (int k = 0; k < H.cfg.spec.shape_params(); ++k) th[k] = theta[k];
+    double amp = H.cfg.spec.amplitude ? theta[H.cfg.spec.shape_params()] : 1.0;
+    if (!I.w.p) I.w.alloc(3 * sizeof(double));
+    CK(cudaMemcpyAsync(I.w.p, th.data(), 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    ctx.run("near_direct", [&] {
+      dev::launch_snapshot(st, M.snap_tiles.as<dev::SnapTile>(), M.n_snap_tiles, M.geo.as<dev::BlockGeom>(),
+                           M.pts.as<double>(), M.n, M.d, H.cfg.spec.family, 1, I.w.as<double>(), amp, I.D.as<double>());
+    });
+    CK(cudaStreamSynchronize(st));  // th lives on this stack frame
+    if (counters) counters->online.add(static_cast<std::uint64_t>(M.E_raw));
+  }
+}
+
+}  // namespace
+
+std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const double* theta, int n_theta,
+                                         StageCounters* counters) {
+  if (!m->ctx) throw std::logic_error("instantiate: host-only matrix (built without a device)");
+  CK(cudaSetDevice(m->ctx->device));
+  // validate theta first so nothing is allocated for a bad call
+  (void)parametric_vectors(m->hm->grids, theta, n_theta);
+  auto I = std::make_shared<DevInstance>();
+  I->M = m;
+  {
+    std::lock_guard<std::mutex> lk(m->mu);
+    if (!m->pool_D.empty()) {
+      I->D = std::move(m->pool_D.back());
+      m->pool_D.pop_back();
+    }
+  }
+  if (I->D.bytes < static_cast<size_t>(m->E) * sizeof(double)) I->D.alloc(static_cast<size_t>(m->E) * sizeof(double));
+  I->H.alloc(static_cast<size_t>(std::max<std::int64_t>(m->H_len, 1)) * sizeof(double));
+  if (m->C_len) I->C.alloc(static_cast<size_t>(m->C_len) * sizeof(double));
+  const std::int64_t wl = m->mode == NearMode::Snapshot ? m->R_snap : m->w_len;
+  if (wl) I->w.alloc(static_cast<size_t>(wl) * sizeof(double));
+  run_instantiate(*I, theta, n_theta, counters);
+  return I;
+}
+
+void reinstantiate(DevInstance& inst, const double* theta, int n_theta, StageCounters* counters) {
+  run_instantiate(inst, theta, n_theta, counters);
+}
+const std::vector<double>& instance_theta(const DevInstance& inst) { return inst.theta; }
+void instance_sync(DevInstance& inst) { CK(cudaStreamSynchronize(inst.M->st())); }
+
+void instance_far_h(DevInstance& I, Index far_index, std::vector<double>& out, Index& rows, Index& cols) {
+  const DevMatrix& M = *I.M;
+  const HostMatrix& H = *M.hm;
+  if (far_index < 0 || far_index >= static_cast<Index>(H.blocks.far.size())) throw std::out_of_range("far index");
+  const dev::ClassMeta& cm = M.cmeta_h[H.far_key[far_index]];
+  rows = cm.rl;
+  cols = cm.rr;
+  out.resize(static_cast<size_t>(rows * cols));
+  CK(cudaMemcpyAsync(out.data(), I.H.as<double>() + cm.h_off, out.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                     M.st()));
+  CK(cudaStreamSynchronize(M.st()));
+}
+
+void instance_near_d(DevInstance& I, Index b, std::vector<double>& out) {
+  const DevMatrix& M = *I.M;
+  const HostMatrix& H = *M.hm;
+  if (b < 0 || b >= static_cast<Index>(H.blocks.near.size())) throw std::out_of_range("near index");
+  if (M.near_doff[b] < 0) throw std::out_of_range("near block not resident on this shard");
+  const Block blk = H.blocks.near[b];
+  const Index N = H.tree->nodes[blk.sigma].count * H.tree->nodes[blk.tau].count;
+  out.resize(static_cast<size_t>(N));
+  CK(cudaMemcpyAsync(out.data(), I.D.as<double>() + M.near_doff[b], N * sizeof(double), cudaMemcpyDeviceToHost,
+                     M.st()));
+  CK(cudaStreamSynchronize(M.st()));
+}
+
+void instance_class_c(DevInstance& I, Index k, std::vector<double>& out) {
+  const DevMatrix& M = *I.M;
+  if (!M.h2) throw std::invalid_argument("explicit C_k exists only for the H2 format");
+  if (k < 0 || k >= M.ncls) throw std::out_of_range("class index");
+  out.resize(static_cast<size_t>(M.P) * M.P);
+  CK(cudaMemcpyAsync(out.data(), I.C.as<double>() + k * static_cast<std::int64_t>(M.P) * M.P,
+                     out.size() * sizeof(double), cudaMemcpyDeviceToHost, M.st()));
+  CK(cudaStreamSynchronize(M.st()));
+}
+
+// ------------------------------------------------------------------ apply
+namespace {
+
+// Computes this shard's rows of y in tree order into M.yp (n x m layout;
+// only rows [row_begin, row_end) are defined) from xp (tree order).
+void apply_tree_order(DevInstance& I, Index m) {
+  DevMatrix& M = *I.M;
+  const HostMatrix& H = *M.hm;
+  Context& ctx = *M.ctx;
+  cudaStream_t st = ctx.stream;
+  const int P = M.P;
+  const int mm = static_cast<int>(m);
+  if (M.h2) {
+    ctx.run("leaf_fwd", [&] {
+      dev::launch_leaf_fwd(st, M.leaves_all.as<std::int32_t>(), M.n_leaves_all, M.node_begin.as<std::int64_t>(),
+                           M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, P, M.xp.as<double>(), mm,
+                           M.xhat.as<double>());
+    });
+    for (int l = H.tree->l_max - 1; l >= 0; --l) {
+      const auto r = M.up_range[l];
+      if (r.second == r.first) continue;
+      ctx.run("up", [&] {
+        dev::launch_up(st, M.up_nodes.as<std::int32_t>() + r.first, r.second - r.first,
+                       M.node_first_child.as<std::int32_t>(), M.node_count.as<std::int32_t>(), M.Etr.as<double>(), M.d,
+                       M.ps, P, mm, M.xhat.as<double>());
+      });
+    }
+    CK(cudaMemsetAsync(M.yhat.p, 0, sizeof(double) * M.nnodes * P * m, st));
+    ctx.run("coupling", [&] {
+      dev::launch_coupling(st, M.cp_sig.as<std::int32_t>(), M.n_cp_sig, M.cp_beg.as<std::int64_t>(),
+                           M.cp_tau.as<std::int32_t>(), M.cp_cls.as<std::int32_t>(), I.C.as<double>(), P, mm,
+                           M.xhat.as<double>(), M.yhat.as<double>());
+    });
+  }
+  if (M.n_row_items == 0) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
+  for (Index c = 0; c < m; ++c)
+    ctx.run("near_mvm", [&] {
+      dev::launch_near_mvm(st, M.row_items.as<dev::RowItem>(), M.n_row_items, M.nb_tb.as<std::int64_t>(),
+                           M.nb_tn.as<std::int32_t>(), M.nb_doff.as<std::int64_t>(), I.D.as<double>(),
+                           M.xp.as<double>() + c * M.n, M.yp.as<double>() + c * M.n);
+    });
+  if (M.h2) {
+    for (int l = 1; l <= H.tree->l_max; ++l) {
+      const auto r = M.down_range[l];
+      if (r.second == r.first) continue;
+      ctx.run("down", [&] {
+        dev::launch_down(st, M.down_nodes.as<std::int32_t>() + r.first, r.second - r.first,
+                         M.node_parent.as<std::int32_t>(), M.Etr.as<double>(), M.d, M.ps, P, mm, M.yhat.as<double>());
+      });
+    }
+    ctx.run("leaf_bwd", [&] {
+      dev::launch_leaf_bwd(st, M.leaves_local.as<std::int32_t>(), M.n_leaves_local, M.node_begin.as<std::int64_t>(),
+                           M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, P, M.yhat.as<double>(),
+                           mm, H.row_begin, H.row_end, M.yp.as<double>());
+    });
+  } else {
+    for (int l = 0; l <= H.tree->l_max; ++l) {
+      const auto r = M.fh_level_range[l];
+      if (r.second == r.first) continue;
+      for (Index c = 0; c < m; ++c)
+        ctx.run("far_h", [&] {
+          dev::launch_far_h(st, M.fh_items.as<dev::FarHItem>() + r.first, r.second - r.first, M.fh_level_maxrows[l],
+                            M.fh_tb.as<std::int64_t>(), M.fh_tn.as<std::int32_t>(), M.fh_cls.as<std::int32_t>(),
+                            M.fh_soff.as<std::int64_t>(), M.fh_toff.as<std::int64_t>(),
+                            M.cmeta.as<dev::ClassMeta>(), M.fh_S.as<double>(), M.fh_T.as<double>(),
+                            I.H.as<double>(), M.xp.as<double>() + c * M.n, H.row_begin, H.row_end,
+                            M.yp.as<double>() + c * M.n);
+        });
+    }
+  }
+}
+
+}  // namespace
+
+void apply_device(DevInstance& I, const double* x_dev, double* y_dev, Index m) {
+  DevMatrix& M = *I.M;
+  PHM_CHECK(m >= 1, "apply: m must be >= 1");
+  CK(cudaSetDevice(M.ctx->device));
+  ensure_workspace(M, m);
+  cudaStream_t st = M.st();
+  M.ctx->run("gather", [&] { dev::launch_gather(st, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
+  apply_tree_order(I, m);
+  M.ctx->run("scatter", [&] { dev::launch_scatter(st, M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev); });
+}
+
+void apply_host(DevInstance& I, const double* x, double* y, Index m) {
+  DevMatrix& M = *I.M;
+  const HostMatrix& H = *M.hm;
+  if (H.row_begin != 0 || H.row_end != M.n)
+    throw std::logic_error("apply on a row shard: use the sharded apply and gather y across ranks");
+  CK(cudaSetDevice(M.ctx->device));
+  ensure_workspace(M, m);
+  cudaStream_t st = M.st();
+  CK(cudaMemcpyAsync(M.xdev.p, x, sizeof(double) * M.n * m, cudaMemcpyHostToDevice, st));
+  apply_device(I, M.xdev.as<double>(), M.ydev.as<double>(), m);
+  CK(cudaMemcpyAsync(y, M.ydev.p, sizeof(double) * M.n * m, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+void apply_device_rows(DevInstance& I, const double* x_dev, double* yrows_dev, Index m) {
+  DevMatrix& M = *I.M;
+  const HostMatrix& H = *M.hm;
+  CK(cudaSetDevice(M.ctx->device));
+  ensure_workspace(M, m);
+  cudaStream_t st = M.st();
+  M.ctx->run("gather", [&] { dev::launch_gather(st, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
+  apply_tree_order(I, m);
+  const Index rows = H.row_end - H.row_begin;
+  if (rows > 0)
+    CK(cudaMemcpy2DAsync(yrows_dev, rows * sizeof(double), M.yp.as<double>() + H.row_begin, M.n * sizeof(double),
+                         rows * sizeof(double), m, cudaMemcpyDeviceToDevice, st));
+}
+
+void unpermute_device(DevMatrix& M, const double* yperm_dev, double* y_dev, Index mcols) {
+  CK(cudaSetDevice(M.ctx->device));
+  M.ctx->run("scatter", [&] {
+    dev::launch_scatter(M.st(), yperm_dev, M.perm.as<std::int32_t>(), M.n, mcols, y_dev);
+  });
+}
+
+}  // namespace phm

@@ -1,0 +1,70 @@
+// Engine interface between the C ABI (capi.cpp) and the CUDA layer
+// (device.cu). Plain C++: no CUDA types cross this header.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host/phm.hpp"
+
+namespace phm {
+
+struct Context;     // device, stream, timers
+struct DevMatrix;   // parametric matrix resident on the GPU
+struct DevInstance; // matrix instantiated at one theta
+
+std::shared_ptr<Context> context_create(int device);
+void context_set_stream(Context& ctx, void* stream);  // nullptr = own stream
+void* context_stream(Context& ctx);
+void context_sync(Context& ctx);
+void context_enable_timing(Context& ctx, bool on);
+// Sum of CUDA-event durations (ms) and launch count of the named kernel
+// recorded since the last reset (synchronises the stream).
+void context_timer(Context& ctx, const std::string& name, double* ms, std::int64_t* count);
+void context_reset_timers(Context& ctx);
+std::int64_t context_launches(Context& ctx);  // kernels launched so far
+
+// Offline build: host structure + TT-cross (host), upload, and for
+// NearMode::Snapshot the GPU snapshot generator (K11).
+std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const double* points, Index n, int d,
+                                        const Config& cfg);
+// Host-only build: structure and offline TT data, no device (CPU tests).
+std::shared_ptr<DevMatrix> matrix_build_host_only(const double* points, Index n, int d, const Config& cfg);
+bool matrix_on_device(const DevMatrix& m);
+const HostMatrix& matrix_host(const DevMatrix& m);
+// Near payload actually resident on the device (bytes), and per-near-block
+// rank R_b (0 for non-local blocks).
+std::int64_t matrix_device_bytes(const DevMatrix& m);
+std::int64_t matrix_near_rank(const DevMatrix& m, Index near_block);
+// Device -> host copy of one snapshot / G1 column kap of a near block.
+void matrix_near_column(const DevMatrix& m, Index near_block, Index kap, double* out);
+// Sum over local near blocks of n_sigma n_tau (R_b + 1): the instantiate
+// stream's algorithmic element count (x8 bytes); and sum of n_sigma n_tau.
+std::int64_t matrix_near_elems(const DevMatrix& m, bool with_rank);
+
+std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const double* theta, int n_theta,
+                                         StageCounters* counters);
+// Re-instantiate in place at a new theta (reuses the device buffers).
+void reinstantiate(DevInstance& inst, const double* theta, int n_theta, StageCounters* counters);
+const std::vector<double>& instance_theta(const DevInstance& inst);
+void instance_sync(DevInstance& inst);
+
+// H_b(theta) of far block i (rows x cols, column-major), D_b of near block b
+// (n_sigma x n_tau column-major), explicit C_k of class k (P x P).
+void instance_far_h(DevInstance& inst, Index far_index, std::vector<double>& out, Index& rows, Index& cols);
+void instance_near_d(DevInstance& inst, Index near_index, std::vector<double>& out);
+void instance_class_c(DevInstance& inst, Index cls, std::vector<double>& out);
+
+// y = K(theta) x for m right-hand sides (column-major n x m), original point
+// order. Host variants copy in/out and synchronise; device variants are
+// asynchronous on the context stream.
+void apply_host(DevInstance& inst, const double* x, double* y, Index m);
+void apply_device(DevInstance& inst, const double* x_dev, double* y_dev, Index m);
+// Sharded pieces: rows [row_begin, row_end) of y in tree order, and the
+// final un-permute of a gathered tree-order vector.
+void apply_device_rows(DevInstance& inst, const double* x_dev, double* yrows_dev, Index m);
+void unpermute_device(DevMatrix& m, const double* yperm_dev, double* y_dev, Index mcols);
+
+}  // namespace phm

@@ -1,0 +1,776 @@
+// sm_100a kernels (see kernels.cuh for the index). All arithmetic is fp64.
+// The instantiate (K1) and near-MVM (K6) kernels are HBM streams; everything
+// is laid out so each warp load instruction touches contiguous 256-512 B.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace phm {
+namespace dev {
+
+// ------------------------------------------------------------ helpers
+// sm_100 has 256-bit global loads/stores (LDG.E.NA.EFL2.256 / STG.E.256):
+// one instruction moves 4 doubles, halving LSU issue for the HBM streams.
+struct alignas(32) dbl4 {
+  double x, y, z, w;
+};
+__device__ __forceinline__ dbl4 ld_stream4(const double* p) {
+  dbl4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st4(double* p, const dbl4& v) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ double2 ld_stream2(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+
+// Radial profiles of kernels.cpp:49-78 plus gauss / matern32 / matern52.
+// The generic Matern (needs K_nu) is produced on the host instead.
+__device__ __forceinline__ double kernel_profile(int fam, double r, const double* th) {
+  const double l = th[0];
+  switch (fam) {
+    case 0: return exp(-r / l);
+    case 1: {
+      if (r == 0.0) return 0.0;
+      const double s = r / l;
+      return s * s * log(s);
+    }
+    case 2: {
+      const double s = r / l;
+      return exp(-s * s);
+    }
+    case 3: {
+      const double s = r / l;
+      return sqrt(1.0 + s * s);
+    }
+    case 5: {
+      const double s = r / l;
+      return exp(-0.5 * s * s);
+    }
+    case 6: {
+      const double s = sqrt(3.0) * r / l;
+      return (1.0 + s) * exp(-s);
+    }
+    case 7: {
+      const double s = sqrt(5.0) * r / l;
+      return (1.0 + s + s * s / 3.0) * exp(-s);
+    }
+  }
+  return __longlong_as_double(0x7ff8000000000000LL);  // NaN: unsupported on device
+}
+
+// ---------------------------------------------------------------- K11
+// One thread per (i, j) entry: r_ij computed once (no FMA contraction, same
+// rounding as the reference's r2 accumulation, nearfield.cpp:38-45), then R
+// profile evaluations written to R slabs (coalesced across threads).
+__global__ void k_snapshot(const SnapTile* __restrict__ tiles, std::int64_t ntiles, const BlockGeom* __restrict__ geo,
+                           const double* __restrict__ pts, std::int64_t n, int d, int fam, int R,
+                           const double* __restrict__ theta_nodes, double amp, double* __restrict__ out) {
+  for (std::int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const SnapTile T = tiles[t];
+    const BlockGeom g = geo[T.blk];
+    for (int e = threadIdx.x; e < T.len; e += blockDim.x) {
+      const std::int64_t ee = T.e0 + e;
+      const std::int64_t i = ee % g.s_n, j = ee / g.s_n;
+      double r2 = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double dl = __dsub_rn(pts[k * n + g.s_begin + i], pts[k * n + g.t_begin + j]);
+        r2 = __dadd_rn(r2, __dmul_rn(dl, dl));
+      }
+      const double r = sqrt(r2);
+      for (int kap = 0; kap < R; ++kap)
+        out[T.out_off + kap * T.stride + e] = amp * kernel_profile(fam, r, theta_nodes + 3 * kap);
+    }
+  }
+}
+
+// ----------------------------------------------------------------- K1
+// Snapshot mode: every near block shares w = v(theta), so the instantiate is
+// one flat stream D[e] = sum_k w_k S[k E + e] over all local near entries
+// (E padded to a multiple of 4). Each thread issues U x R independent
+// 256-bit loads before it accumulates, which keeps enough bytes in flight
+// per SM to cover HBM latency.
+template <int R>
+__global__ void __launch_bounds__(256) k_inst_flat(const double* __restrict__ G, std::int64_t E,
+                                                   const double* __restrict__ w, double* __restrict__ D) {
+  constexpr int U = R >= 8 ? 1 : 2;
+  double wr[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) wr[k] = w[k];
+  const std::int64_t E4 = E >> 2;
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  std::int64_t q = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; q + (U - 1) * stride < E4; q += U * stride) {
+    dbl4 v[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < R; ++k) v[u][k] = ld_stream4(G + 4 * (E4 * k + q + u * stride));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      dbl4 acc = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        acc.x += v[u][k].x * wr[k];
+        acc.y += v[u][k].y * wr[k];
+        acc.z += v[u][k].z * wr[k];
+        acc.w += v[u][k].w * wr[k];
+      }
+      st4(D + 4 * (q + u * stride), acc);
+    }
+  }
+  for (; q < E4; q += stride) {
+    dbl4 acc = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const dbl4 v = ld_stream4(G + 4 * (E4 * k + q));
+      acc.x += v.x * wr[k];
+      acc.y += v.y * wr[k];
+      acc.z += v.z * wr[k];
+      acc.w += v.w * wr[k];
+    }
+    st4(D + 4 * q, acc);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_inst_flat_any(const double* __restrict__ G, std::int64_t E, int R,
+                                                       const double* __restrict__ w, double* __restrict__ D) {
+  const std::int64_t E4 = E >> 2;
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t q = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < E4; q += stride) {
+    dbl4 acc = {0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < R; ++k) {
+      const dbl4 v = ld_stream4(G + 4 * (E4 * k + q));
+      const double wk = w[k];
+      acc.x += v.x * wk;
+      acc.y += v.y * wk;
+      acc.z += v.z * wk;
+      acc.w += v.w * wk;
+    }
+    st4(D + 4 * q, acc);
+  }
+}
+
+// TT near mode: per-block G1_b (N_b x R_b, column-major, N_b padded to 4)
+// against the block's own w_b.
+__global__ void __launch_bounds__(256) k_inst_tiles(const InstTile* __restrict__ tiles, std::int64_t nt,
+                                                    const double* __restrict__ G, const double* __restrict__ w,
+                                                    double* __restrict__ D) {
+  for (std::int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
+    const InstTile T = tiles[t];
+    const double* Gb = G + T.g_off;
+    double* Db = D + T.d_off;
+    const double* wb = w + T.w_off;
+    for (int e = 4 * threadIdx.x; e < T.len; e += 4 * blockDim.x) {
+      dbl4 acc = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < T.R; ++k) {
+        const dbl4 v = ld_stream4(Gb + T.g_stride * k + e);
+        const double wk = wb[k];
+        acc.x += v.x * wk;
+        acc.y += v.y * wk;
+        acc.z += v.z * wk;
+        acc.w += v.w * wk;
+      }
+      st4(Db + e, acc);
+    }
+  }
+}
+
+// w_b = I * prod_i contract_mode2(G_{b,i+1}, v_i) (nearfield.cpp:71-77),
+// evaluated right to left as a vector chain; one warp per near block.
+__global__ void k_near_w(const NearW* __restrict__ meta, std::int64_t nb, const double* __restrict__ cores,
+                         const std::int32_t* __restrict__ dims, ThetaV tv, double* __restrict__ w) {
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  constexpr int kMaxR = 256;
+  double* za = sm + warp * 2 * kMaxR;
+  double* zb = za + kMaxR;
+  for (std::int64_t b = static_cast<std::int64_t>(blockIdx.x) * wpb + warp; b < nb;
+       b += static_cast<std::int64_t>(gridDim.x) * wpb) {
+    const NearW M = meta[b];
+    // z = [1] (the last core has r1 = 1)
+    if (lane == 0) za[0] = 1.0;
+    __syncwarp();
+    std::int64_t off = M.core_off;
+    // core offsets: walk forward to find each core start
+    std::int64_t offs[kMaxThetaDim];
+    for (int c = 0; c < M.ncores; ++c) {
+      offs[c] = off;
+      const std::int32_t* dm = dims + M.dims_off + 3 * c;
+      off += static_cast<std::int64_t>(dm[0]) * dm[1] * dm[2];
+    }
+    double* zin = za;
+    double* zout = zb;
+    for (int c = M.ncores - 1; c >= 0; --c) {
+      const std::int32_t* dm = dims + M.dims_off + 3 * c;
+      const int r0 = dm[0], m = dm[1], r1 = dm[2];
+      const double* G = cores + offs[c];
+      const double* v = tv.v[c];
+      for (int a = lane; a < r0; a += 32) {
+        double s = 0.0;
+        for (int j = 0; j < m; ++j) {
+          const double vj = v[j];
+          if (vj == 0.0) continue;
+          double t = 0.0;
+          for (int cc = 0; cc < r1; ++cc) t += G[a + j * r0 + cc * r0 * m] * zin[cc];
+          s += vj * t;
+        }
+        zout[a] = s;
+      }
+      __syncwarp();
+      double* tmp = zin;
+      zin = zout;
+      zout = tmp;
+    }
+    for (int a = lane; a < M.R; a += 32) w[M.w_off + a] = zin[a];
+    __syncwarp();
+  }
+}
+
+__global__ void k_set_vec(double* dst, int n, ThetaV tv) {
+  // dst = v_0 (x) v_1 (x) ... (first factor fastest), amplitude handled by caller
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int rem = i;
+  double s = 1.0;
+  for (int k = 0; k < tv.dt; ++k) {
+    s *= tv.v[k][rem % tv.p[k]];
+    rem /= tv.p[k];
+  }
+  dst[i] = s;
+}
+
+__global__ void k_scale(double* x, std::int64_t n, double a) {
+  const std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] *= a;
+}
+
+// ----------------------------------------------------------------- K2
+// One CTA per translation class. H = prod_i contract(G_{d+i}, v_i)
+// (farfield.cpp:149-155); for H^2 also C = L H R^T in 32-column tiles.
+__global__ void k_class_inst(const ClassMeta* __restrict__ meta, int ncls, const double* __restrict__ mid,
+                             const std::int32_t* __restrict__ mid_dims, const double* __restrict__ Lm,
+                             const double* __restrict__ Rm, ThetaV tv, int P, int want_c, int capA, int capB,
+                             double* __restrict__ H, double* __restrict__ C) {
+  extern __shared__ double sm[];
+  const ClassMeta M = meta[blockIdx.x];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int rl = M.rl, rr = M.rr;
+  double* A = sm;         // rl x r (running product)
+  double* B = A + capA;   // next contracted core
+  double* Tt = B + capB;  // rl x 32 tile of H R^T, or A B scratch
+  // first theta core
+  std::int64_t off = M.mid_off;
+  int r0 = mid_dims[M.dims_off + 0], m0 = mid_dims[M.dims_off + 1], r1 = mid_dims[M.dims_off + 2];
+  for (int e = tid; e < r0 * r1; e += nt) {
+    const int a = e % r0, c = e / r0;
+    double s = 0.0;
+    for (int j = 0; j < m0; ++j) {
+      const double vj = tv.v[0][j];
+      if (vj != 0.0) s += vj * mid[off + a + j * r0 + static_cast<std::int64_t>(c) * r0 * m0];
+    }
+    A[e] = s;
+  }
+  off += static_cast<std::int64_t>(r0) * m0 * r1;
+  for (int q = 1; q < tv.dt; ++q) {
+    const int s0 = mid_dims[M.dims_off + 3 * q], sm_ = mid_dims[M.dims_off + 3 * q + 1],
+              s1 = mid_dims[M.dims_off + 3 * q + 2];
+    __syncthreads();
+    for (int e = tid; e < s0 * s1; e += nt) {
+      const int a = e % s0, c = e / s0;
+      double s = 0.0;
+      for (int j = 0; j < sm_; ++j) {
+        const double vj = tv.v[q][j];
+        if (vj != 0.0) s += vj * mid[off + a + j * s0 + static_cast<std::int64_t>(c) * s0 * sm_];
+      }
+      B[e] = s;
+    }
+    off += static_cast<std::int64_t>(s0) * sm_ * s1;
+    __syncthreads();
+    // A <- A B  (rl x s1); use Tt region as scratch then copy back
+    for (int e = tid; e < rl * s1; e += nt) {
+      const int a = e % rl, c = e / rl;
+      double s = 0.0;
+      for (int k = 0; k < s0; ++k) s += A[a + k * rl] * B[k + c * s0];
+      Tt[e] = s;
+    }
+    __syncthreads();
+    for (int e = tid; e < rl * s1; e += nt) A[e] = Tt[e];
+  }
+  __syncthreads();
+  for (int e = tid; e < rl * rr; e += nt) H[M.h_off + e] = A[e];
+  if (!want_c) return;
+  for (int b0 = 0; b0 < P; b0 += 32) {
+    const int bw = min(32, P - b0);
+    __syncthreads();
+    for (int e = tid; e < rl * bw; e += nt) {  // Tt[i, bb] = sum_c H[i,c] R[b0+bb, c]
+      const int i = e % rl, bb = e / rl;
+      double s = 0.0;
+      for (int c = 0; c < rr; ++c) s += A[i + c * rl] * Rm[M.r_off + (b0 + bb) + static_cast<std::int64_t>(c) * P];
+      Tt[i + bb * rl] = s;
+    }
+    __syncthreads();
+    for (int e = tid; e < P * bw; e += nt) {  // C[a, b0+bb] = sum_i L[a,i] Tt[i,bb]
+      const int a = e % P, bb = e / P;
+      double s = 0.0;
+      for (int i = 0; i < rl; ++i) s += Lm[M.l_off + a + static_cast<std::int64_t>(i) * P] * Tt[i + bb * rl];
+      C[M.c_off + a + static_cast<std::int64_t>(b0 + bb) * P] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K10
+__global__ void k_gather(const double* __restrict__ x, const std::int32_t* __restrict__ perm, std::int64_t n,
+                         std::int64_t m, double* __restrict__ xp) {
+  const std::int64_t t = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n * m) return;
+  const std::int64_t c = t / n, p = t % n;
+  xp[t] = x[c * n + perm[p]];
+}
+__global__ void k_scatter(const double* __restrict__ yp, const std::int32_t* __restrict__ perm, std::int64_t n,
+                          std::int64_t m, double* __restrict__ y) {
+  const std::int64_t t = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n * m) return;
+  const std::int64_t c = t / n, p = t % n;
+  y[c * n + perm[p]] = yp[t];
+}
+
+// ----------------------------------------------------------------- K3
+// xhat_sigma[a] = sum_i x_i prod_k U_k(i, a_k) (chebyshev.cpp:236-252); one
+// CTA per non-empty leaf, factor rows staged in shared memory per 64 points.
+__global__ void k_leaf_fwd(const std::int32_t* __restrict__ leaves, const std::int64_t* __restrict__ begin,
+                           const std::int32_t* __restrict__ count, const double* __restrict__ U, std::int64_t n,
+                           int d, int ps, int P, const double* __restrict__ xp, int m, double* __restrict__ xhat) {
+  extern __shared__ double sm[];
+  const int leaf = leaves[blockIdx.x];
+  const std::int64_t b0 = begin[leaf];
+  const int cnt = count[leaf];
+  double* su = sm;                 // 64 x d x ps
+  double* sx = su + 64 * d * ps;   // 64
+  for (int c = 0; c < m; ++c) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};  // up to 4 outputs per thread (P <= 4 * blockDim)
+    for (int i0 = 0; i0 < cnt; i0 += 64) {
+      const int len = min(64, cnt - i0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < len * d * ps; e += blockDim.x) {
+        const int i = e / (d * ps), r = e % (d * ps), k = r / ps, j = r % ps;
+        su[e] = U[(static_cast<std::int64_t>(k) * n + b0 + i0 + i) * ps + j];
+      }
+      for (int e = threadIdx.x; e < len; e += blockDim.x) sx[e] = xp[static_cast<std::int64_t>(c) * n + b0 + i0 + e];
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int a = threadIdx.x + q * blockDim.x;
+        if (a >= P) break;
+        int dig[3];
+        int rem = a;
+        for (int k = 0; k < d; ++k) {
+          dig[k] = rem % ps;
+          rem /= ps;
+        }
+        double s = acc[q];
+        for (int i = 0; i < len; ++i) {
+          double f = sx[i];
+          for (int k = 0; k < d; ++k) f *= su[(i * d + k) * ps + dig[k]];
+          s += f;
+        }
+        acc[q] = s;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int a = threadIdx.x + q * blockDim.x;
+      if (a < P) xhat[(static_cast<std::int64_t>(leaf) * m + c) * P + a] = acc[q];
+    }
+  }
+}
+
+// ----------------------------------------------------------------- K4
+// xhat_p[a] = sum_children sum_b prod_k E_{c,k}(b_k, a_k) xhat_c[b]
+// (fast_kron_transposed, chebyshev.cpp:253-260). One CTA per parent.
+__global__ void k_up(const std::int32_t* __restrict__ nodes, const std::int32_t* __restrict__ first_child,
+                     const std::int32_t* __restrict__ count, const double* __restrict__ E, int d, int ps, int P,
+                     int nc, int m, double* __restrict__ xhat) {
+  extern __shared__ double sm[];
+  const int p = nodes[blockIdx.x];
+  const int fc = first_child[p];
+  const int fsz = d * ps * ps;
+  double* se = sm;             // nc x d x ps x ps
+  double* sx = se + nc * fsz;  // nc x P
+  for (int e = threadIdx.x; e < nc * fsz; e += blockDim.x) se[e] = E[static_cast<std::int64_t>(fc) * fsz + e];
+  for (int c = 0; c < m; ++c) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < nc * P; e += blockDim.x) {
+      const int ch = e / P, b = e % P;
+      sx[e] = count[fc + ch] > 0 ? xhat[(static_cast<std::int64_t>(fc + ch) * m + c) * P + b] : 0.0;
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < P; a += blockDim.x) {
+      int da[3];
+      int rem = a;
+      for (int k = 0; k < d; ++k) {
+        da[k] = rem % ps;
+        rem /= ps;
+      }
+      double s = 0.0;
+      for (int ch = 0; ch < nc; ++ch) {
+        if (count[fc + ch] == 0) continue;
+        const double* ef = se + ch * fsz;
+        const double* xc = sx + ch * P;
+        for (int b = 0; b < P; ++b) {
+          int r2 = b;
+          double f = xc[b];
+          for (int k = 0; k < d; ++k) {
+            f *= ef[(k * ps + (r2 % ps)) * ps + da[k]];
+            r2 /= ps;
+          }
+          s += f;
+        }
+      }
+      xhat[(static_cast<std::int64_t>(p) * m + c) * P + a] = s;
+    }
+  }
+}
+
+// ----------------------------------------------------------------- K5
+// yhat_sigma = sum over the far blocks of sigma of C_k xhat_tau (CSR by
+// sigma, deterministic order, no atomics). One CTA per sigma node.
+__global__ void k_coupling(const std::int32_t* __restrict__ sig, const std::int64_t* __restrict__ fbeg,
+                           const std::int32_t* __restrict__ ftau, const std::int32_t* __restrict__ fcls,
+                           const double* __restrict__ C, int P, int m, const double* __restrict__ xhat,
+                           double* __restrict__ yhat) {
+  extern __shared__ double sm[];
+  const int s = sig[blockIdx.x];
+  const std::int64_t b0 = fbeg[blockIdx.x], b1 = fbeg[blockIdx.x + 1];
+  const std::int64_t PP = static_cast<std::int64_t>(P) * P;
+  for (int c = 0; c < m; ++c) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (std::int64_t b = b0; b < b1; ++b) {
+      const int tau = ftau[b];
+      const double* Ck = C + fcls[b] * PP;
+      __syncthreads();
+      for (int e = threadIdx.x; e < P; e += blockDim.x) sm[e] = xhat[(static_cast<std::int64_t>(tau) * m + c) * P + e];
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int a = threadIdx.x + q * blockDim.x;
+        if (a >= P) break;
+        double s = 0.0;
+        for (int j = 0; j < P; ++j) s += Ck[a + static_cast<std::int64_t>(j) * P] * sm[j];
+        acc[q] += s;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int a = threadIdx.x + q * blockDim.x;
+      if (a < P) yhat[(static_cast<std::int64_t>(s) * m + c) * P + a] = acc[q];
+    }
+  }
+}
+
+// ----------------------------------------------------------------- K6
+// y[rows] = sum over the near blocks of sigma of D_b x_tau. 8 warps split the
+// columns of each block; each lane owns rows lane + 32q (q < 4), so every
+// warp load reads 32 consecutive doubles of one column. Fixed reduction
+// order over warps: deterministic.
+__global__ void __launch_bounds__(256) k_near_mvm(const RowItem* __restrict__ items, const std::int64_t* __restrict__ tb,
+                                                  const std::int32_t* __restrict__ tn,
+                                                  const std::int64_t* __restrict__ doff, const double* __restrict__ D,
+                                                  const double* __restrict__ xp, double* __restrict__ yp) {
+  __shared__ double red[8][128];
+  const RowItem it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  bool live[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) live[q] = lane + 32 * q < it.rows;
+  for (int b = it.bbeg; b < it.bend; ++b) {
+    const double* Db = D + doff[b] + it.i0 + lane;
+    const double* xb = xp + tb[b];
+    const int ncol = tn[b];
+    const std::int64_t ld = it.ld;
+    int j = warp;
+    for (; j + 8 < ncol; j += 16) {
+      const double x0 = xb[j], x1 = xb[j + 8];
+      double v0[4], v1[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        v0[q] = live[q] ? ld_stream(Db + j * ld + 32 * q) : 0.0;
+        v1[q] = live[q] ? ld_stream(Db + (j + 8) * ld + 32 * q) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] += v0[q] * x0 + v1[q] * x1;
+    }
+    for (; j < ncol; j += 8) {
+      const double x0 = xb[j];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (live[q]) acc[q] += ld_stream(Db + j * ld + 32 * q) * x0;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) red[warp][lane + 32 * q] = acc[q];
+  __syncthreads();
+  if (threadIdx.x < it.rows) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+    yp[it.row0 + threadIdx.x] = s;
+  }
+}
+
+// ----------------------------------------------------------------- K7
+// yhat_child[b] += sum_a prod_k E_k(b_k, a_k) yhat_parent[a] (fast_kron,
+// chebyshev.cpp:286-295). One CTA per child node of the level.
+__global__ void k_down(const std::int32_t* __restrict__ nodes, const std::int32_t* __restrict__ parent,
+                       const double* __restrict__ E, int d, int ps, int P, int m, double* __restrict__ yhat) {
+  extern __shared__ double sm[];
+  const int ch = nodes[blockIdx.x];
+  const int p = parent[ch];
+  const int fsz = d * ps * ps;
+  double* se = sm;
+  double* sy = se + fsz;
+  for (int e = threadIdx.x; e < fsz; e += blockDim.x) se[e] = E[static_cast<std::int64_t>(ch) * fsz + e];
+  for (int c = 0; c < m; ++c) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < P; e += blockDim.x) sy[e] = yhat[(static_cast<std::int64_t>(p) * m + c) * P + e];
+    __syncthreads();
+    for (int b = threadIdx.x; b < P; b += blockDim.x) {
+      int db[3];
+      int rem = b;
+      for (int k = 0; k < d; ++k) {
+        db[k] = rem % ps;
+        rem /= ps;
+      }
+      double s = 0.0;
+      for (int a = 0; a < P; ++a) {
+        int r2 = a;
+        double f = sy[a];
+        for (int k = 0; k < d; ++k) {
+          f *= se[(k * ps + db[k]) * ps + (r2 % ps)];
+          r2 /= ps;
+        }
+        s += f;
+      }
+      yhat[(static_cast<std::int64_t>(ch) * m + c) * P + b] += s;
+    }
+  }
+}
+
+// y_i += sum_a prod_k U_k(i, a_k) yhat_sigma[a] (chebyshev.cpp:270-282).
+__global__ void k_leaf_bwd(const std::int32_t* __restrict__ leaves, const std::int64_t* __restrict__ begin,
+                           const std::int32_t* __restrict__ count, const double* __restrict__ U, std::int64_t n,
+                           int d, int ps, int P, const double* __restrict__ yhat, int m, std::int64_t row_lo,
+                           std::int64_t row_hi, double* __restrict__ yp) {
+  extern __shared__ double sm[];
+  const int leaf = leaves[blockIdx.x];
+  const std::int64_t b0 = begin[leaf];
+  const int cnt = count[leaf];
+  for (int c = 0; c < m; ++c) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < P; e += blockDim.x) sm[e] = yhat[(static_cast<std::int64_t>(leaf) * m + c) * P + e];
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const std::int64_t pos = b0 + i;
+      if (pos < row_lo || pos >= row_hi) continue;
+      // fold dimension by dimension: last dim first, like the reference
+      double f[3][16];
+      for (int k = 0; k < d; ++k)
+        for (int j = 0; j < ps; ++j) f[k][j] = U[(static_cast<std::int64_t>(k) * n + pos) * ps + j];
+      double s = 0.0;
+      for (int a = 0; a < P; ++a) {
+        int rem = a;
+        double g = sm[a];
+        for (int k = 0; k < d; ++k) {
+          g *= f[k][rem % ps];
+          rem /= ps;
+        }
+        s += g;
+      }
+      yp[static_cast<std::int64_t>(c) * n + pos] += s;
+    }
+  }
+}
+
+// ----------------------------------------------------------------- K8
+// H form: y_sigma += S_b (H_k (T_b^T x_tau)) for the far blocks of sigma at
+// one level (phmatrix.cpp:231-237). One CTA per sigma; rows clipped to the
+// local shard.
+__global__ void k_far_h(const FarHItem* __restrict__ items, const std::int64_t* __restrict__ tbeg,
+                        const std::int32_t* __restrict__ tcnt, const std::int32_t* __restrict__ cls,
+                        const std::int64_t* __restrict__ s_off, const std::int64_t* __restrict__ t_off,
+                        const ClassMeta* __restrict__ meta, const double* __restrict__ S, const double* __restrict__ T,
+                        const double* __restrict__ H, const double* __restrict__ xp, std::int64_t row_lo,
+                        std::int64_t row_hi, double* __restrict__ yp) {
+  extern __shared__ double sm[];
+  const FarHItem it = items[blockIdx.x];
+  double* acc = sm;               // rows
+  double* tv = acc + it.rows;     // <= 128
+  double* uv = tv + 128;          // <= 128
+  for (int i = threadIdx.x; i < it.rows; i += blockDim.x) acc[i] = 0.0;
+  for (int b = it.bbeg; b < it.bend; ++b) {
+    const ClassMeta M = meta[cls[b]];
+    const int rl = M.rl, rr = M.rr, nt = tcnt[b];
+    const double* Tb = T + t_off[b];
+    const double* Sb = S + s_off[b];
+    const double* xb = xp + tbeg[b];
+    __syncthreads();
+    for (int c = threadIdx.x; c < rr; c += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < nt; ++j) s += Tb[j + static_cast<std::int64_t>(c) * nt] * xb[j];
+      tv[c] = s;
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < rl; a += blockDim.x) {
+      double s = 0.0;
+      for (int c = 0; c < rr; ++c) s += H[M.h_off + a + static_cast<std::int64_t>(c) * rl] * tv[c];
+      uv[a] = s;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < it.rows; i += blockDim.x) {
+      double s = 0.0;
+      for (int a = 0; a < rl; ++a) s += Sb[i + static_cast<std::int64_t>(a) * it.rows] * uv[a];
+      acc[i] += s;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < it.rows; i += blockDim.x) {
+    const std::int64_t pos = it.row0 + i;
+    if (pos >= row_lo && pos < row_hi) yp[pos] += acc[i];
+  }
+}
+
+// ------------------------------------------------------------ launchers
+void launch_snapshot(cudaStream_t st, const SnapTile* tiles, std::int64_t ntiles, const BlockGeom* geo,
+                     const double* pts, std::int64_t n, int d, int fam, int R, const double* theta_nodes, double amp,
+                     double* out) {
+  const int grid = static_cast<int>(std::min<std::int64_t>(ntiles, 148 * 16));
+  if (grid > 0) k_snapshot<<<grid, 256, 0, st>>>(tiles, ntiles, geo, pts, n, d, fam, R, theta_nodes, amp, out);
+}
+
+void launch_inst_flat(cudaStream_t st, const double* G, std::int64_t E, int R, const double* w, double* D) {
+  const std::int64_t E4 = E / 4;
+  if (E4 == 0) return;
+  const int grid = static_cast<int>(std::min<std::int64_t>((E4 + 255) / 256, 148 * 8));
+  switch (R) {
+    case 1: k_inst_flat<1><<<grid, 256, 0, st>>>(G, E, w, D); break;
+    case 2: k_inst_flat<2><<<grid, 256, 0, st>>>(G, E, w, D); break;
+    case 4: k_inst_flat<4><<<grid, 256, 0, st>>>(G, E, w, D); break;
+    case 6: k_inst_flat<6><<<grid, 256, 0, st>>>(G, E, w, D); break;
+    case 8: k_inst_flat<8><<<grid, 256, 0, st>>>(G, E, w, D); break;
+    case 10: k_inst_flat<10><<<grid, 256, 0, st>>>(G, E, w, D); break;
+    case 12: k_inst_flat<12><<<grid, 256, 0, st>>>(G, E, w, D); break;
+    case 16: k_inst_flat<16><<<grid, 256, 0, st>>>(G, E, w, D); break;
+    default: k_inst_flat_any<<<grid, 256, 0, st>>>(G, E, R, w, D); break;
+  }
+}
+
+void launch_inst_tiles(cudaStream_t st, const InstTile* tiles, std::int64_t nt, const double* G, const double* w,
+                       double* D) {
+  const int grid = static_cast<int>(std::min<std::int64_t>(nt, 148 * 8));
+  if (grid > 0) k_inst_tiles<<<grid, 256, 0, st>>>(tiles, nt, G, w, D);
+}
+
+void launch_near_w(cudaStream_t st, const NearW* meta, std::int64_t nb, const double* cores, const std::int32_t* dims,
+                   const ThetaV& tv, double* w) {
+  if (nb == 0) return;
+  const int wpb = 8;
+  const int grid = static_cast<int>(std::min<std::int64_t>((nb + wpb - 1) / wpb, 148 * 16));
+  k_near_w<<<grid, 32 * wpb, wpb * 2 * 256 * sizeof(double), st>>>(meta, nb, cores, dims, tv, w);
+}
+
+void launch_set_vec(cudaStream_t st, double* dst, int n, const ThetaV& tv, double amp) {
+  k_set_vec<<<(n + 127) / 128, 128, 0, st>>>(dst, n, tv);
+  if (amp != 1.0) k_scale<<<(n + 127) / 128, 128, 0, st>>>(dst, n, amp);
+}
+
+void launch_class_inst(cudaStream_t st, const ClassMeta* meta, int ncls, const double* mid, const std::int32_t* dims,
+                       const double* L, const double* R, const ThetaV& tv, int P, bool want_c, int capA, int capB,
+                       int capT, double* H, double* C) {
+  if (ncls == 0) return;
+  const size_t smem = static_cast<size_t>(capA + capB + capT) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_class_inst, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  k_class_inst<<<ncls, 256, smem, st>>>(meta, ncls, mid, dims, L, R, tv, P, want_c ? 1 : 0, capA, capB, H, C);
+}
+
+void launch_gather(cudaStream_t st, const double* x, const std::int32_t* perm, std::int64_t n, std::int64_t m,
+                   double* xp) {
+  const std::int64_t t = n * m;
+  k_gather<<<static_cast<unsigned>((t + 255) / 256), 256, 0, st>>>(x, perm, n, m, xp);
+}
+void launch_scatter(cudaStream_t st, const double* yp, const std::int32_t* perm, std::int64_t n, std::int64_t m,
+                    double* y) {
+  const std::int64_t t = n * m;
+  k_scatter<<<static_cast<unsigned>((t + 255) / 256), 256, 0, st>>>(yp, perm, n, m, y);
+}
+
+static int threads_for(int P) { return P <= 64 ? 64 : (P <= 128 ? 128 : 256); }
+
+void launch_leaf_fwd(cudaStream_t st, const std::int32_t* leaves, int nleaves, const std::int64_t* begin,
+                     const std::int32_t* count, const double* U, std::int64_t n, int d, int ps, int P, const double* xp,
+                     int m, double* xhat) {
+  if (nleaves == 0) return;
+  const size_t smem = (64 * d * ps + 64) * sizeof(double);
+  k_leaf_fwd<<<nleaves, threads_for(P), smem, st>>>(leaves, begin, count, U, n, d, ps, P, xp, m, xhat);
+}
+void launch_up(cudaStream_t st, const std::int32_t* nodes, int cnt, const std::int32_t* first_child,
+               const std::int32_t* count, const double* E, int d, int ps, int P, int m, double* xhat) {
+  if (cnt == 0) return;
+  const int nc = 1 << d;
+  const size_t smem = (nc * d * ps * ps + nc * P) * sizeof(double);
+  k_up<<<cnt, threads_for(P), smem, st>>>(nodes, first_child, count, E, d, ps, P, nc, m, xhat);
+}
+void launch_coupling(cudaStream_t st, const std::int32_t* sig, int nsig, const std::int64_t* fbeg,
+                     const std::int32_t* ftau, const std::int32_t* fcls, const double* C, int P, int m,
+                     const double* xhat, double* yhat) {
+  if (nsig == 0) return;
+  k_coupling<<<nsig, threads_for(P), P * sizeof(double), st>>>(sig, fbeg, ftau, fcls, C, P, m, xhat, yhat);
+}
+void launch_near_mvm(cudaStream_t st, const RowItem* items, int nitems, const std::int64_t* tb, const std::int32_t* tn,
+                     const std::int64_t* doff, const double* D, const double* xp, double* yp) {
+  if (nitems == 0) return;
+  k_near_mvm<<<nitems, 256, 0, st>>>(items, tb, tn, doff, D, xp, yp);
+}
+void launch_down(cudaStream_t st, const std::int32_t* nodes, int cnt, const std::int32_t* parent, const double* E,
+                 int d, int ps, int P, int m, double* yhat) {
+  if (cnt == 0) return;
+  const size_t smem = (d * ps * ps + P) * sizeof(double);
+  k_down<<<cnt, threads_for(P), smem, st>>>(nodes, parent, E, d, ps, P, m, yhat);
+}
+void launch_leaf_bwd(cudaStream_t st, const std::int32_t* leaves, int nleaves, const std::int64_t* begin,
+                     const std::int32_t* count, const double* U, std::int64_t n, int d, int ps, int P,
+                     const double* yhat, int m, std::int64_t row_lo, std::int64_t row_hi, double* yp) {
+  if (nleaves == 0) return;
+  k_leaf_bwd<<<nleaves, 128, P * sizeof(double), st>>>(leaves, begin, count, U, n, d, ps, P, yhat, m, row_lo, row_hi,
+                                                        yp);
+}
+void launch_far_h(cudaStream_t st, const FarHItem* items, int nitems, int max_rows, const std::int64_t* tbeg,
+                  const std::int32_t* tcnt, const std::int32_t* cls, const std::int64_t* s_off,
+                  const std::int64_t* t_off, const ClassMeta* meta, const double* S, const double* T, const double* H,
+                  const double* xp, std::int64_t row_lo, std::int64_t row_hi, double* yp) {
+  if (nitems == 0) return;
+  const size_t smem = (max_rows + 256) * sizeof(double);
+  k_far_h<<<nitems, 128, smem, st>>>(items, tbeg, tcnt, cls, s_off, t_off, meta, S, T, H, xp, row_lo, row_hi, yp);
+}
+
+}  // namespace dev
+}  // namespace phm

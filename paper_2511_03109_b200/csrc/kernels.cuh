@@ -1,0 +1,72 @@
+// sm_100a kernels of the online stage (instantiate + MVM) and the offline
+// snapshot generator. Numbering follows SURVEY.md §2.1:
+//   K11 k_snapshot        near-field kernel snapshots at theta nodes (offline)
+//   K1  k_inst_flat       D = sum_k w_k S_k  (snapshot mode, flat HBM stream)
+//   K1  k_inst_tiles      D_b = G1_b w_b     (TT near mode, per-block tiles)
+//   --  k_near_w          w_b = prod_i contract(G_{b,i+1}, v_i) (TT mode)
+//   K2  k_class_inst      H_k(theta) and C_k = L_k H_k R_k^T per class
+//   K10 k_gather/k_scatter tree-order permutation of x / y
+//   K3  k_leaf_fwd        xhat_sigma = U_sigma^T x_sigma
+//   K4  k_up              xhat_parent += E^T xhat_child (one launch per level)
+//   K5  k_coupling        yhat_sigma += C_k xhat_tau (CSR by sigma)
+//   K6  k_near_mvm        y_sigma = sum_tau D_b x_tau (CSR by sigma, no atomics)
+//   K7  k_down/k_leaf_bwd yhat_child += E yhat_parent; y += U yhat
+//   K8  k_far_h           y_sigma += S_b H_k T_b^T x_tau (H form, per level)
+#pragma once
+
+#include <cstdint>
+
+namespace phm {
+namespace dev {
+
+constexpr int kMaxThetaDim = 3;
+constexpr int kMaxThetaNodes = 32;
+
+struct ThetaV {  // parametric vectors v_k(theta_k) (farfield.cpp:16-29), by value
+  double v[kMaxThetaDim][kMaxThetaNodes];
+  int p[kMaxThetaDim];
+  int dt;
+};
+
+struct BlockGeom {  // one near block in tree order
+  std::int64_t s_begin, t_begin;
+  std::int32_t s_n, t_n;
+};
+
+struct SnapTile {  // K11 tile: entries [e0, e0+len) of block blk
+  std::int64_t out_off;  // output offset of entry e0 in slab 0
+  std::int64_t stride;   // slab stride
+  std::int32_t e0, len, blk, pad;
+};
+
+struct InstTile {  // K1 (TT mode) tile, len even, offsets even
+  std::int64_t d_off, g_off, g_stride, w_off;
+  std::int32_t len, R;
+};
+
+struct NearW {  // theta-core chain of one TT near block
+  std::int64_t core_off;  // into near_cores
+  std::int64_t w_off;     // into w
+  std::int32_t dims_off;  // into near_core_dims (3 ints per core)
+  std::int32_t ncores;    // number of theta cores (= d_theta)
+  std::int32_t R;
+  std::int32_t pad;
+};
+
+struct ClassMeta {
+  std::int64_t mid_off, l_off, r_off, h_off, c_off;
+  std::int32_t rl, rr, dims_off, pad;  // dims_off into class_mid_dims (3 per theta core)
+};
+
+struct RowItem {  // K6 work item: up to 128 rows of one leaf sigma
+  std::int64_t row0;
+  std::int32_t rows, ld, i0, bbeg, bend, pad;
+};
+
+struct FarHItem {  // K8 work item: one sigma node at one level
+  std::int64_t row0;
+  std::int32_t rows, bbeg, bend, pad;
+};
+
+}  // namespace dev
+}  // namespace phm

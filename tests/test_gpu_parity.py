@@ -1,0 +1,209 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs and the same offline data.
+
+Tolerances are the north_star's (fp64): instantiated blocks D_b, H_k, C_k
+within 1e-12 relative Frobenius; MVM output within 1e-11 relative 2-norm.
+Relations follow the reference's tests (proj/tests/test_phmatrix.cpp,
+test_nearfield.cpp, test_farfield.cpp)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_BLOCK = 1e-12
+TOL_Y = 1e-11
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def _node_sizes(pm):
+    ints, _ = pm.nodes()
+    return ints[:, 3]
+
+
+def _build(ph, po, pts, cfg, fmt, mask=None):
+    pm = ph.offline_h2(pts, cfg) if fmt == ph.Format.H2 else ph.offline_h(pts, cfg)
+    om = po.from_product(pm, pts, snapshot_mask=mask)
+    return pm, om
+
+
+def _check_instance(ph, pm, om, theta, block_stride=1):
+    inst = ph.instantiate(pm, theta)
+    oi = om.instantiate(theta)
+    sizes = _node_sizes(pm)
+    near, far, key = pm.blocks()
+    worst = 0.0
+    for b in range(0, len(near), block_stride):
+        s, t = near[b]
+        shape = (sizes[s], sizes[t])
+        worst = max(worst, rel(inst.near_d(b, shape), oi.near(b, shape)))
+    assert worst <= TOL_BLOCK, f"near D_b rel err {worst:.3e}"
+    ncls = pm.info()["n_classes"]
+    wh = 0.0
+    for i in range(0, len(far), max(1, len(far) // 200)):
+        wh = max(wh, rel(inst.far_h(i), oi.class_h(key[i])))
+    assert wh <= TOL_BLOCK, f"far H rel err {wh:.3e}"
+    if pm.format == ph.Format.H2:
+        P = pm.info()["P"]
+        wc = 0.0
+        for k in range(0, ncls, max(1, ncls // 50)):
+            wc = max(wc, rel(inst.class_c(k), oi.class_c(k, P)))
+        assert wc <= TOL_BLOCK, f"C_k rel err {wc:.3e}"
+    return inst, oi
+
+
+@pytest.mark.parametrize("fam", ["e", "m32", "gauss"])
+def test_h2_snapshot_3d_matches_oracle(ph, po, fam):
+    pts = ph.generate_points(3000, 3, 0)
+    box = {"e": (0.05, 0.5), "m32": (0.05, 0.5), "gauss": (0.1, 1.0)}[fam]
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.from_id(fam), [box]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT, seed=0)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    for theta in ([box[0]], [0.5 * (box[0] + box[1]) + 0.0123], [box[1]]):
+        inst, oi = _check_instance(ph, pm, om, theta, block_stride=7)
+        x = ph.generate_normal(pts.shape[0], 11)
+        assert rel(inst.apply(x), oi.apply(x)) <= TOL_Y
+
+
+def test_snapshot_generation_matches_oracle(ph, po):
+    """K11 entries equal the reference's near_oracle (nearfield.cpp:35-46)."""
+    pts = ph.generate_points(1500, 3, 3)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    sizes = _node_sizes(pm)
+    near, _, _ = pm.blocks()
+    worst = 0.0
+    for b in range(0, len(near), 5):
+        s, t = near[b]
+        shape = (sizes[s], sizes[t])
+        assert pm.near_rank(b) == 8
+        for kap in (0, 3, 7):
+            g = pm.near_column(b, kap, shape).ravel(order="F")
+            o = om.near_snapshot_column(b, kap, shape[0] * shape[1])
+            worst = max(worst, np.max(np.abs(g - o) / np.maximum(np.abs(o), 1e-300)))
+    assert worst <= 1e-15, f"snapshot max rel err {worst:.3e}"
+
+
+def test_h_tt_mode_2d_c1_like(ph, po):
+    """BASELINE config 1 shape (param-H, Gaussian, p_s = 6, p_theta = 8), reduced n."""
+    pts = ph.generate_points(1024, 2, 0)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.GAUSS, [(0.1, 1.0)]), l_max=2, p_s=6, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.TT, seed=0)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H)
+    for theta in ([0.1], [0.3456], [1.0]):
+        inst, oi = _check_instance(ph, pm, om, theta)
+        x = ph.generate_normal(pts.shape[0], 2)
+        assert rel(inst.apply(x), oi.apply(x)) <= TOL_Y
+
+
+def test_h2_tt_mode_and_accuracy_vs_exact(ph, po):
+    """test_phmatrix.cpp:54-82: induced dense vs exact <= 10 eps ||K||_F."""
+    pts = ph.generate_points(512, 3, 42)
+    cfg = ph.PHConfig(spec=ph.KernelSpec.default(ph.Family.SE), l_max=2, p_s=6, p_theta=8, eps=1e-4, seed=1)
+    for fmt in (ph.Format.H, ph.Format.H2):
+        pm, om = _build(ph, po, pts, cfg, fmt)
+        rng = np.random.default_rng(9)
+        for _ in range(3):
+            theta = [rng.uniform(0.25, 1.0)]
+            inst, oi = _check_instance(ph, pm, om, theta)
+            exact = po.dense_kernel(pts, ph.Family.SE, theta)
+            dense = inst.to_dense()
+            assert np.linalg.norm(dense - exact) <= 10 * cfg.eps * np.linalg.norm(exact)
+            assert rel(dense, oi.to_dense()) <= TOL_Y
+
+
+def test_direct_near_mode(ph, po):
+    """test_phmatrix.cpp:173-192: direct mode charges one online eval per near entry."""
+    pts = ph.generate_points(256, 3, 23)
+    cfg = ph.PHConfig(spec=ph.KernelSpec.default(ph.Family.SE), l_max=1, p_s=4, p_theta=6, eps=1e-4, seed=1,
+                      near_mode=ph.NearMode.DIRECT)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H)
+    before = pm.info()["evals_online"]
+    inst, oi = _check_instance(ph, pm, om, [0.5])
+    near, _, _ = pm.blocks()
+    sizes = _node_sizes(pm)
+    entries = int(sum(sizes[s] * sizes[t] for s, t in near))
+    assert pm.info()["evals_online"] - before == entries
+    exact = po.dense_kernel(pts, ph.Family.SE, [0.5])
+    assert np.linalg.norm(inst.to_dense() - exact) <= 10 * cfg.eps * np.linalg.norm(exact)
+
+
+def test_mvm_relations(ph, po):
+    """Linearity, zero-in-zero-out, e_j extracts a column, determinism
+    (test_phmatrix.cpp:100-148, 194-216)."""
+    pts = ph.generate_points(2000, 3, 5)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    pm = ph.offline_h2(pts, cfg)
+    inst = ph.instantiate(pm, [0.21])
+    n = pts.shape[0]
+    rng = np.random.default_rng(4)
+    x, z = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    assert np.all(inst.apply(np.zeros(n)) == 0.0)
+    lhs = inst.apply(2 * x - 3 * z)
+    rhs = 2 * inst.apply(x) - 3 * inst.apply(z)
+    assert np.max(np.abs(lhs - rhs)) <= 1e-12 * np.max(np.abs(rhs)) + 1e-14
+    y1, y2 = inst.apply(x), inst.apply(x)
+    assert np.array_equal(y1, y2)  # bitwise deterministic
+    inst2 = ph.instantiate(pm, [0.21])
+    assert np.array_equal(inst2.apply(x), y1)
+    Y = inst.apply(np.eye(n)[:, [0, 100, n - 1]])
+    for c, j in enumerate([0, 100, n - 1]):
+        e = np.zeros(n)
+        e[j] = 1.0
+        assert np.max(np.abs(inst.apply(e) - Y[:, c])) <= 1e-13
+
+
+def test_multi_rhs_matches_column_loop(ph, po):
+    pts = ph.generate_points(2500, 3, 8)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.MATERN52, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    inst = ph.instantiate(pm, [0.3])
+    X = np.stack([ph.generate_normal(pts.shape[0], s) for s in range(5)], axis=1)
+    Y = inst.apply(X)
+    Yo = om.instantiate([0.3]).apply(X)
+    for c in range(X.shape[1]):
+        assert rel(Y[:, c], Yo[:, c]) <= TOL_Y
+        assert np.array_equal(Y[:, c], inst.apply(X[:, c]))
+
+
+def test_two_parameter_amplitude_kernel(ph, po):
+    """theta = (l, sigma^2) with an 8 x 6 tensor grid (BASELINE config 4 form)."""
+    pts = ph.generate_mixture_points(3000, 3, 16, 0.05, 0)
+    spec = ph.KernelSpec(ph.Family.MATERN52, [(0.05, 0.5), (0.5, 2.0)], amplitude=True)
+    cfg = ph.PHConfig(spec=spec, l_max=2, p_s=4, p_theta=[8, 6], eta=1.0, near_mode=ph.NearMode.SNAPSHOT)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    assert pm.near_rank(0) == 8  # sigma^2 enters linearly: rank-1 amplitude core
+    for theta in ([0.05, 0.5], [0.17, 1.3], [0.5, 2.0]):
+        inst, oi = _check_instance(ph, pm, om, theta, block_stride=11)
+        x = ph.generate_normal(pts.shape[0], 3)
+        assert rel(inst.apply(x), oi.apply(x)) <= TOL_Y
+
+
+def test_errors_map_to_reference_exceptions(ph):
+    pts = ph.generate_points(128, 2, 8)
+    cfg = ph.PHConfig(spec=ph.KernelSpec.default(ph.Family.SE), l_max=1, p_s=4, p_theta=5, eps=1e-4)
+    pm = ph.offline_h(pts, cfg)
+    with pytest.raises(ph.DomainError):
+        ph.instantiate(pm, [3.0])
+    inst = ph.instantiate(pm, [0.5])
+    with pytest.raises(ph.InvalidArgument):
+        inst.apply(np.zeros(129))
+
+
+def test_reinstantiate_in_place(ph, po):
+    pts = ph.generate_points(2000, 3, 1)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    pm = ph.offline_h2(pts, cfg)
+    a = ph.instantiate(pm, [0.4])
+    x = ph.generate_normal(2000, 9)
+    ya = a.apply(x)
+    b = ph.instantiate(pm, [0.1])
+    b.reinstantiate([0.4])
+    assert np.array_equal(b.apply(x), ya)
