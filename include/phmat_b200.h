@@ -182,6 +182,15 @@ int phm_to_dense(phm_instance inst, double* out, int64_t guard);
 int phm_generate_points(int64_t n, int d, uint64_t seed, double* out);
 int phm_generate_mixture_points(int64_t n, int d, int clusters, double sigma, uint64_t seed, double* out);
 int phm_generate_normal(int64_t n, uint64_t seed, double* out);
+/* Offline TT tooling on a dense tensor (first index fastest): TT-cross with
+ * the reference's options (tt.hpp:107-130, tt.cpp:269-480) and TT-rounding
+ * (tt.cpp:159-224; abs_budget < 0 selects the relative form with eps).
+ * Cores are written when cap >= *len; flags = {rank_capped, converged}. */
+int phm_tt_cross_dense(const double* tensor, const int64_t* dims, int ndims, double eps, int64_t r_max,
+                       uint64_t seed, int round_after, int32_t* ncores, int64_t* core_dims, double* core_data,
+                       int64_t cap, int64_t* len, uint64_t* evals, int32_t* flags, double* est);
+int phm_tt_round(int ncores_in, const int64_t* dims_in, const double* data_in, double eps, double abs_budget,
+                 int32_t* ncores, int64_t* dims, double* data, int64_t cap, int64_t* len);
 /* theta draws of run_experiment (harness.cpp:254-260), one parameter. */
 int phm_theta_draws(double lo, double hi, int64_t count, uint64_t seed, double* out);
 

@@ -134,6 +134,9 @@ SIGNATURES = {
     "phm_generate_mixture_points": ([C.c_int64, C.c_int, C.c_int, C.c_double, C.c_uint64, _DP], C.c_int),
     "phm_generate_normal": ([C.c_int64, C.c_uint64, _DP], C.c_int),
     "phm_theta_draws": ([C.c_double, C.c_double, C.c_int64, C.c_uint64, _DP], C.c_int),
+    "phm_tt_cross_dense": ([_DP, _I64P, C.c_int, C.c_double, C.c_int64, C.c_uint64, C.c_int, _I32P, _I64P, _DP,
+                            C.c_int64, _I64P, _U64P, _I32P, _DP], C.c_int),
+    "phm_tt_round": ([C.c_int, _I64P, _DP, C.c_double, C.c_double, _I32P, _I64P, _DP, C.c_int64, _I64P], C.c_int),
 }
 
 _lib = None
@@ -563,6 +566,60 @@ def generate_normal(n: int, seed: int) -> np.ndarray:
     out = np.empty(n, dtype=np.float64)
     _check(lib().phm_generate_normal(n, seed, _dp(out)))
     return out
+
+
+def _unpack_cores(nc, dims, data):
+    cores, off = [], 0
+    for r0, m, r1 in dims[: 3 * nc].reshape(-1, 3):
+        sz = int(r0 * m * r1)
+        cores.append(data[off: off + sz].reshape((int(r0), int(m), int(r1)), order="F").copy())
+        off += sz
+    return cores
+
+
+def tt_cross(tensor, eps=1e-5, r_max=120, seed=0, round_after=True):
+    """TT-cross of a dense tensor (first index fastest; pass a Fortran-ordered
+    array or any array whose F-order flattening is the tensor). Returns
+    (cores, info) with cores shaped (r0, m, r1)."""
+    t = np.asfortranarray(tensor, dtype=np.float64)
+    flat = np.ascontiguousarray(t.ravel(order="F"))
+    dims = np.array(t.shape, dtype=np.int64)
+    nc, ln, ev = C.c_int32(), C.c_int64(), C.c_uint64()
+    flags = np.zeros(2, dtype=np.int32)
+    est = C.c_double()
+    cd = np.zeros(3 * len(dims), dtype=np.int64)
+    args = (_dp(flat), dims.ctypes.data_as(_I64P), len(dims), eps, r_max, seed, 1 if round_after else 0,
+            C.byref(nc), cd.ctypes.data_as(_I64P))
+    _check(lib().phm_tt_cross_dense(*args, None, 0, C.byref(ln), C.byref(ev), flags.ctypes.data_as(_I32P),
+                                    C.byref(est)))
+    data = np.empty(ln.value, dtype=np.float64)
+    _check(lib().phm_tt_cross_dense(*args, _dp(data), ln.value, C.byref(ln), C.byref(ev),
+                                    flags.ctypes.data_as(_I32P), C.byref(est)))
+    return _unpack_cores(nc.value, cd, data), {"evals": ev.value, "rank_capped": bool(flags[0]),
+                                               "converged": bool(flags[1]), "est_rel_error": est.value}
+
+
+def tt_round(cores, eps=0.0, abs_budget=-1.0):
+    dims = np.array([c.shape for c in cores], dtype=np.int64).ravel()
+    data = np.ascontiguousarray(np.concatenate([np.asarray(c).ravel(order="F") for c in cores]))
+    nc, ln = C.c_int32(), C.c_int64()
+    od = np.zeros(3 * len(cores), dtype=np.int64)
+    _check(lib().phm_tt_round(len(cores), dims.ctypes.data_as(_I64P), _dp(data), eps, abs_budget, C.byref(nc),
+                              od.ctypes.data_as(_I64P), None, 0, C.byref(ln)))
+    out = np.empty(ln.value, dtype=np.float64)
+    _check(lib().phm_tt_round(len(cores), dims.ctypes.data_as(_I64P), _dp(data), eps, abs_budget, C.byref(nc),
+                              od.ctypes.data_as(_I64P), _dp(out), ln.value, C.byref(ln)))
+    return _unpack_cores(nc.value, od, out)
+
+
+def tt_full(cores) -> np.ndarray:
+    cur = np.asarray(cores[0]).reshape(-1, cores[0].shape[2], order="F")
+    dims = [cores[0].shape[1]]
+    for c in cores[1:]:
+        r0, m, r1 = c.shape
+        cur = (cur @ np.asarray(c).reshape(r0, m * r1, order="F")).reshape(-1, r1, order="F")
+        dims.append(m)
+    return cur.reshape(dims, order="F")
 
 
 def theta_draws(lo: float, hi: float, count: int, seed: int) -> np.ndarray:

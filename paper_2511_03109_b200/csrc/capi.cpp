@@ -605,6 +605,77 @@ int phm_generate_mixture_points(int64_t n, int d, int clusters, double sigma, ui
     phm::generate_mixture_points(n, d, clusters, sigma, seed, out);
   });
 }
+namespace {
+void export_tt(const phm::TTTensor& tt, int32_t* ncores, int64_t* dims, double* data, int64_t cap, int64_t* len) {
+  int64_t total = 0;
+  for (const auto& c : tt.cores) total += c.size();
+  if (len) *len = total;
+  if (ncores) *ncores = tt.order();
+  if (dims)
+    for (int i = 0; i < tt.order(); ++i) {
+      dims[3 * i] = tt.cores[i].r0;
+      dims[3 * i + 1] = tt.cores[i].m;
+      dims[3 * i + 2] = tt.cores[i].r1;
+    }
+  if (data && cap >= total) {
+    int64_t off = 0;
+    for (const auto& c : tt.cores) {
+      std::memcpy(data + off, c.data.data(), c.data.size() * sizeof(double));
+      off += c.size();
+    }
+  }
+}
+}  // namespace
+
+int phm_tt_cross_dense(const double* tensor, const int64_t* dims, int ndims, double eps, int64_t r_max,
+                       uint64_t seed, int round_after, int32_t* ncores, int64_t* core_dims, double* core_data,
+                       int64_t cap, int64_t* len, uint64_t* evals, int32_t* flags, double* est) {
+  return guarded([&] {
+    need(tensor, "tensor");
+    need(dims, "dims");
+    if (ndims < 1 || ndims > 16) throw std::invalid_argument("ndims must be 1..16");
+    phm::EntryFn f;
+    f.dims.assign(dims, dims + ndims);
+    std::vector<int64_t> strides(ndims, 1);
+    for (int k = 1; k < ndims; ++k) strides[k] = strides[k - 1] * dims[k - 1];
+    f.fn = [tensor, strides, ndims](const phm::Index* idx) {
+      int64_t o = 0;
+      for (int k = 0; k < ndims; ++k) o += idx[k] * strides[k];
+      return tensor[o];
+    };
+    phm::CrossOptions co;
+    co.eps = eps;
+    co.r_max = r_max;
+    co.seed = seed;
+    co.round_after = round_after != 0;
+    const phm::CrossResult r = phm::tt_cross(f, co);
+    export_tt(r.tt, ncores, core_dims, core_data, cap, len);
+    if (evals) *evals = r.evals;
+    if (flags) {
+      flags[0] = r.rank_capped ? 1 : 0;
+      flags[1] = r.converged ? 1 : 0;
+    }
+    if (est) *est = r.est_rel_error;
+  });
+}
+
+int phm_tt_round(int ncores_in, const int64_t* dims_in, const double* data_in, double eps, double abs_budget,
+                 int32_t* ncores, int64_t* dims, double* data, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    need(dims_in, "dims");
+    need(data_in, "data");
+    phm::TTTensor tt;
+    int64_t off = 0;
+    for (int i = 0; i < ncores_in; ++i) {
+      phm::TTCore c = phm::TTCore::zeros(dims_in[3 * i], dims_in[3 * i + 1], dims_in[3 * i + 2]);
+      std::memcpy(c.data.data(), data_in + off, c.data.size() * sizeof(double));
+      off += c.size();
+      tt.cores.push_back(std::move(c));
+    }
+    export_tt(phm::tt_round(tt, eps, abs_budget), ncores, dims, data, cap, len);
+  });
+}
+
 int phm_theta_draws(double lo, double hi, int64_t count, uint64_t seed, double* out) {
   return guarded([&] {
     need(out, "out");
