@@ -42,6 +42,11 @@ void launch_up(cudaStream_t, const std::int32_t*, int, const std::int32_t*, cons
                int, int, int, double*);
 void launch_coupling(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*,
                      const std::int32_t*, const double*, int, int, const double*, double*);
+bool coupling_mma_supported(int P);
+void launch_coupling_mma(cudaStream_t, const CouplingItem*, int, const std::int32_t*, const std::int32_t*,
+                         const double*, int, const double*, int, int, double*);
+void launch_coupling_reduce(cudaStream_t, const std::int32_t*, const std::int32_t*, int, const double*, int, int, int,
+                            double*);
 void launch_near_mvm(cudaStream_t, const RowItem*, int, const std::int64_t*, const std::int32_t*,
                      const std::int64_t*, const double*, const double*, double*);
 void launch_down(cudaStream_t, const std::int32_t*, int, const std::int32_t*, const double*, int, int, int, int,
@@ -237,6 +242,10 @@ struct DevMatrix {
   // H^2 coupling CSR by sigma node
   DBuf cp_sig, cp_beg, cp_tau, cp_cls;
   int n_cp_sig = 0;
+  // H^2 coupling, grouped DMMA path (P in {16, 32, 64, 128})
+  bool cp_mma = false;
+  DBuf cg_items, cg_cls, cg_tau, cg_grp_sigma, cg_grp_items, cg_partial;
+  int n_cg_items = 0, n_cg_groups = 0;
   // H form far CSR by level
   DBuf fh_items, fh_tb, fh_tn, fh_cls, fh_soff, fh_toff, fh_S, fh_T;
   std::vector<std::pair<int, int>> fh_level_range;  // [item begin, item end) per level
@@ -646,6 +655,59 @@ std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const doub
     upload(M.cp_beg, beg, st);
     upload(M.cp_tau, tau, st);
     upload(M.cp_cls, cls, st);
+    M.cp_mma = dev::coupling_mma_supported(M.P);
+    if (M.cp_mma) {
+      // Groups: sigma nodes of one level with the same child parity, in node
+      // id (Morton) order, 32 per group; classes of a group split into items.
+      constexpr int kSlots = dev::kGroupSlots;
+      constexpr int kItemClasses = 64;
+      std::map<std::pair<int, int>, std::vector<int>> by_lp;  // (level, parity) -> sigmas
+      for (int s = 0; s < M.nnodes; ++s) {
+        if (by_sigma[s].empty()) continue;
+        int parity = 0;
+        for (int k = 0; k < d; ++k) parity |= static_cast<int>(T.nodes[s].coords[k] & 1) << k;
+        by_lp[{T.nodes[s].level, parity}].push_back(s);
+      }
+      std::vector<std::int32_t> grp_sigma, grp_items{0}, item_cls, cls_tau;
+      std::vector<dev::CouplingItem> items;
+      for (auto& kv : by_lp) {
+        const auto& sigs = kv.second;
+        for (size_t g0 = 0; g0 < sigs.size(); g0 += kSlots) {
+          const int grp = static_cast<int>(grp_items.size()) - 1;
+          std::map<int, std::array<std::int32_t, kSlots>> table;
+          for (int slot = 0; slot < kSlots; ++slot) {
+            const size_t si = g0 + slot;
+            grp_sigma.push_back(si < sigs.size() ? sigs[si] : -1);
+            if (si >= sigs.size()) continue;
+            for (Index i : by_sigma[sigs[si]]) {
+              auto it = table.find(H.far_key[i]);
+              if (it == table.end()) {
+                std::array<std::int32_t, kSlots> row;
+                row.fill(-1);
+                it = table.emplace(H.far_key[i], row).first;
+              }
+              it->second[slot] = H.blocks.far[i].tau;
+            }
+          }
+          int e = static_cast<int>(item_cls.size());
+          for (auto& cr : table) {
+            item_cls.push_back(cr.first);
+            cls_tau.insert(cls_tau.end(), cr.second.begin(), cr.second.end());
+          }
+          const int e_end = static_cast<int>(item_cls.size());
+          for (; e < e_end; e += kItemClasses) items.push_back({grp, e, std::min(e + kItemClasses, e_end), 0});
+          grp_items.push_back(static_cast<std::int32_t>(items.size()));
+        }
+      }
+      M.n_cg_items = static_cast<int>(items.size());
+      M.n_cg_groups = static_cast<int>(grp_items.size()) - 1;
+      upload(M.cg_items, items, st);
+      upload(M.cg_cls, item_cls, st);
+      upload(M.cg_tau, cls_tau, st);
+      upload(M.cg_grp_sigma, grp_sigma, st);
+      upload(M.cg_grp_items, grp_items, st);
+      M.cg_partial.alloc(sizeof(double) * std::max(1, M.n_cg_items) * kSlots * M.P);
+    }
     // basis: leaf factors [k][pos][j] for all points, transfers per node
     std::vector<double> u(static_cast<size_t>(d) * n * M.ps, 0.0);
     std::vector<std::int32_t> lall, lloc;
@@ -916,11 +978,25 @@ void apply_tree_order(DevInstance& I, Index m) {
       });
     }
     CK(cudaMemsetAsync(M.yhat.p, 0, sizeof(double) * M.nnodes * P * m, st));
-    ctx.run("coupling", [&] {
-      dev::launch_coupling(st, M.cp_sig.as<std::int32_t>(), M.n_cp_sig, M.cp_beg.as<std::int64_t>(),
-                           M.cp_tau.as<std::int32_t>(), M.cp_cls.as<std::int32_t>(), I.C.as<double>(), P, mm,
-                           M.xhat.as<double>(), M.yhat.as<double>());
-    });
+    if (M.cp_mma) {
+      for (int c = 0; c < mm; ++c) {
+        ctx.run("coupling", [&] {
+          dev::launch_coupling_mma(st, M.cg_items.as<dev::CouplingItem>(), M.n_cg_items, M.cg_cls.as<std::int32_t>(),
+                                   M.cg_tau.as<std::int32_t>(), I.C.as<double>(), P, M.xhat.as<double>(), mm, c,
+                                   M.cg_partial.as<double>());
+        });
+        ctx.run("coupling_reduce", [&] {
+          dev::launch_coupling_reduce(st, M.cg_grp_sigma.as<std::int32_t>(), M.cg_grp_items.as<std::int32_t>(),
+                                      M.n_cg_groups, M.cg_partial.as<double>(), P, mm, c, M.yhat.as<double>());
+        });
+      }
+    } else {
+      ctx.run("coupling", [&] {
+        dev::launch_coupling(st, M.cp_sig.as<std::int32_t>(), M.n_cp_sig, M.cp_beg.as<std::int64_t>(),
+                             M.cp_tau.as<std::int32_t>(), M.cp_cls.as<std::int32_t>(), I.C.as<double>(), P, mm,
+                             M.xhat.as<double>(), M.yhat.as<double>());
+      });
+    }
   }
   if (M.n_row_items == 0) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
   for (Index c = 0; c < m; ++c)

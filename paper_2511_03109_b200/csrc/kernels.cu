@@ -483,6 +483,113 @@ __global__ void k_coupling(const std::int32_t* __restrict__ sig, const std::int6
   }
 }
 
+// K5, grouped fp64 tensor-core version. One CTA per (sigma group, class
+// range): for every class k of the range, C_k (P x P) times the 32 gathered
+// xhat_tau columns of the group (X_k, P x 32) on mma.sync.m16n8k4.f64
+// (DMMA; sm_100 has no tcgen05 f64 kind), accumulated in registers across
+// the classes. Warp w owns output rows [16w, 16w + 16); X_k is staged in
+// shared memory by cp.async, double-buffered against the MMAs of the
+// previous class. Per-item partial sums are reduced in a fixed order by
+// k_coupling_reduce: deterministic, no atomics.
+__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int sz = valid ? 16 : 0;  // src-size 0 zero-fills (missing partner)
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int P>
+__global__ void __launch_bounds__(P / 16 * 32) k_coupling_mma(const CouplingItem* __restrict__ items,
+                                                              const std::int32_t* __restrict__ item_cls,
+                                                              const std::int32_t* __restrict__ cls_tau,
+                                                              const double* __restrict__ C,
+                                                              const double* __restrict__ xhat, int m, int col,
+                                                              double* __restrict__ partial) {
+  constexpr int LD = P + 4;           // conflict-free B-fragment reads
+  constexpr int KS = P / 4;           // k-steps of the m16n8k4 MMA
+  constexpr int NT = kGroupSlots / 8; // n-tiles of 8 slots
+  extern __shared__ double smem[];    // 2 x [32][LD]
+  const CouplingItem it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t0 = lane & 3;
+  const int row0 = warp * 16;
+  double acc[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+
+  auto gather = [&](int e, int buf) {
+    double* X = smem + buf * kGroupSlots * LD;
+    const std::int32_t* taus = cls_tau + static_cast<std::int64_t>(e) * kGroupSlots;
+    for (int c = threadIdx.x; c < kGroupSlots * (P / 2); c += blockDim.x) {
+      const int slot = c / (P / 2), q = c % (P / 2);
+      const int tau = taus[slot];
+      const double* src = xhat + (static_cast<std::int64_t>(tau < 0 ? 0 : tau) * m + col) * P + 2 * q;
+      cp_async16(X + slot * LD + 2 * q, src, tau >= 0);
+    }
+    cp_async_commit();
+  };
+
+  const int e0 = it.e_begin;
+  if (e0 < it.e_end) gather(e0, 0);
+  for (int e = e0; e < it.e_end; ++e) {
+    const int buf = (e - e0) & 1;
+    if (e + 1 < it.e_end) {
+      gather(e + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* Ck = C + static_cast<std::int64_t>(item_cls[e]) * P * P;
+    const double* X = smem + buf * kGroupSlots * LD;
+    double a[KS][2];
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      const std::int64_t k = 4 * s + t0;
+      a[s][0] = __ldg(Ck + (row0 + g) + k * P);
+      a[s][1] = __ldg(Ck + (row0 + g + 8) + k * P);
+    }
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      const int k = 4 * s + t0;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) dmma_16x8x4(acc[j], a[s][0], a[s][1], X[(8 * j + g) * LD + k]);
+    }
+    __syncthreads();  // X[buf] is refilled two classes later
+  }
+  double* out = partial + static_cast<std::int64_t>(blockIdx.x) * kGroupSlots * P;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const int n0 = 8 * j + 2 * t0;
+    out[n0 * P + row0 + g] = acc[j][0];
+    out[(n0 + 1) * P + row0 + g] = acc[j][1];
+    out[n0 * P + row0 + g + 8] = acc[j][2];
+    out[(n0 + 1) * P + row0 + g + 8] = acc[j][3];
+  }
+}
+
+__global__ void k_coupling_reduce(const std::int32_t* __restrict__ grp_sigma, const std::int32_t* __restrict__ grp_items,
+                                  const double* __restrict__ partial, int P, int m, int col, double* __restrict__ yhat) {
+  const int grp = blockIdx.x;
+  const int ib = grp_items[grp], ie = grp_items[grp + 1];
+  for (int e = threadIdx.x; e < kGroupSlots * P; e += blockDim.x) {
+    const int slot = e / P, a = e % P;
+    const int sigma = grp_sigma[grp * kGroupSlots + slot];
+    if (sigma < 0) continue;
+    double s = 0.0;
+    for (int i = ib; i < ie; ++i) s += partial[static_cast<std::int64_t>(i) * kGroupSlots * P + e];
+    yhat[(static_cast<std::int64_t>(sigma) * m + col) * P + a] = s;
+  }
+}
+
 // ----------------------------------------------------------------- K6
 // y[rows] = sum over the near blocks of sigma of D_b x_tau. 8 warps split the
 // columns of each block; each lane owns rows lane + 32q (q < 4), so every
@@ -745,6 +852,39 @@ void launch_coupling(cudaStream_t st, const std::int32_t* sig, int nsig, const s
   if (nsig == 0) return;
   k_coupling<<<nsig, threads_for(P), P * sizeof(double), st>>>(sig, fbeg, ftau, fcls, C, P, m, xhat, yhat);
 }
+bool coupling_mma_supported(int P) { return P == 16 || P == 32 || P == 64 || P == 128; }
+
+void launch_coupling_mma(cudaStream_t st, const CouplingItem* items, int nitems, const std::int32_t* item_cls,
+                         const std::int32_t* cls_tau, const double* C, int P, const double* xhat, int m, int col,
+                         double* partial) {
+  if (nitems == 0) return;
+  const size_t smem = 2 * kGroupSlots * (P + 4) * sizeof(double);
+  switch (P) {
+#define PHM_CASE(PP)                                                                                     \
+  case PP: {                                                                                             \
+    static bool attr = false;                                                                            \
+    if (!attr) {                                                                                         \
+      cudaFuncSetAttribute(k_coupling_mma<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); \
+      attr = true;                                                                                       \
+    }                                                                                                    \
+    k_coupling_mma<PP><<<nitems, PP / 16 * 32, smem, st>>>(items, item_cls, cls_tau, C, xhat, m, col, partial); \
+    break;                                                                                               \
+  }
+    PHM_CASE(16)
+    PHM_CASE(32)
+    PHM_CASE(64)
+    PHM_CASE(128)
+#undef PHM_CASE
+    default: break;
+  }
+}
+
+void launch_coupling_reduce(cudaStream_t st, const std::int32_t* grp_sigma, const std::int32_t* grp_items, int ngroups,
+                            const double* partial, int P, int m, int col, double* yhat) {
+  if (ngroups == 0) return;
+  k_coupling_reduce<<<ngroups, 256, 0, st>>>(grp_sigma, grp_items, partial, P, m, col, yhat);
+}
+
 void launch_near_mvm(cudaStream_t st, const RowItem* items, int nitems, const std::int64_t* tb, const std::int32_t* tn,
                      const std::int64_t* doff, const double* D, const double* xp, double* yp) {
   if (nitems == 0) return;

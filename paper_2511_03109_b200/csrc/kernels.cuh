@@ -63,6 +63,15 @@ struct RowItem {  // K6 work item: up to 128 rows of one leaf sigma
   std::int32_t rows, ld, i0, bbeg, bend, pad;
 };
 
+// K5 (grouped DMMA): a group is up to 32 sigma nodes of one level with the
+// same child parity (so their far partners share translation classes); an
+// item is a contiguous range of that group's classes. cls_tau[e*32 + slot] is
+// the tau node of (sigma slot, class item_cls[e]) or -1.
+constexpr int kGroupSlots = 32;
+struct CouplingItem {
+  std::int32_t group, e_begin, e_end, pad;
+};
+
 struct FarHItem {  // K8 work item: one sigma node at one level
   std::int64_t row0;
   std::int32_t rows, bbeg, bend, pad;
