@@ -227,16 +227,10 @@ def run_ours(args):
     x_dev = x_host.cuda()
     y_dev = torch.empty(n, dtype=torch.float64, device="cuda")
     rows = info["row_end"] - info["row_begin"]
-    counts = None
     if world > 1:
-        cnt = torch.tensor([rows], dtype=torch.int64, device="cuda")
-        allc = [torch.zeros_like(cnt) for _ in range(world)]
-        dist.all_gather(allc, cnt)
-        counts = [int(v.item()) for v in allc]
-        maxr = max(counts)
-        yrows = torch.zeros(maxr, dtype=torch.float64, device="cuda")
-        gathered = torch.empty(world * maxr, dtype=torch.float64, device="cuda")
-        yperm = torch.empty(n, dtype=torch.float64, device="cuda")
+        from paper_2511_03109_b200.dist import RowGather, row_counts
+
+        rg = RowGather(row_counts(rows), 1, device="cuda")
     inst = ph.instantiate(pm, [thetas[0]])
 
     def step(s):
@@ -244,12 +238,8 @@ def run_ours(args):
         if world == 1:
             inst.apply_device(x_dev.data_ptr(), y_dev.data_ptr(), 1)
         else:
-            inst.apply_rows_device(x_dev.data_ptr(), yrows.data_ptr(), 1)
-            dist.all_gather_into_tensor(gathered, yrows)
-            off = 0
-            for r in range(world):  # padded all-gather -> contiguous tree order
-                yperm[off: off + counts[r]].copy_(gathered[r * maxr: r * maxr + counts[r]])
-                off += counts[r]
+            inst.apply_rows_device(x_dev.data_ptr(), rg.send.data_ptr(), 1)
+            yperm = rg.gather(rg.send)  # NCCL all-gather(v) of the row blocks
             ph.lib().phm_unpermute_device(pm._h, ph._P(yperm.data_ptr()), ph._P(y_dev.data_ptr()), 1)
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
