@@ -131,6 +131,9 @@ struct Context {
       cudaEventDestroy(r.b);
     }
     for (auto e : pool) cudaEventDestroy(e);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
+    if (side) cudaStreamDestroy(side);
     if (own) cudaStreamDestroy(own);
   }
   cudaEvent_t ev() {
@@ -146,6 +149,10 @@ struct Context {
   // Brackets one kernel launch with events on the launching stream.
   template <typename F>
   void run(const char* name, F&& f) {
+    run_on(stream, name, std::forward<F>(f));
+  }
+  template <typename F>
+  void run_on(cudaStream_t s, const char* name, F&& f) {
     ++launches;
     if (!timing) {
       f();
@@ -153,11 +160,23 @@ struct Context {
       return;
     }
     Rec r{name, ev(), ev()};
-    CK(cudaEventRecord(r.a, stream));
+    CK(cudaEventRecord(r.a, s));
     f();
     CK(cudaGetLastError());
-    CK(cudaEventRecord(r.b, stream));
+    CK(cudaEventRecord(r.b, s));
     recs.push_back(r);
+  }
+  // Second stream for the H^2 far-field chain, which overlaps the near-field
+  // GEMV (compute-bound DMMA next to an HBM stream); fork/join by events.
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  void fork() {
+    CK(cudaEventRecord(fork_ev, stream));
+    CK(cudaStreamWaitEvent(side, fork_ev, 0));
+  }
+  void join() {
+    CK(cudaEventRecord(join_ev, side));
+    CK(cudaStreamWaitEvent(stream, join_ev, 0));
   }
   void flush_timers() {
     if (recs.empty()) return;
@@ -187,6 +206,9 @@ std::shared_ptr<Context> context_create(int device) {
   auto ctx = std::make_shared<Context>();
   ctx->device = device;
   CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
   ctx->stream = ctx->own;
   return ctx;
 }
@@ -963,38 +985,50 @@ void apply_tree_order(DevInstance& I, Index m) {
   const int P = M.P;
   const int mm = static_cast<int>(m);
   if (M.h2) {
-    ctx.run("leaf_fwd", [&] {
-      dev::launch_leaf_fwd(st, M.leaves_all.as<std::int32_t>(), M.n_leaves_all, M.node_begin.as<std::int64_t>(),
+    // Far-field chain (forward, coupling, downward) on the side stream,
+    // concurrent with the near-field GEMV on the main stream.
+    ctx.fork();
+    cudaStream_t fs = ctx.side;
+    ctx.run_on(fs, "leaf_fwd", [&] {
+      dev::launch_leaf_fwd(fs, M.leaves_all.as<std::int32_t>(), M.n_leaves_all, M.node_begin.as<std::int64_t>(),
                            M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, P, M.xp.as<double>(), mm,
                            M.xhat.as<double>());
     });
     for (int l = H.tree->l_max - 1; l >= 0; --l) {
       const auto r = M.up_range[l];
       if (r.second == r.first) continue;
-      ctx.run("up", [&] {
-        dev::launch_up(st, M.up_nodes.as<std::int32_t>() + r.first, r.second - r.first,
+      ctx.run_on(fs, "up", [&] {
+        dev::launch_up(fs, M.up_nodes.as<std::int32_t>() + r.first, r.second - r.first,
                        M.node_first_child.as<std::int32_t>(), M.node_count.as<std::int32_t>(), M.Etr.as<double>(), M.d,
                        M.ps, P, mm, M.xhat.as<double>());
       });
     }
-    CK(cudaMemsetAsync(M.yhat.p, 0, sizeof(double) * M.nnodes * P * m, st));
+    CK(cudaMemsetAsync(M.yhat.p, 0, sizeof(double) * M.nnodes * P * m, fs));
     if (M.cp_mma) {
       for (int c = 0; c < mm; ++c) {
-        ctx.run("coupling", [&] {
-          dev::launch_coupling_mma(st, M.cg_items.as<dev::CouplingItem>(), M.n_cg_items, M.cg_cls.as<std::int32_t>(),
+        ctx.run_on(fs, "coupling", [&] {
+          dev::launch_coupling_mma(fs, M.cg_items.as<dev::CouplingItem>(), M.n_cg_items, M.cg_cls.as<std::int32_t>(),
                                    M.cg_tau.as<std::int32_t>(), I.C.as<double>(), P, M.xhat.as<double>(), mm, c,
                                    M.cg_partial.as<double>());
         });
-        ctx.run("coupling_reduce", [&] {
-          dev::launch_coupling_reduce(st, M.cg_grp_sigma.as<std::int32_t>(), M.cg_grp_items.as<std::int32_t>(),
+        ctx.run_on(fs, "coupling_reduce", [&] {
+          dev::launch_coupling_reduce(fs, M.cg_grp_sigma.as<std::int32_t>(), M.cg_grp_items.as<std::int32_t>(),
                                       M.n_cg_groups, M.cg_partial.as<double>(), P, mm, c, M.yhat.as<double>());
         });
       }
     } else {
-      ctx.run("coupling", [&] {
-        dev::launch_coupling(st, M.cp_sig.as<std::int32_t>(), M.n_cp_sig, M.cp_beg.as<std::int64_t>(),
+      ctx.run_on(fs, "coupling", [&] {
+        dev::launch_coupling(fs, M.cp_sig.as<std::int32_t>(), M.n_cp_sig, M.cp_beg.as<std::int64_t>(),
                              M.cp_tau.as<std::int32_t>(), M.cp_cls.as<std::int32_t>(), I.C.as<double>(), P, mm,
                              M.xhat.as<double>(), M.yhat.as<double>());
+      });
+    }
+    for (int l = 1; l <= H.tree->l_max; ++l) {
+      const auto r = M.down_range[l];
+      if (r.second == r.first) continue;
+      ctx.run_on(fs, "down", [&] {
+        dev::launch_down(fs, M.down_nodes.as<std::int32_t>() + r.first, r.second - r.first,
+                         M.node_parent.as<std::int32_t>(), M.Etr.as<double>(), M.d, M.ps, P, mm, M.yhat.as<double>());
       });
     }
   }
@@ -1006,14 +1040,7 @@ void apply_tree_order(DevInstance& I, Index m) {
                            M.xp.as<double>() + c * M.n, M.yp.as<double>() + c * M.n);
     });
   if (M.h2) {
-    for (int l = 1; l <= H.tree->l_max; ++l) {
-      const auto r = M.down_range[l];
-      if (r.second == r.first) continue;
-      ctx.run("down", [&] {
-        dev::launch_down(st, M.down_nodes.as<std::int32_t>() + r.first, r.second - r.first,
-                         M.node_parent.as<std::int32_t>(), M.Etr.as<double>(), M.d, M.ps, P, mm, M.yhat.as<double>());
-      });
-    }
+    ctx.join();
     ctx.run("leaf_bwd", [&] {
       dev::launch_leaf_bwd(st, M.leaves_local.as<std::int32_t>(), M.n_leaves_local, M.node_begin.as<std::int64_t>(),
                            M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, P, M.yhat.as<double>(),

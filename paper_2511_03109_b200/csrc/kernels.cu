@@ -762,6 +762,162 @@ __global__ void k_far_h(const FarHItem* __restrict__ items, const std::int64_t* 
   }
 }
 
+// ---------------------------------------------- K4 / K7, mode-wise versions
+// (A_d (x) ... (x) A_1)^(T) z as d sequential mode contractions in shared
+// memory (the fast_kron of chebyshev.cpp:152-193): d * P * ps FMAs per child
+// instead of P^2 * d.
+__device__ __forceinline__ void mode_round(const double* __restrict__ zin, double* __restrict__ zout,
+                                           const double* __restrict__ A, int ps, int P, int stride, bool transposed,
+                                           bool accumulate) {
+  for (int q = threadIdx.x; q < P; q += blockDim.x) {
+    const int bk = (q / stride) % ps;
+    const int base = q - bk * stride;
+    double s = 0.0;
+    for (int a = 0; a < ps; ++a) {
+      const double f = transposed ? A[a * ps + bk] : A[bk * ps + a];
+      s += f * zin[base + a * stride];
+    }
+    zout[q] = accumulate ? zout[q] + s : s;
+  }
+}
+
+// xhat_p = sum over non-empty children c of (E_{c,d} (x) ... (x) E_{c,1})^T xhat_c.
+__global__ void k_up2(const std::int32_t* __restrict__ nodes, const std::int32_t* __restrict__ first_child,
+                      const std::int32_t* __restrict__ count, const double* __restrict__ E, int d, int ps, int P,
+                      int nc, int m, double* __restrict__ xhat) {
+  extern __shared__ double sm[];
+  const int p = nodes[blockIdx.x];
+  const int fc = first_child[p];
+  const int fsz = d * ps * ps;
+  double* se = sm;               // d x ps x ps factors of the current child
+  double* za = se + fsz;         // ping
+  double* zb = za + P;           // pong
+  double* acc = zb + P;          // P
+  for (int c = 0; c < m; ++c) {
+    for (int e = threadIdx.x; e < P; e += blockDim.x) acc[e] = 0.0;
+    for (int ch = 0; ch < nc; ++ch) {
+      if (count[fc + ch] == 0) continue;
+      __syncthreads();
+      for (int e = threadIdx.x; e < fsz; e += blockDim.x) se[e] = E[static_cast<std::int64_t>(fc + ch) * fsz + e];
+      for (int e = threadIdx.x; e < P; e += blockDim.x)
+        za[e] = xhat[(static_cast<std::int64_t>(fc + ch) * m + c) * P + e];
+      __syncthreads();
+      double* in = za;
+      double* out = zb;
+      int stride = 1;
+      for (int k = 0; k < d; ++k) {
+        if (k == d - 1) {
+          mode_round(in, acc, se + k * ps * ps, ps, P, stride, true, true);
+        } else {
+          mode_round(in, out, se + k * ps * ps, ps, P, stride, true, false);
+          __syncthreads();
+          double* t = in;
+          in = out;
+          out = t;
+        }
+        stride *= ps;
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < P; e += blockDim.x) xhat[(static_cast<std::int64_t>(p) * m + c) * P + e] = acc[e];
+    __syncthreads();
+  }
+}
+
+// yhat_child += (E_d (x) ... (x) E_1) yhat_parent.
+__global__ void k_down2(const std::int32_t* __restrict__ nodes, const std::int32_t* __restrict__ parent,
+                        const double* __restrict__ E, int d, int ps, int P, int m, double* __restrict__ yhat) {
+  extern __shared__ double sm[];
+  const int ch = nodes[blockIdx.x];
+  const int p = parent[ch];
+  const int fsz = d * ps * ps;
+  double* se = sm;
+  double* za = se + fsz;
+  double* zb = za + P;
+  double* yc = zb + P;
+  for (int e = threadIdx.x; e < fsz; e += blockDim.x) se[e] = E[static_cast<std::int64_t>(ch) * fsz + e];
+  for (int c = 0; c < m; ++c) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < P; e += blockDim.x) {
+      za[e] = yhat[(static_cast<std::int64_t>(p) * m + c) * P + e];
+      yc[e] = yhat[(static_cast<std::int64_t>(ch) * m + c) * P + e];
+    }
+    __syncthreads();
+    double* in = za;
+    double* out = zb;
+    int stride = 1;
+    for (int k = 0; k < d; ++k) {
+      if (k == d - 1) {
+        mode_round(in, yc, se + k * ps * ps, ps, P, stride, false, true);
+      } else {
+        mode_round(in, out, se + k * ps * ps, ps, P, stride, false, false);
+        __syncthreads();
+        double* t = in;
+        in = out;
+        out = t;
+      }
+      stride *= ps;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < P; e += blockDim.x) yhat[(static_cast<std::int64_t>(ch) * m + c) * P + e] = yc[e];
+  }
+}
+
+// y_i += <kron row of point i, yhat> folded one dimension at a time, last
+// dimension first (chebyshev.cpp:270-282); one CTA per leaf, the partial
+// folds of all points of a 32-point chunk live in shared memory.
+__global__ void k_leaf_bwd2(const std::int32_t* __restrict__ leaves, const std::int64_t* __restrict__ begin,
+                            const std::int32_t* __restrict__ count, const double* __restrict__ U, std::int64_t n,
+                            int d, int ps, int P, const double* __restrict__ yhat, int m, std::int64_t row_lo,
+                            std::int64_t row_hi, double* __restrict__ yp) {
+  extern __shared__ double sm[];
+  constexpr int kChunk = 32;
+  const int leaf = leaves[blockIdx.x];
+  const std::int64_t b0 = begin[leaf];
+  const int cnt = count[leaf];
+  double* yh = sm;                 // P
+  double* ta = yh + P;             // kChunk x P/ps
+  double* tb = ta + kChunk * (P / ps);
+  for (int c = 0; c < m; ++c) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < P; e += blockDim.x) yh[e] = yhat[(static_cast<std::int64_t>(leaf) * m + c) * P + e];
+    __syncthreads();
+    for (int i0 = 0; i0 < cnt; i0 += kChunk) {
+      const int len = min(kChunk, cnt - i0);
+      const double* in = yh;
+      int inlen = P;   // per-point length (shared yh has no point stride)
+      bool shared_in = true;
+      double* out = ta;
+      for (int k = d - 1; k >= 1; --k) {
+        const int olen = inlen / ps;
+        for (int e = threadIdx.x; e < len * olen; e += blockDim.x) {
+          const int i = e / olen, q = e % olen;
+          const std::int64_t pos = b0 + i0 + i;
+          const double* u = U + (static_cast<std::int64_t>(k) * n + pos) * ps;
+          const double* z = shared_in ? in : in + i * inlen;
+          double s = 0.0;
+          for (int a = 0; a < ps; ++a) s += z[q + a * olen] * u[a];
+          out[i * olen + q] = s;
+        }
+        __syncthreads();
+        in = out;
+        out = (out == ta) ? tb : ta;
+        inlen = olen;
+        shared_in = false;
+      }
+      for (int i = threadIdx.x; i < len; i += blockDim.x) {
+        const std::int64_t pos = b0 + i0 + i;
+        const double* u = U + pos * ps;  // dimension 0
+        const double* z = shared_in ? in : in + i * inlen;
+        double s = 0.0;
+        for (int a = 0; a < ps; ++a) s += u[a] * z[a];
+        if (pos >= row_lo && pos < row_hi) yp[static_cast<std::int64_t>(c) * n + pos] += s;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // ------------------------------------------------------------ launchers
 void launch_snapshot(cudaStream_t st, const SnapTile* tiles, std::int64_t ntiles, const BlockGeom* geo,
                      const double* pts, std::int64_t n, int d, int fam, int R, const double* theta_nodes, double amp,
@@ -843,8 +999,8 @@ void launch_up(cudaStream_t st, const std::int32_t* nodes, int cnt, const std::i
                const std::int32_t* count, const double* E, int d, int ps, int P, int m, double* xhat) {
   if (cnt == 0) return;
   const int nc = 1 << d;
-  const size_t smem = (nc * d * ps * ps + nc * P) * sizeof(double);
-  k_up<<<cnt, threads_for(P), smem, st>>>(nodes, first_child, count, E, d, ps, P, nc, m, xhat);
+  const size_t smem = (d * ps * ps + 3 * P) * sizeof(double);
+  k_up2<<<cnt, threads_for(P), smem, st>>>(nodes, first_child, count, E, d, ps, P, nc, m, xhat);
 }
 void launch_coupling(cudaStream_t st, const std::int32_t* sig, int nsig, const std::int64_t* fbeg,
                      const std::int32_t* ftau, const std::int32_t* fcls, const double* C, int P, int m,
@@ -893,15 +1049,15 @@ void launch_near_mvm(cudaStream_t st, const RowItem* items, int nitems, const st
 void launch_down(cudaStream_t st, const std::int32_t* nodes, int cnt, const std::int32_t* parent, const double* E,
                  int d, int ps, int P, int m, double* yhat) {
   if (cnt == 0) return;
-  const size_t smem = (d * ps * ps + P) * sizeof(double);
-  k_down<<<cnt, threads_for(P), smem, st>>>(nodes, parent, E, d, ps, P, m, yhat);
+  const size_t smem = (d * ps * ps + 3 * P) * sizeof(double);
+  k_down2<<<cnt, threads_for(P), smem, st>>>(nodes, parent, E, d, ps, P, m, yhat);
 }
 void launch_leaf_bwd(cudaStream_t st, const std::int32_t* leaves, int nleaves, const std::int64_t* begin,
                      const std::int32_t* count, const double* U, std::int64_t n, int d, int ps, int P,
                      const double* yhat, int m, std::int64_t row_lo, std::int64_t row_hi, double* yp) {
   if (nleaves == 0) return;
-  k_leaf_bwd<<<nleaves, 128, P * sizeof(double), st>>>(leaves, begin, count, U, n, d, ps, P, yhat, m, row_lo, row_hi,
-                                                        yp);
+  const size_t smem = (P + 2 * 32 * (P / ps)) * sizeof(double);
+  k_leaf_bwd2<<<nleaves, 128, smem, st>>>(leaves, begin, count, U, n, d, ps, P, yhat, m, row_lo, row_hi, yp);
 }
 void launch_far_h(cudaStream_t st, const FarHItem* items, int nitems, int max_rows, const std::int64_t* tbeg,
                   const std::int32_t* tcnt, const std::int32_t* cls, const std::int64_t* s_off,
