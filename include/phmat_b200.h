@@ -94,6 +94,8 @@ typedef struct phm_config {
   int32_t threads;     /* 0: PHMAT_THREADS / hardware */
   int32_t shard_rank;
   int32_t shard_count;
+  int32_t symmetric_near; /* snapshot mode: store sigma <= tau blocks only (D_ts = D_st^T) */
+  int32_t reserved;
 } phm_config;
 
 /* StructureMetrics (phmatrix.hpp:141-153) + build statistics. */
@@ -102,6 +104,7 @@ typedef struct phm_info {
   int64_t P;                 /* p_s^d */
   int64_t row_begin, row_end;/* tree-order rows owned by this shard */
   int64_t near_entries;      /* sum over local near blocks of n_sigma n_tau */
+  int64_t near_stored;       /* near entries actually stored (symmetric storage halves them) */
   int64_t near_stream_elems; /* sum of n_sigma n_tau (R_b + 1): K1's algorithmic elements */
   int64_t device_bytes;
   int64_t storage_entries;

@@ -68,14 +68,15 @@ class _Config(C.Structure):
         ("format", C.c_int32), ("l_max", C.c_int32), ("p_s", C.c_int32), ("near_mode", C.c_int32),
         ("eps", C.c_double), ("eta", C.c_double), ("r_max_far", C.c_int64), ("r_max_near", C.c_int64),
         ("seed", C.c_uint64), ("translation_cache", C.c_int32), ("threads", C.c_int32),
-        ("shard_rank", C.c_int32), ("shard_count", C.c_int32),
+        ("shard_rank", C.c_int32), ("shard_count", C.c_int32), ("symmetric_near", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
 class _Info(C.Structure):
     _fields_ = [(k, C.c_int64) for k in (
         "n", "d", "nodes", "n_near", "n_far", "n_classes", "c_sp", "constructed", "P",
-        "row_begin", "row_end", "near_entries", "near_stream_elems", "device_bytes", "storage_entries")] + [
+        "row_begin", "row_end", "near_entries", "near_stored", "near_stream_elems", "device_bytes", "storage_entries")] + [
         (k, C.c_double) for k in (
             "storage_gb", "nf_ratio", "ff_ratio", "coupling_ratio", "rank", "tree_s", "ff_s", "nf_s", "upload_s")] + [
         ("evals_offline", C.c_uint64), ("evals_online", C.c_uint64), ("evals_audit", C.c_uint64),
@@ -227,6 +228,7 @@ class PHConfig:
     threads: int = 0
     shard_rank: int = 0
     shard_count: int = 1
+    symmetric_near: bool = True
 
     def to_c(self, fmt: int) -> _Config:
         c = _Config()
@@ -248,6 +250,7 @@ class PHConfig:
         c.r_max_far, c.r_max_near, c.seed = self.r_max_far, self.r_max_near, self.seed
         c.translation_cache = 1 if self.translation_cache else 0
         c.threads, c.shard_rank, c.shard_count = self.threads, self.shard_rank, self.shard_count
+        c.symmetric_near = 1 if self.symmetric_near else 0
         return c
 
 

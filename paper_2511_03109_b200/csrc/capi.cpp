@@ -86,6 +86,7 @@ phm::Config to_config(const phm_config& c) {
   cfg.threads = c.threads;
   cfg.shard_rank = c.shard_rank;
   cfg.shard_count = c.shard_count < 1 ? 1 : c.shard_count;
+  cfg.symmetric_near = c.symmetric_near != 0;
   return cfg;
 }
 
@@ -195,6 +196,7 @@ void phm_config_default(phm_config* c) {
   c->threads = 0;
   c->shard_rank = 0;
   c->shard_count = 1;
+  c->symmetric_near = 1;
 }
 
 int phm_context_create(int device, phm_context* out) {
@@ -309,8 +311,9 @@ int phm_matrix_info(phm_matrix m, phm_info* info) {
     info->row_begin = H.row_begin;
     info->row_end = H.row_end;
     if (phm::matrix_on_device(*m->m)) {
-      info->near_entries = phm::matrix_near_elems(*m->m, false);
-      info->near_stream_elems = phm::matrix_near_elems(*m->m, true);
+      info->near_entries = phm::matrix_near_elems(*m->m, 0);
+      info->near_stored = phm::matrix_near_elems(*m->m, 1);
+      info->near_stream_elems = phm::matrix_near_elems(*m->m, 2);
       info->device_bytes = phm::matrix_device_bytes(*m->m);
     }
     info->tree_s = H.stats.tree_s;

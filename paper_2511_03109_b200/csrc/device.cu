@@ -49,6 +49,9 @@ void launch_coupling_reduce(cudaStream_t, const std::int32_t*, const std::int32_
                             double*);
 void launch_near_mvm(cudaStream_t, const RowItem*, int, const std::int64_t*, const std::int32_t*,
                      const std::int64_t*, const double*, const double*, double*);
+void launch_near_mvm_sym(cudaStream_t, const SymItem*, int, const double*, const double*, double*);
+void launch_near_gather(cudaStream_t, int, const std::int64_t*, const std::int32_t*, const std::int32_t*,
+                        const GatherSeg*, const double*, double*);
 void launch_down(cudaStream_t, const std::int32_t*, int, const std::int32_t*, const double*, int, int, int, int,
                  double*);
 void launch_leaf_bwd(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*, const double*,
@@ -255,6 +258,12 @@ struct DevMatrix {
   std::int64_t n_inst_tiles = 0, n_near_local = 0, w_len = 0;
   DBuf row_items, nb_tb, nb_tn, nb_doff;
   int n_row_items = 0;
+  // symmetric near storage (sigma <= tau blocks only)
+  bool sym = false;
+  std::vector<char> near_trans;  // block stored as the transpose of its partner
+  std::int64_t E_logical = 0;    // sum of n_sigma n_tau over local near blocks
+  DBuf sym_items, g_row0, g_rows, g_sbeg, g_segs, sym_part;
+  int n_sym_items = 0, n_gather_leaves = 0;
   // far field
   int ncls = 0;
   std::vector<dev::ClassMeta> cmeta_h;
@@ -348,7 +357,9 @@ std::int64_t matrix_near_rank(const DevMatrix& m, Index b) {
   if (b < 0 || b >= static_cast<Index>(m.near_R.size())) throw std::out_of_range("near block index");
   return m.near_R[b];
 }
-std::int64_t matrix_near_elems(const DevMatrix& m, bool with_rank) { return with_rank ? m.E_rank : m.E_raw; }
+std::int64_t matrix_near_elems(const DevMatrix& m, int kind) {
+  return kind == 0 ? m.E_logical : (kind == 1 ? m.E_raw : m.E_rank);
+}
 
 void matrix_near_column(const DevMatrix& m, Index b, Index kap, double* out) {
   if (!m.ctx) throw std::logic_error("host-only matrix has no device near payload");
@@ -357,11 +368,14 @@ void matrix_near_column(const DevMatrix& m, Index b, Index kap, double* out) {
   if (kap < 0 || kap >= m.near_R[b]) throw std::out_of_range("near column index");
   const HostMatrix& H = *m.hm;
   const Block blk = H.blocks.near[b];
-  const Index N = H.tree->nodes[blk.sigma].count * H.tree->nodes[blk.tau].count;
+  const Index ns = H.tree->nodes[blk.sigma].count, nt = H.tree->nodes[blk.tau].count;
   CK(cudaSetDevice(m.ctx->device));
-  CK(cudaMemcpyAsync(out, m.G.as<double>() + m.near_goff[b] + kap * m.near_gstride[b], N * sizeof(double),
+  std::vector<double> tmp(static_cast<size_t>(ns * nt));
+  CK(cudaMemcpyAsync(tmp.data(), m.G.as<double>() + m.near_goff[b] + kap * m.near_gstride[b], ns * nt * sizeof(double),
                      cudaMemcpyDeviceToHost, m.st()));
   CK(cudaStreamSynchronize(m.st()));
+  for (Index j = 0; j < nt; ++j)
+    for (Index i = 0; i < ns; ++i) out[i + j * ns] = m.near_trans[b] ? tmp[j + i * nt] : tmp[i + j * ns];
 }
 
 std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const double* points, Index n, int d,
@@ -418,17 +432,42 @@ std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const doub
   M.near_R.assign(nnear, 0);
   int Rshape = 1;  // snapshot rank: product of non-amplitude theta grids
   for (int k = 0; k < cfg.spec.shape_params(); ++k) Rshape *= H.grids.grids[k].p;
+  // Symmetric near storage: the near relation is symmetric and every kernel
+  // family is radial, so with snapshots (or direct evaluation) D_{tau,sigma}
+  // equals D_{sigma,tau}^T bit for bit (the squared distance accumulates the
+  // same rounded squares). Only blocks with sigma <= tau are stored.
+  M.sym = M.mode == NearMode::Snapshot && cfg.symmetric_near &&
+          cfg.shard_count == 1;
+  M.near_trans.assign(nnear, 0);
+  std::vector<Index> canon(nnear);
+  for (Index b = 0; b < nnear; ++b) canon[b] = b;
+  if (M.sym) {
+    std::unordered_map<std::uint64_t, Index> where;
+    auto key = [](int s, int t) { return (static_cast<std::uint64_t>(s) << 32) | static_cast<std::uint32_t>(t); };
+    for (Index b = 0; b < nnear; ++b) where[key(H.blocks.near[b].sigma, H.blocks.near[b].tau)] = b;
+    for (Index b = 0; b < nnear; ++b) {
+      const Block blk = H.blocks.near[b];
+      if (blk.sigma > blk.tau) {
+        canon[b] = where.at(key(blk.tau, blk.sigma));
+        M.near_trans[b] = 1;
+      }
+    }
+  }
   {
     std::int64_t off = 0;
     for (Index b = 0; b < nnear; ++b) {
       if (!H.near_local[b]) continue;
       const Block blk = H.blocks.near[b];
       const std::int64_t N = T.nodes[blk.sigma].count * T.nodes[blk.tau].count;
+      M.E_logical += N;
+      ++M.n_near_local;
+      if (M.near_trans[b]) continue;
       M.near_doff[b] = off;
       off += pad4(N);
       M.E_raw += N;
-      ++M.n_near_local;
     }
+    for (Index b = 0; b < nnear; ++b)
+      if (M.near_trans[b]) M.near_doff[b] = M.near_doff[canon[b]];
     M.E = off;
   }
   std::vector<dev::BlockGeom> geo(nnear);
@@ -442,7 +481,7 @@ std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const doub
     std::vector<dev::SnapTile> tiles;
     const int kTile = 4096;
     for (Index b = 0; b < nnear; ++b) {
-      if (M.near_doff[b] < 0) continue;
+      if (M.near_doff[b] < 0 || M.near_trans[b]) continue;
       const std::int64_t N = static_cast<std::int64_t>(geo[b].s_n) * geo[b].t_n;
       for (std::int64_t e0 = 0; e0 < N; e0 += kTile)
         tiles.push_back({M.near_doff[b] + e0, M.E, static_cast<std::int32_t>(e0),
@@ -481,7 +520,7 @@ std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const doub
       parallel_for(
           nnear,
           [&](Index b) {
-            if (M.near_doff[b] < 0) return;
+            if (M.near_doff[b] < 0 || M.near_trans[b]) return;
             const auto& g = geo[b];
             for (std::int64_t j = 0; j < g.t_n; ++j)
               for (std::int64_t i = 0; i < g.s_n; ++i) {
@@ -571,8 +610,61 @@ std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const doub
     M.E_rank = M.E_raw;
   }
 
+  if (M.sym) {
+    // K6 on symmetric storage: one item per (stored block, 128-row chunk);
+    // partial segments gathered per leaf in near-list order.
+    std::vector<dev::SymItem> items;
+    std::vector<std::vector<dev::GatherSeg>> segs_of(M.nnodes);
+    std::int64_t poff = 0;
+    for (Index b = 0; b < nnear; ++b) {
+      if (M.near_doff[b] < 0 || M.near_trans[b]) continue;
+      const Block blk = H.blocks.near[b];
+      const TreeNode& s = T.nodes[blk.sigma];
+      const TreeNode& u = T.nodes[blk.tau];
+      const bool diag = blk.sigma == blk.tau;
+      const int ns = static_cast<int>(s.count), nt = static_cast<int>(u.count);
+      for (int i0 = 0; i0 < ns; i0 += 128) {
+        dev::SymItem it{};
+        it.d_off = M.near_doff[b];
+        it.x_row0 = s.begin;
+        it.x_col0 = u.begin;
+        it.ld = ns;
+        it.i0 = i0;
+        it.rows = std::min(128, ns - i0);
+        it.ncol = nt;
+        it.diag = diag ? 1 : 0;
+        it.p_row = poff;
+        segs_of[blk.sigma].push_back({poff, i0, it.rows});
+        poff += it.rows;
+        if (!diag) {
+          it.p_col = poff;
+          segs_of[blk.tau].push_back({poff, 0, nt});
+          poff += nt;
+        }
+        items.push_back(it);
+      }
+    }
+    std::vector<std::int64_t> lrow0;
+    std::vector<std::int32_t> lrows, sbeg{0};
+    std::vector<dev::GatherSeg> segs;
+    for (int id = 0; id < M.nnodes; ++id) {
+      if (segs_of[id].empty()) continue;
+      lrow0.push_back(T.nodes[id].begin);
+      lrows.push_back(static_cast<std::int32_t>(T.nodes[id].count));
+      segs.insert(segs.end(), segs_of[id].begin(), segs_of[id].end());
+      sbeg.push_back(static_cast<std::int32_t>(segs.size()));
+    }
+    M.n_sym_items = static_cast<int>(items.size());
+    M.n_gather_leaves = static_cast<int>(lrow0.size());
+    upload(M.sym_items, items, st);
+    upload(M.g_row0, lrow0, st);
+    upload(M.g_rows, lrows, st);
+    upload(M.g_sbeg, sbeg, st);
+    upload(M.g_segs, segs, st);
+    M.sym_part.alloc(sizeof(double) * std::max<std::int64_t>(poff, 1));
+  }
   // K6 work: CSR by sigma leaf, row chunks of 128
-  {
+  if (!M.sym) {
     std::vector<std::vector<Index>> by_sigma(M.nnodes);
     for (Index b = 0; b < nnear; ++b)
       if (M.near_doff[b] >= 0) by_sigma[H.blocks.near[b].sigma].push_back(b);
@@ -955,11 +1047,17 @@ void instance_near_d(DevInstance& I, Index b, std::vector<double>& out) {
   if (b < 0 || b >= static_cast<Index>(H.blocks.near.size())) throw std::out_of_range("near index");
   if (M.near_doff[b] < 0) throw std::out_of_range("near block not resident on this shard");
   const Block blk = H.blocks.near[b];
-  const Index N = H.tree->nodes[blk.sigma].count * H.tree->nodes[blk.tau].count;
-  out.resize(static_cast<size_t>(N));
-  CK(cudaMemcpyAsync(out.data(), I.D.as<double>() + M.near_doff[b], N * sizeof(double), cudaMemcpyDeviceToHost,
+  const Index ns = H.tree->nodes[blk.sigma].count, nt = H.tree->nodes[blk.tau].count;
+  out.resize(static_cast<size_t>(ns * nt));
+  CK(cudaMemcpyAsync(out.data(), I.D.as<double>() + M.near_doff[b], ns * nt * sizeof(double), cudaMemcpyDeviceToHost,
                      M.st()));
   CK(cudaStreamSynchronize(M.st()));
+  if (M.near_trans[b]) {  // stored as the (nt x ns) partner block
+    std::vector<double> t(out.size());
+    for (Index j = 0; j < nt; ++j)
+      for (Index i = 0; i < ns; ++i) t[i + j * ns] = out[j + i * nt];
+    out.swap(t);
+  }
 }
 
 void instance_class_c(DevInstance& I, Index k, std::vector<double>& out) {
@@ -1032,13 +1130,26 @@ void apply_tree_order(DevInstance& I, Index m) {
       });
     }
   }
-  if (M.n_row_items == 0) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
-  for (Index c = 0; c < m; ++c)
-    ctx.run("near_mvm", [&] {
-      dev::launch_near_mvm(st, M.row_items.as<dev::RowItem>(), M.n_row_items, M.nb_tb.as<std::int64_t>(),
-                           M.nb_tn.as<std::int32_t>(), M.nb_doff.as<std::int64_t>(), I.D.as<double>(),
-                           M.xp.as<double>() + c * M.n, M.yp.as<double>() + c * M.n);
-    });
+  if ((M.sym ? M.n_gather_leaves : M.n_row_items) == 0) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
+  for (Index c = 0; c < m; ++c) {
+    if (M.sym) {
+      ctx.run("near_mvm", [&] {
+        dev::launch_near_mvm_sym(st, M.sym_items.as<dev::SymItem>(), M.n_sym_items, I.D.as<double>(),
+                                 M.xp.as<double>() + c * M.n, M.sym_part.as<double>());
+      });
+      ctx.run("near_gather", [&] {
+        dev::launch_near_gather(st, M.n_gather_leaves, M.g_row0.as<std::int64_t>(), M.g_rows.as<std::int32_t>(),
+                                M.g_sbeg.as<std::int32_t>(), M.g_segs.as<dev::GatherSeg>(), M.sym_part.as<double>(),
+                                M.yp.as<double>() + c * M.n);
+      });
+    } else {
+      ctx.run("near_mvm", [&] {
+        dev::launch_near_mvm(st, M.row_items.as<dev::RowItem>(), M.n_row_items, M.nb_tb.as<std::int64_t>(),
+                             M.nb_tn.as<std::int32_t>(), M.nb_doff.as<std::int64_t>(), I.D.as<double>(),
+                             M.xp.as<double>() + c * M.n, M.yp.as<double>() + c * M.n);
+      });
+    }
+  }
   if (M.h2) {
     ctx.join();
     ctx.run("leaf_bwd", [&] {

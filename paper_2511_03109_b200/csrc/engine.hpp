@@ -40,9 +40,10 @@ std::int64_t matrix_device_bytes(const DevMatrix& m);
 std::int64_t matrix_near_rank(const DevMatrix& m, Index near_block);
 // Device -> host copy of one snapshot / G1 column kap of a near block.
 void matrix_near_column(const DevMatrix& m, Index near_block, Index kap, double* out);
-// Sum over local near blocks of n_sigma n_tau (R_b + 1): the instantiate
-// stream's algorithmic element count (x8 bytes); and sum of n_sigma n_tau.
-std::int64_t matrix_near_elems(const DevMatrix& m, bool with_rank);
+// kind 0: sum over local near blocks of n_sigma n_tau (the logical near
+// field); 1: entries actually stored (symmetric storage keeps sigma <= tau);
+// 2: stored entries times (R_b + 1), the instantiate stream's elements.
+std::int64_t matrix_near_elems(const DevMatrix& m, int kind);
 
 std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const double* theta, int n_theta,
                                          StageCounters* counters);

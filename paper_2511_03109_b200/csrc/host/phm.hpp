@@ -271,6 +271,7 @@ struct Config {
   int threads = 0;
   int shard_rank = 0;   // leaf row-cluster sharding (multi-GPU); 0 / 1 = whole
   int shard_count = 1;
+  bool symmetric_near = true;  // snapshot mode: store sigma <= tau near blocks only
   double resolved_eta(int d) const { return eta > 0.0 ? eta : std::sqrt(double(d)); }
 };
 

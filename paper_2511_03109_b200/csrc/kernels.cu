@@ -641,6 +641,98 @@ __global__ void __launch_bounds__(256) k_near_mvm(const RowItem* __restrict__ it
   }
 }
 
+// K6, symmetric storage: every stored block is streamed once and used twice
+// (y_sigma += D x_tau and y_tau += D^T x_sigma), halving the near-field
+// bytes of both instantiate and MVM for the (symmetric) radial kernels.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_near_mvm_sym(const SymItem* __restrict__ items, const double* __restrict__ D,
+                                                      const double* __restrict__ xp, double* __restrict__ part) {
+  __shared__ double red[8][128];
+  const SymItem it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double racc[4] = {0.0, 0.0, 0.0, 0.0};
+  double xs[4];
+  bool live[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    live[q] = lane + 32 * q < it.rows;
+    xs[q] = live[q] ? xp[it.x_row0 + it.i0 + lane + 32 * q] : 0.0;
+  }
+  const double* Db = D + it.d_off + it.i0 + lane;
+  const double* xt = xp + it.x_col0;
+  const std::int64_t ld = it.ld;
+  int j = warp;
+  for (; j + 8 < it.ncol; j += 16) {
+    const double x0 = xt[j], x1 = xt[j + 8];
+    double v0[4], v1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      v0[q] = live[q] ? ld_stream(Db + j * ld + 32 * q) : 0.0;
+      v1[q] = live[q] ? ld_stream(Db + (j + 8) * ld + 32 * q) : 0.0;
+    }
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      racc[q] += v0[q] * x0 + v1[q] * x1;
+      c0 += v0[q] * xs[q];
+      c1 += v1[q] * xs[q];
+    }
+    if (!it.diag) {
+      c0 = warp_sum(c0);
+      c1 = warp_sum(c1);
+      if (lane == 0) {
+        part[it.p_col + j] = c0;
+        part[it.p_col + j + 8] = c1;
+      }
+    }
+  }
+  for (; j < it.ncol; j += 8) {
+    const double x0 = xt[j];
+    double c0 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double v = live[q] ? ld_stream(Db + j * ld + 32 * q) : 0.0;
+      racc[q] += v * x0;
+      c0 += v * xs[q];
+    }
+    if (!it.diag) {
+      c0 = warp_sum(c0);
+      if (lane == 0) part[it.p_col + j] = c0;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) red[warp][lane + 32 * q] = racc[q];
+  __syncthreads();
+  if (threadIdx.x < it.rows) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+    part[it.p_row + threadIdx.x] = s;
+  }
+}
+
+// y[rows of leaf] = sum of the leaf's partial segments, in list order.
+__global__ void k_near_gather(const std::int64_t* __restrict__ leaf_row0, const std::int32_t* __restrict__ leaf_rows,
+                              const std::int32_t* __restrict__ seg_beg, const GatherSeg* __restrict__ segs,
+                              const double* __restrict__ part, double* __restrict__ yp) {
+  const int l = blockIdx.x;
+  const int sb = seg_beg[l], se = seg_beg[l + 1];
+  for (int r = threadIdx.x; r < leaf_rows[l]; r += blockDim.x) {
+    double s = 0.0;
+    for (int k = sb; k < se; ++k) {
+      const GatherSeg g = segs[k];
+      const int o = r - g.base;
+      if (o >= 0 && o < g.len) s += part[g.poff + o];
+    }
+    yp[leaf_row0[l] + r] = s;
+  }
+}
+
 // ----------------------------------------------------------------- K7
 // yhat_child[b] += sum_a prod_k E_k(b_k, a_k) yhat_parent[a] (fast_kron,
 // chebyshev.cpp:286-295). One CTA per child node of the level.
@@ -1008,6 +1100,17 @@ void launch_coupling(cudaStream_t st, const std::int32_t* sig, int nsig, const s
   if (nsig == 0) return;
   k_coupling<<<nsig, threads_for(P), P * sizeof(double), st>>>(sig, fbeg, ftau, fcls, C, P, m, xhat, yhat);
 }
+void launch_near_mvm_sym(cudaStream_t st, const SymItem* items, int nitems, const double* D, const double* xp,
+                         double* part) {
+  if (nitems == 0) return;
+  k_near_mvm_sym<<<nitems, 256, 0, st>>>(items, D, xp, part);
+}
+void launch_near_gather(cudaStream_t st, int nleaves, const std::int64_t* leaf_row0, const std::int32_t* leaf_rows,
+                        const std::int32_t* seg_beg, const GatherSeg* segs, const double* part, double* yp) {
+  if (nleaves == 0) return;
+  k_near_gather<<<nleaves, 128, 0, st>>>(leaf_row0, leaf_rows, seg_beg, segs, part, yp);
+}
+
 bool coupling_mma_supported(int P) { return P == 16 || P == 32 || P == 64 || P == 128; }
 
 void launch_coupling_mma(cudaStream_t st, const CouplingItem* items, int nitems, const std::int32_t* item_cls,

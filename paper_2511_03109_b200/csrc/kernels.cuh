@@ -72,6 +72,19 @@ struct CouplingItem {
   std::int32_t group, e_begin, e_end, pad;
 };
 
+// K6 with symmetric near storage: one item per (stored block, 128-row
+// chunk). The item writes its row partial D x_tau (rows doubles at p_row)
+// and, for off-diagonal blocks, its column partial D^T x_sigma (ncol doubles
+// at p_col); k_near_gather sums the partials of each leaf in a fixed order.
+struct SymItem {
+  std::int64_t d_off, x_row0, x_col0, p_row, p_col;
+  std::int32_t ld, i0, rows, ncol, diag, pad;
+};
+struct GatherSeg {  // contribution to rows [base, base + len) of one leaf
+  std::int64_t poff;
+  std::int32_t base, len;
+};
+
 struct FarHItem {  // K8 work item: one sigma node at one level
   std::int64_t row0;
   std::int32_t rows, bbeg, bend, pad;

@@ -55,12 +55,12 @@ def _check_instance(ph, pm, om, theta, block_stride=1):
     return inst, oi
 
 
-@pytest.mark.parametrize("fam", ["e", "m32", "gauss"])
-def test_h2_snapshot_3d_matches_oracle(ph, po, fam):
+@pytest.mark.parametrize("fam,sym", [("e", True), ("e", False), ("m32", True), ("gauss", False)])
+def test_h2_snapshot_3d_matches_oracle(ph, po, fam, sym):
     pts = ph.generate_points(3000, 3, 0)
     box = {"e": (0.05, 0.5), "m32": (0.05, 0.5), "gauss": (0.1, 1.0)}[fam]
     cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.from_id(fam), [box]), l_max=2, p_s=4, p_theta=8, eta=1.0,
-                      near_mode=ph.NearMode.SNAPSHOT, seed=0)
+                      near_mode=ph.NearMode.SNAPSHOT, seed=0, symmetric_near=sym)
     pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
     for theta in ([box[0]], [0.5 * (box[0] + box[1]) + 0.0123], [box[1]]):
         inst, oi = _check_instance(ph, pm, om, theta, block_stride=7)
@@ -74,6 +74,9 @@ def test_snapshot_generation_matches_oracle(ph, po):
     cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
                       near_mode=ph.NearMode.SNAPSHOT)
     pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    info = pm.info()
+    # symmetric storage keeps only sigma <= tau blocks (about half)
+    assert info["near_stored"] < 0.6 * info["near_entries"]
     sizes = _node_sizes(pm)
     near, _, _ = pm.blocks()
     worst = 0.0
@@ -194,6 +197,24 @@ def test_errors_map_to_reference_exceptions(ph):
     inst = ph.instantiate(pm, [0.5])
     with pytest.raises(ph.InvalidArgument):
         inst.apply(np.zeros(129))
+
+
+def test_symmetric_storage_is_exact(ph):
+    """D_{tau,sigma} = D_{sigma,tau}^T bitwise, and the symmetric two-sided
+    near GEMV agrees with the full-storage one to rounding."""
+    pts = ph.generate_points(3000, 3, 6)
+    base = dict(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                near_mode=ph.NearMode.SNAPSHOT)
+    a = ph.offline_h2(pts, ph.PHConfig(**base, symmetric_near=True))
+    b = ph.offline_h2(pts, ph.PHConfig(**base, symmetric_near=False))
+    ia, ib = ph.instantiate(a, [0.123]), ph.instantiate(b, [0.123])
+    sizes = _node_sizes(a)
+    near, _, _ = a.blocks()
+    for k in range(0, len(near), 13):
+        s, t = near[k]
+        assert np.array_equal(ia.near_d(k, (sizes[s], sizes[t])), ib.near_d(k, (sizes[s], sizes[t])))
+    x = ph.generate_normal(3000, 1)
+    assert rel(ia.apply(x), ib.apply(x)) <= 1e-14
 
 
 def test_reinstantiate_in_place(ph, po):
