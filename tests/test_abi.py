@@ -47,6 +47,44 @@ def test_library_is_sm100a(ph):
     assert "sm_100a" in out
 
 
+def test_cpp_facade_compiles_and_links(ph, tmp_path):
+    """include/phmat_b200.hpp (reference-named C++ facade) compiles against
+    the C ABI and links; without a GPU the context throws runtime_error and
+    the host-only structure build works."""
+    import shutil
+    import subprocess
+
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    src = tmp_path / "t.cpp"
+    src.write_text(r'''
+#include "phmat_b200.hpp"
+#include <cstdio>
+int main() {
+  std::vector<double> pts(2 * 256);
+  phm_generate_points(256, 2, 3, pts.data());
+  phmat_b200::PHConfig cfg;
+  cfg.c.l_max = 2; cfg.c.p_s = 4; cfg.c.p_theta[0] = 5; cfg.c.eps = 1e-3;
+  phm_matrix m = nullptr;
+  phmat_b200::check(phm_matrix_build_host(pts.data(), 256, 2, &cfg.c, &m));
+  phm_info info; phmat_b200::check(phm_matrix_info(m, &info));
+  std::printf("near=%lld far=%lld\n", (long long)info.n_near, (long long)info.n_far);
+  phm_matrix_destroy(m);
+  try { phmat_b200::Context ctx(0); std::printf("gpu\n"); }
+  catch (const std::runtime_error& e) { std::printf("nogpu\n"); }
+  try { std::vector<double> th{3.0}; phm_instance i; phmat_b200::check(phm_instantiate(nullptr, th.data(), 1, &i)); }
+  catch (const std::invalid_argument&) { std::printf("invalid\n"); }
+  return 0;
+}
+''')
+    exe = tmp_path / "t"
+    libdir = os.path.dirname(ph.library_path())
+    subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                    "-L", libdir, "-lphmat_b200", f"-Wl,-rpath,{libdir}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert "near=" in out and "invalid" in out
+
+
 def test_version_and_defaults(ph):
     assert ph.lib().phm_version() == 1
     c = ph.PHConfig().to_c(ph.Format.H2)
