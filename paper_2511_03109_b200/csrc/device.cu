@@ -949,9 +949,11 @@ void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCoun
   I.theta.assign(theta, theta + n_theta);
   const dev::ThetaV tv = make_theta_v(v);
 
-  // far: H_k (and C_k) per class
-  ctx.run("class_inst", [&] {
-    dev::launch_class_inst(st, M.cmeta.as<dev::ClassMeta>(), M.ncls, M.class_mid.as<double>(),
+  // far: H_k (and C_k) per class, on the side stream: compute-bound work
+  // that hides under the HBM-bound near-field stream below.
+  ctx.fork();
+  ctx.run_on(ctx.side, "class_inst", [&] {
+    dev::launch_class_inst(ctx.side, M.cmeta.as<dev::ClassMeta>(), M.ncls, M.class_mid.as<double>(),
                            M.class_mid_dims.as<std::int32_t>(), M.class_L.as<double>(), M.class_R.as<double>(), tv, M.P,
                            M.h2, M.capA, M.capB, M.capT, I.H.as<double>(), I.C.as<double>());
   });
@@ -994,6 +996,7 @@ void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCoun
     CK(cudaStreamSynchronize(st));  // th lives on this stack frame
     if (counters) counters->online.add(static_cast<std::uint64_t>(M.E_raw));
   }
+  ctx.join();  // H_k / C_k ready before anything later on the main stream
 }
 
 }  // namespace

@@ -716,6 +716,76 @@ __global__ void __launch_bounds__(256) k_near_mvm_sym(const SymItem* __restrict_
   }
 }
 
+// Warp-per-item version: one warp streams a whole stored block (<= 128
+// rows per item), lane l owning rows l + 32q. Column partials of 32
+// consecutive columns are kept per lane and reduced across the warp with one
+// transpose-reduce (16 + 8 + 4 + 2 + 1 = 31 shuffles for 32 columns) instead
+// of a 5-shuffle reduction per column; lane l ends with column j0 + l.
+template <int NQ>
+__device__ __forceinline__ void sym_block(const SymItem& it, const double* __restrict__ D,
+                                          const double* __restrict__ xp, double* __restrict__ part, int lane) {
+  double racc[NQ], xs[NQ];
+  bool live[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    live[q] = lane + 32 * q < it.rows;
+    xs[q] = live[q] ? xp[it.x_row0 + it.i0 + lane + 32 * q] : 0.0;
+    racc[q] = 0.0;
+  }
+  const double* Db = D + it.d_off + it.i0 + lane;
+  const double* xt = xp + it.x_col0;
+  const std::int64_t ld = it.ld;
+  for (int j0 = 0; j0 < it.ncol; j0 += 32) {
+    double c[32];
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = j0 + jj;
+      double cj = 0.0;
+      if (j < it.ncol) {
+        const double x0 = xt[j];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const double v = live[q] ? ld_stream(Db + j * ld + 32 * q) : 0.0;
+          racc[q] += v * x0;
+          cj += v * xs[q];
+        }
+      }
+      c[jj] = cj;
+    }
+    if (!it.diag) {
+      // transpose-reduce: after the round with offset o each lane keeps the
+      // half of its columns whose bit o matches its own lane bit
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const bool upper = lane & o;
+#pragma unroll
+        for (int k = 0; k < o; ++k) {
+          const double send = upper ? c[k] : c[k + o];
+          const double keep = upper ? c[k + o] : c[k];
+          c[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (j0 + lane < it.ncol) part[it.p_col + j0 + lane] = c[0];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+    if (live[q]) part[it.p_row + lane + 32 * q] = racc[q];
+}
+
+__global__ void __launch_bounds__(128) k_near_mvm_sym2(const SymItem* __restrict__ items, int nitems,
+                                                       const double* __restrict__ D, const double* __restrict__ xp,
+                                                       double* __restrict__ part) {
+  const int w = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (w >= nitems) return;
+  const int lane = threadIdx.x & 31;
+  const SymItem it = items[w];
+  if (it.rows <= 64)
+    sym_block<2>(it, D, xp, part, lane);
+  else
+    sym_block<4>(it, D, xp, part, lane);
+}
+
 // y[rows of leaf] = sum of the leaf's partial segments, in list order.
 __global__ void k_near_gather(const std::int64_t* __restrict__ leaf_row0, const std::int32_t* __restrict__ leaf_rows,
                               const std::int32_t* __restrict__ seg_beg, const GatherSeg* __restrict__ segs,
@@ -1103,7 +1173,7 @@ void launch_coupling(cudaStream_t st, const std::int32_t* sig, int nsig, const s
 void launch_near_mvm_sym(cudaStream_t st, const SymItem* items, int nitems, const double* D, const double* xp,
                          double* part) {
   if (nitems == 0) return;
-  k_near_mvm_sym<<<nitems, 256, 0, st>>>(items, D, xp, part);
+  k_near_mvm_sym2<<<(nitems + 3) / 4, 128, 0, st>>>(items, nitems, D, xp, part);
 }
 void launch_near_gather(cudaStream_t st, int nleaves, const std::int64_t* leaf_row0, const std::int32_t* leaf_rows,
                         const std::int32_t* seg_beg, const GatherSeg* segs, const double* part, double* yp) {
