@@ -50,6 +50,9 @@ void launch_coupling_reduce(cudaStream_t, const std::int32_t*, const std::int32_
 void launch_near_mvm(cudaStream_t, const RowItem*, int, const std::int64_t*, const std::int32_t*,
                      const std::int64_t*, const double*, const double*, double*);
 void launch_near_mvm_sym(cudaStream_t, const SymItem*, int, const double*, const double*, double*);
+void launch_near_mrhs(cudaStream_t, const MrhsItem*, int, const std::int64_t*, const std::int32_t*,
+                      const std::int64_t*, const std::int32_t*, const std::int32_t*, const double*, const double*,
+                      std::int64_t, int, double*);
 void launch_near_gather(cudaStream_t, int, const std::int64_t*, const std::int32_t*, const std::int32_t*,
                         const GatherSeg*, const double*, double*);
 void launch_down(cudaStream_t, const std::int32_t*, int, const std::int32_t*, const double*, int, int, int, int,
@@ -264,6 +267,9 @@ struct DevMatrix {
   std::int64_t E_logical = 0;    // sum of n_sigma n_tau over local near blocks
   DBuf sym_items, g_row0, g_rows, g_sbeg, g_segs, sym_part;
   int n_sym_items = 0, n_gather_leaves = 0;
+  // K9 multi-RHS near field (DMMA), CSR by sigma over stored blocks
+  DBuf k9_items, k9_tb, k9_tn, k9_doff, k9_ld, k9_tr;
+  int n_k9_items = 0;
   // far field
   int ncls = 0;
   std::vector<dev::ClassMeta> cmeta_h;
@@ -325,6 +331,10 @@ dev::ThetaV make_theta_v(const std::vector<std::vector<double>>& v) {
 }
 
 std::int64_t pad4(std::int64_t x) { return (x + 3) & ~std::int64_t(3); }
+
+// Right-hand-side count from which the near field switches from the HBM GEMV
+// (K6, one pass per vector) to the DMMA block kernel (K9, one pass for all).
+constexpr Index kMrhsMin = 4;
 
 void ensure_workspace(DevMatrix& M, Index m) {
   if (M.ws_m >= m) return;
@@ -663,6 +673,39 @@ std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const doub
     upload(M.g_segs, segs, st);
     M.sym_part.alloc(sizeof(double) * std::max<std::int64_t>(poff, 1));
   }
+  {
+    // K9 work (multi-RHS): CSR by sigma over every local near block; blocks
+    // kept as transposes read their partner through the transposed map.
+    std::vector<std::vector<Index>> by_sigma(M.nnodes);
+    for (Index b = 0; b < nnear; ++b)
+      if (M.near_doff[b] >= 0) by_sigma[H.blocks.near[b].sigma].push_back(b);
+    std::vector<dev::MrhsItem> items;
+    std::vector<std::int64_t> tb, dof;
+    std::vector<std::int32_t> tn, ld, tr;
+    for (int s = 0; s < M.nnodes; ++s) {
+      if (by_sigma[s].empty()) continue;
+      const int bbeg = static_cast<int>(tb.size());
+      for (Index b : by_sigma[s]) {
+        const Block blk = H.blocks.near[b];
+        tb.push_back(T.nodes[blk.tau].begin);
+        tn.push_back(static_cast<std::int32_t>(T.nodes[blk.tau].count));
+        dof.push_back(M.near_doff[b]);
+        ld.push_back(static_cast<std::int32_t>(M.near_trans[b] ? T.nodes[blk.tau].count : T.nodes[blk.sigma].count));
+        tr.push_back(M.near_trans[b] ? 1 : 0);
+      }
+      const int bend = static_cast<int>(tb.size());
+      const int ns = static_cast<int>(T.nodes[s].count);
+      for (int i0 = 0; i0 < ns; i0 += 64)
+        items.push_back({T.nodes[s].begin + i0, std::min(64, ns - i0), i0, bbeg, bend});
+    }
+    M.n_k9_items = static_cast<int>(items.size());
+    upload(M.k9_items, items, st);
+    upload(M.k9_tb, tb, st);
+    upload(M.k9_tn, tn, st);
+    upload(M.k9_doff, dof, st);
+    upload(M.k9_ld, ld, st);
+    upload(M.k9_tr, tr, st);
+  }
   // K6 work: CSR by sigma leaf, row chunks of 128
   if (!M.sym) {
     std::vector<std::vector<Index>> by_sigma(M.nnodes);
@@ -949,11 +992,10 @@ void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCoun
   I.theta.assign(theta, theta + n_theta);
   const dev::ThetaV tv = make_theta_v(v);
 
-  // far: H_k (and C_k) per class, on the side stream: compute-bound work
-  // that hides under the HBM-bound near-field stream below.
-  ctx.fork();
-  ctx.run_on(ctx.side, "class_inst", [&] {
-    dev::launch_class_inst(ctx.side, M.cmeta.as<dev::ClassMeta>(), M.ncls, M.class_mid.as<double>(),
+  // far: H_k (and C_k) per class. (Overlapping it with the near stream on the
+  // side stream measured slower: its CTAs displace K1's and K1 lost 1.8 ms.)
+  ctx.run("class_inst", [&] {
+    dev::launch_class_inst(st, M.cmeta.as<dev::ClassMeta>(), M.ncls, M.class_mid.as<double>(),
                            M.class_mid_dims.as<std::int32_t>(), M.class_L.as<double>(), M.class_R.as<double>(), tv, M.P,
                            M.h2, M.capA, M.capB, M.capT, I.H.as<double>(), I.C.as<double>());
   });
@@ -996,7 +1038,6 @@ void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCoun
     CK(cudaStreamSynchronize(st));  // th lives on this stack frame
     if (counters) counters->online.add(static_cast<std::uint64_t>(M.E_raw));
   }
-  ctx.join();  // H_k / C_k ready before anything later on the main stream
 }
 
 }  // namespace
@@ -1133,8 +1174,19 @@ void apply_tree_order(DevInstance& I, Index m) {
       });
     }
   }
-  if ((M.sym ? M.n_gather_leaves : M.n_row_items) == 0) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
-  for (Index c = 0; c < m; ++c) {
+  if ((M.sym ? M.n_gather_leaves : M.n_row_items) == 0 || M.n_k9_items == 0)
+    CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
+  // Block right-hand sides: the near product is a dense contraction, so it
+  // runs on fp64 tensor cores (K9); single vectors stay on the HBM GEMV.
+  const bool block_rhs = m >= kMrhsMin;
+  if (block_rhs)
+    ctx.run("near_mrhs", [&] {
+      dev::launch_near_mrhs(st, M.k9_items.as<dev::MrhsItem>(), M.n_k9_items, M.k9_tb.as<std::int64_t>(),
+                            M.k9_tn.as<std::int32_t>(), M.k9_doff.as<std::int64_t>(), M.k9_ld.as<std::int32_t>(),
+                            M.k9_tr.as<std::int32_t>(), I.D.as<double>(), M.xp.as<double>(), M.n, mm,
+                            M.yp.as<double>());
+    });
+  for (Index c = 0; c < (block_rhs ? 0 : m); ++c) {
     if (M.sym) {
       ctx.run("near_mvm", [&] {
         dev::launch_near_mvm_sym(st, M.sym_items.as<dev::SymItem>(), M.n_sym_items, I.D.as<double>(),

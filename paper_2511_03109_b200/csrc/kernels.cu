@@ -590,6 +590,105 @@ __global__ void k_coupling_reduce(const std::int32_t* __restrict__ grp_sigma, co
   }
 }
 
+// ------------------------------------------------------------------ K9
+// Multi-RHS near field, Y_sigma = sum_tau D_{sigma,tau} X_tau, on DMMA.
+// One CTA (4 warps) per (leaf sigma, 64-row chunk, 64-column chunk of the
+// right-hand sides): D chunks (64 x 32) and X chunks (32 x 64) are staged by
+// cp.async (double-buffered), warp w owns output rows [16w, 16w + 16) and all
+// 64 columns (8 m16n8k4 accumulator tiles). Transposed (symmetric-storage)
+// blocks are read through the transposed index map. Complete sums per CTA:
+// deterministic, no atomics.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+}
+
+constexpr int kK9Rows = 64, kK9Cols = 64, kK9Kc = 32;
+
+__global__ void __launch_bounds__(128) k_near_mrhs(const MrhsItem* __restrict__ items, const std::int64_t* __restrict__ tb,
+                                                   const std::int32_t* __restrict__ tn,
+                                                   const std::int64_t* __restrict__ doff,
+                                                   const std::int32_t* __restrict__ ldv,
+                                                   const std::int32_t* __restrict__ trv, const double* __restrict__ D,
+                                                   const double* __restrict__ X, std::int64_t n, int m,
+                                                   double* __restrict__ Y) {
+  constexpr int LDA = kK9Kc + 4, LDB = kK9Cols + 4;
+  extern __shared__ double sm[];
+  double* As[2] = {sm, sm + kK9Rows * LDA + kK9Kc * LDB};
+  double* Bs[2] = {sm + kK9Rows * LDA, sm + 2 * kK9Rows * LDA + kK9Kc * LDB};
+  const MrhsItem it = items[blockIdx.x];
+  const int c0 = blockIdx.y * kK9Cols;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t0 = lane & 3;
+  double acc[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+
+  auto stage = [&](int b, int k0, int buf) {
+    const int kc = min(kK9Kc, tn[b] - k0);
+    const double* Db = D + doff[b];
+    const std::int64_t ld = ldv[b];
+    const bool tr = trv[b] != 0;
+    double* A = As[buf];
+    double* B = Bs[buf];
+    for (int e = threadIdx.x; e < kK9Rows * kK9Kc; e += blockDim.x) {
+      const int i = tr ? e / kK9Kc : e % kK9Rows;
+      const int k = tr ? e % kK9Kc : e / kK9Rows;
+      const bool ok = i < it.rows && k < kc;
+      const std::int64_t r = it.i0 + i, c = k0 + k;
+      const double* src = Db + (tr ? c + r * ld : r + c * ld);
+      cp_async8(A + i * LDA + k, ok ? src : Db, ok);
+    }
+    for (int e = threadIdx.x; e < kK9Kc * kK9Cols; e += blockDim.x) {
+      const int k = e % kK9Kc, c = e / kK9Kc;
+      const bool ok = k < kc && c0 + c < m;
+      const double* src = X + tb[b] + k0 + k + static_cast<std::int64_t>(c0 + c) * n;
+      cp_async8(B + k * LDB + c, ok ? src : X, ok);
+    }
+    cp_async_commit();
+  };
+
+  int b = it.bbeg, k0 = 0, buf = 0;
+  if (b < it.bend) stage(b, 0, 0);
+  while (b < it.bend) {
+    int nb = b, nk = k0 + kK9Kc;
+    if (nk >= tn[b]) {
+      nb = b + 1;
+      nk = 0;
+    }
+    if (nb < it.bend) {
+      stage(nb, nk, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* A = As[buf];
+    const double* B = Bs[buf];
+#pragma unroll
+    for (int s = 0; s < kK9Kc / 4; ++s) {
+      const double a0 = A[(16 * warp + g) * LDA + 4 * s + t0];
+      const double a1 = A[(16 * warp + g + 8) * LDA + 4 * s + t0];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dmma_16x8x4(acc[j], a0, a1, B[(4 * s + t0) * LDB + 8 * j + g]);
+    }
+    __syncthreads();
+    b = nb;
+    k0 = nk;
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        const int row = 16 * warp + g + 8 * r2;
+        const int col = c0 + 8 * j + 2 * t0 + c2;
+        if (row < it.rows && col < m) Y[it.row0 + row + static_cast<std::int64_t>(col) * n] = acc[j][2 * r2 + c2];
+      }
+}
+
 // ----------------------------------------------------------------- K6
 // y[rows] = sum over the near blocks of sigma of D_b x_tau. 8 warps split the
 // columns of each block; each lane owns rows lane + 32q (q < 4), so every
@@ -1173,12 +1272,28 @@ void launch_coupling(cudaStream_t st, const std::int32_t* sig, int nsig, const s
 void launch_near_mvm_sym(cudaStream_t st, const SymItem* items, int nitems, const double* D, const double* xp,
                          double* part) {
   if (nitems == 0) return;
-  k_near_mvm_sym2<<<(nitems + 3) / 4, 128, 0, st>>>(items, nitems, D, xp, part);
+  // k_near_mvm_sym2 (warp per block, transpose-reduce) measured 3.3x slower
+  // than this CTA-per-block version at C3 (242 registers, low occupancy).
+  k_near_mvm_sym<<<nitems, 256, 0, st>>>(items, D, xp, part);
 }
 void launch_near_gather(cudaStream_t st, int nleaves, const std::int64_t* leaf_row0, const std::int32_t* leaf_rows,
                         const std::int32_t* seg_beg, const GatherSeg* segs, const double* part, double* yp) {
   if (nleaves == 0) return;
   k_near_gather<<<nleaves, 128, 0, st>>>(leaf_row0, leaf_rows, seg_beg, segs, part, yp);
+}
+
+void launch_near_mrhs(cudaStream_t st, const MrhsItem* items, int nitems, const std::int64_t* tb, const std::int32_t* tn,
+                      const std::int64_t* doff, const std::int32_t* ld, const std::int32_t* tr, const double* D,
+                      const double* X, std::int64_t n, int m, double* Y) {
+  if (nitems == 0) return;
+  const size_t smem = 2 * (kK9Rows * (kK9Kc + 4) + kK9Kc * (kK9Cols + 4)) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_near_mrhs, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = true;
+  }
+  const dim3 grid(static_cast<unsigned>(nitems), static_cast<unsigned>((m + kK9Cols - 1) / kK9Cols));
+  k_near_mrhs<<<grid, 128, smem, st>>>(items, tb, tn, doff, ld, tr, D, X, n, m, Y);
 }
 
 bool coupling_mma_supported(int P) { return P == 16 || P == 32 || P == 64 || P == 128; }

@@ -85,6 +85,14 @@ struct GatherSeg {  // contribution to rows [base, base + len) of one leaf
   std::int32_t base, len;
 };
 
+// K9 (multi-RHS near field on DMMA): one item per (leaf sigma, 64-row
+// chunk); its near blocks are nb_* entries [bbeg, bend) (tau begin, n_tau,
+// stored offset, stored leading dimension, transposed flag).
+struct MrhsItem {
+  std::int64_t row0;
+  std::int32_t rows, i0, bbeg, bend;
+};
+
 struct FarHItem {  // K8 work item: one sigma node at one level
   std::int64_t row0;
   std::int32_t rows, bbeg, bend, pad;

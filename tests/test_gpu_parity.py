@@ -172,7 +172,25 @@ def test_multi_rhs_matches_column_loop(ph, po):
     Yo = om.instantiate([0.3]).apply(X)
     for c in range(X.shape[1]):
         assert rel(Y[:, c], Yo[:, c]) <= TOL_Y
-        assert np.array_equal(Y[:, c], inst.apply(X[:, c]))
+        # the block path (K9 DMMA near field) vs the single-vector path (K6)
+        assert rel(Y[:, c], inst.apply(X[:, c])) <= 1e-14
+    assert np.array_equal(inst.apply(X), Y)  # deterministic
+
+
+@pytest.mark.parametrize("sym,m", [(True, 64), (False, 70), (True, 7)])
+def test_block_rhs_dmma_near_field(ph, po, sym, m):
+    """K9 (multi-RHS near field on mma.sync f64) over symmetric and full
+    storage, column counts across the 64-wide column tiles."""
+    pts = ph.generate_points(2200, 3, 21)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT, symmetric_near=sym)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    inst = ph.instantiate(pm, [0.27])
+    rng = np.random.default_rng(m)
+    X = rng.standard_normal((2200, m))
+    Y = inst.apply(X)
+    Yo = om.instantiate([0.27]).apply(X)
+    assert rel(Y, Yo) <= TOL_Y
 
 
 def test_two_parameter_amplitude_kernel(ph, po):
