@@ -50,6 +50,8 @@ void launch_coupling_reduce(cudaStream_t, const std::int32_t*, const std::int32_
 void launch_near_mvm(cudaStream_t, const RowItem*, int, const std::int64_t*, const std::int32_t*,
                      const std::int64_t*, const double*, const double*, double*);
 void launch_near_mvm_sym(cudaStream_t, const SymItem*, int, const double*, const double*, double*);
+void launch_near_mvm_symcsr(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
+                            double*);
 void launch_near_mrhs(cudaStream_t, const MrhsItem*, int, const std::int64_t*, const std::int32_t*,
                       const std::int64_t*, const std::int32_t*, const std::int32_t*, const double*, const double*,
                       std::int64_t, int, double*);
@@ -265,7 +267,7 @@ struct DevMatrix {
   bool sym = false;
   std::vector<char> near_trans;  // block stored as the transpose of its partner
   std::int64_t E_logical = 0;    // sum of n_sigma n_tau over local near blocks
-  DBuf sym_items, g_row0, g_rows, g_sbeg, g_segs, sym_part;
+  DBuf sym_items, sym_blocks, g_row0, g_rows, g_sbeg, g_segs, sym_part;
   int n_sym_items = 0, n_gather_leaves = 0;
   // K9 multi-RHS near field (DMMA), CSR by sigma over stored blocks
   DBuf k9_items, k9_tb, k9_tn, k9_doff, k9_ld, k9_tr;
@@ -455,9 +457,14 @@ std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const doub
     std::unordered_map<std::uint64_t, Index> where;
     auto key = [](int s, int t) { return (static_cast<std::uint64_t>(s) << 32) | static_cast<std::uint32_t>(t); };
     for (Index b = 0; b < nnear; ++b) where[key(H.blocks.near[b].sigma, H.blocks.near[b].tau)] = b;
+    // Owner of the pair {a, b}, a < b: a when a + b is even, b otherwise.
+    // Alternating by parity gives every leaf about half of its partners
+    // (a plain sigma < tau rule would give the first leaves all of them).
     for (Index b = 0; b < nnear; ++b) {
       const Block blk = H.blocks.near[b];
-      if (blk.sigma > blk.tau) {
+      if (blk.sigma == blk.tau) continue;
+      const bool owner = (blk.sigma < blk.tau) == (((blk.sigma + blk.tau) & 1) == 0);
+      if (!owner) {
         canon[b] = where.at(key(blk.tau, blk.sigma));
         M.near_trans[b] = 1;
       }
@@ -621,39 +628,49 @@ std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const doub
   }
 
   if (M.sym) {
-    // K6 on symmetric storage: one item per (stored block, 128-row chunk);
-    // partial segments gathered per leaf in near-list order.
-    std::vector<dev::SymItem> items;
+    // K6 on symmetric storage, CSR by owner leaf: one item per (leaf, 128-row
+    // chunk) over the stored blocks the leaf owns; partial segments are
+    // gathered per leaf in a fixed order.
+    std::vector<std::vector<Index>> owned(M.nnodes);
+    for (Index b = 0; b < nnear; ++b)
+      if (M.near_doff[b] >= 0 && !M.near_trans[b]) owned[H.blocks.near[b].sigma].push_back(b);
+    std::vector<dev::SymRowItem> items;
+    std::vector<dev::SymBlock> blocks;
     std::vector<std::vector<dev::GatherSeg>> segs_of(M.nnodes);
     std::int64_t poff = 0;
-    for (Index b = 0; b < nnear; ++b) {
-      if (M.near_doff[b] < 0 || M.near_trans[b]) continue;
-      const Block blk = H.blocks.near[b];
-      const TreeNode& s = T.nodes[blk.sigma];
-      const TreeNode& u = T.nodes[blk.tau];
-      const bool diag = blk.sigma == blk.tau;
-      const int ns = static_cast<int>(s.count), nt = static_cast<int>(u.count);
+    for (int s = 0; s < M.nnodes; ++s) {
+      if (owned[s].empty()) continue;
+      const int ns = static_cast<int>(T.nodes[s].count);
       for (int i0 = 0; i0 < ns; i0 += 128) {
-        dev::SymItem it{};
-        it.d_off = M.near_doff[b];
-        it.x_row0 = s.begin;
-        it.x_col0 = u.begin;
+        dev::SymRowItem it{};
+        it.x_row0 = T.nodes[s].begin + i0;
+        it.rows = std::min(128, ns - i0);
         it.ld = ns;
         it.i0 = i0;
-        it.rows = std::min(128, ns - i0);
-        it.ncol = nt;
-        it.diag = diag ? 1 : 0;
-        it.p_row = poff;
-        segs_of[blk.sigma].push_back({poff, i0, it.rows});
-        poff += it.rows;
-        if (!diag) {
-          it.p_col = poff;
-          segs_of[blk.tau].push_back({poff, 0, nt});
-          poff += nt;
+        it.bbeg = static_cast<std::int32_t>(blocks.size());
+        for (Index b : owned[s]) {
+          const int tau = H.blocks.near[b].tau;
+          const int nt = static_cast<int>(T.nodes[tau].count);
+          dev::SymBlock sb{};
+          sb.d_off = M.near_doff[b];
+          sb.x_col0 = T.nodes[tau].begin;
+          sb.ncol = nt;
+          sb.p_col = -1;
+          if (tau != s) {
+            sb.p_col = poff;
+            segs_of[tau].push_back({poff, 0, nt});
+            poff += nt;
+          }
+          blocks.push_back(sb);
         }
+        it.bend = static_cast<std::int32_t>(blocks.size());
+        it.p_row = poff;
+        segs_of[s].push_back({poff, i0, it.rows});
+        poff += it.rows;
         items.push_back(it);
       }
     }
+    upload(M.sym_blocks, blocks, st);
     std::vector<std::int64_t> lrow0;
     std::vector<std::int32_t> lrows, sbeg{0};
     std::vector<dev::GatherSeg> segs;
@@ -1189,8 +1206,9 @@ void apply_tree_order(DevInstance& I, Index m) {
   for (Index c = 0; c < (block_rhs ? 0 : m); ++c) {
     if (M.sym) {
       ctx.run("near_mvm", [&] {
-        dev::launch_near_mvm_sym(st, M.sym_items.as<dev::SymItem>(), M.n_sym_items, I.D.as<double>(),
-                                 M.xp.as<double>() + c * M.n, M.sym_part.as<double>());
+        dev::launch_near_mvm_symcsr(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
+                                    M.sym_blocks.as<dev::SymBlock>(), I.D.as<double>(), M.xp.as<double>() + c * M.n,
+                                    M.sym_part.as<double>());
       });
       ctx.run("near_gather", [&] {
         dev::launch_near_gather(st, M.n_gather_leaves, M.g_row0.as<std::int64_t>(), M.g_rows.as<std::int32_t>(),

@@ -885,6 +885,83 @@ __global__ void __launch_bounds__(128) k_near_mvm_sym2(const SymItem* __restrict
     sym_block<4>(it, D, xp, part, lane);
 }
 
+// CSR-by-sigma version: a CTA streams every stored block owned by its leaf
+// (ownership alternates by the parity of sigma + tau, which balances the
+// lists), so each warp keeps loads in flight across blocks and the row sums
+// stay in registers; per column the 8-warp split and a 5-shuffle reduction
+// give the column sum D^T x_sigma.
+__global__ void __launch_bounds__(256) k_near_mvm_symcsr(const SymRowItem* __restrict__ items,
+                                                         const SymBlock* __restrict__ blocks,
+                                                         const double* __restrict__ D, const double* __restrict__ xp,
+                                                         double* __restrict__ part) {
+  __shared__ double red[8][128];
+  const SymRowItem it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double racc[4] = {0.0, 0.0, 0.0, 0.0};
+  double xs[4];
+  bool live[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    live[q] = lane + 32 * q < it.rows;
+    xs[q] = live[q] ? xp[it.x_row0 + lane + 32 * q] : 0.0;
+  }
+  const std::int64_t ld = it.ld;
+  for (int b = it.bbeg; b < it.bend; ++b) {
+    const SymBlock blk = blocks[b];
+    const double* Db = D + blk.d_off + it.i0 + lane;
+    const double* xt = xp + blk.x_col0;
+    const bool diag = blk.p_col < 0;
+    int j = warp;
+    for (; j + 8 < blk.ncol; j += 16) {
+      const double x0 = xt[j], x1 = xt[j + 8];
+      double v0[4], v1[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        v0[q] = live[q] ? ld_stream(Db + j * ld + 32 * q) : 0.0;
+        v1[q] = live[q] ? ld_stream(Db + (j + 8) * ld + 32 * q) : 0.0;
+      }
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        racc[q] += v0[q] * x0 + v1[q] * x1;
+        c0 += v0[q] * xs[q];
+        c1 += v1[q] * xs[q];
+      }
+      if (!diag) {
+        c0 = warp_sum(c0);
+        c1 = warp_sum(c1);
+        if (lane == 0) {
+          part[blk.p_col + j] = c0;
+          part[blk.p_col + j + 8] = c1;
+        }
+      }
+    }
+    for (; j < blk.ncol; j += 8) {
+      const double x0 = xt[j];
+      double c0 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double v = live[q] ? ld_stream(Db + j * ld + 32 * q) : 0.0;
+        racc[q] += v * x0;
+        c0 += v * xs[q];
+      }
+      if (!diag) {
+        c0 = warp_sum(c0);
+        if (lane == 0) part[blk.p_col + j] = c0;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) red[warp][lane + 32 * q] = racc[q];
+  __syncthreads();
+  if (threadIdx.x < it.rows) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+    part[it.p_row + threadIdx.x] = s;
+  }
+}
+
 // y[rows of leaf] = sum of the leaf's partial segments, in list order.
 __global__ void k_near_gather(const std::int64_t* __restrict__ leaf_row0, const std::int32_t* __restrict__ leaf_rows,
                               const std::int32_t* __restrict__ seg_beg, const GatherSeg* __restrict__ segs,
@@ -1275,6 +1352,11 @@ void launch_near_mvm_sym(cudaStream_t st, const SymItem* items, int nitems, cons
   // k_near_mvm_sym2 (warp per block, transpose-reduce) measured 3.3x slower
   // than this CTA-per-block version at C3 (242 registers, low occupancy).
   k_near_mvm_sym<<<nitems, 256, 0, st>>>(items, D, xp, part);
+}
+void launch_near_mvm_symcsr(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks,
+                            const double* D, const double* xp, double* part) {
+  if (nitems == 0) return;
+  k_near_mvm_symcsr<<<nitems, 256, 0, st>>>(items, blocks, D, xp, part);
 }
 void launch_near_gather(cudaStream_t st, int nleaves, const std::int64_t* leaf_row0, const std::int32_t* leaf_rows,
                         const std::int32_t* seg_beg, const GatherSeg* segs, const double* part, double* yp) {

@@ -80,6 +80,17 @@ struct SymItem {
   std::int64_t d_off, x_row0, x_col0, p_row, p_col;
   std::int32_t ld, i0, rows, ncol, diag, pad;
 };
+// CSR form of the symmetric near GEMV: one item per (leaf sigma, 128-row
+// chunk) streaming all stored blocks owned by sigma; row sums accumulate
+// across those blocks, column sums are written per block.
+struct SymRowItem {
+  std::int64_t x_row0, p_row;
+  std::int32_t rows, ld, i0, bbeg, bend, pad;
+};
+struct SymBlock {
+  std::int64_t d_off, x_col0, p_col;  // p_col < 0: diagonal block
+  std::int32_t ncol, pad;
+};
 struct GatherSeg {  // contribution to rows [base, base + len) of one leaf
   std::int64_t poff;
   std::int32_t base, len;
