@@ -236,10 +236,11 @@ def run_ours(args):
     inst = ph.instantiate(pm, [thetas[0]])
 
     def step(s):
-        inst.reinstantiate([thetas[s % len(thetas)]])
         if world == 1:
-            inst.apply_device(x_dev.data_ptr(), y_dev.data_ptr(), 1)
+            # instantiate(theta_s) + MVM as one overlapped schedule
+            inst.instantiate_apply_device([thetas[s % len(thetas)]], x_dev.data_ptr(), y_dev.data_ptr(), 1)
         else:
+            inst.reinstantiate([thetas[s % len(thetas)]])
             inst.apply_rows_device(x_dev.data_ptr(), rg.send.data_ptr(), 1)
             yperm = rg.gather(rg.send)  # NCCL all-gather(v) of the row blocks
             ph.lib().phm_unpermute_device(pm._h, ph._P(yperm.data_ptr()), ph._P(y_dev.data_ptr()), 1)
@@ -302,9 +303,10 @@ def run_ours(args):
         from ctypes import c_double, POINTER
 
         def e2e_step(s):
-            inst.reinstantiate([thetas[s % len(thetas)]])
-            ph._check(ph.lib().phm_apply(inst._h, xh.ctypes.data_as(POINTER(c_double)), n,
-                                         yh.ctypes.data_as(POINTER(c_double)), 1))
+            th = np.array([thetas[s % len(thetas)]])
+            ph._check(ph.lib().phm_instantiate_apply(inst._h, th.ctypes.data_as(POINTER(c_double)), 1,
+                                                     xh.ctypes.data_as(POINTER(c_double)), n,
+                                                     yh.ctypes.data_as(POINTER(c_double)), 1))
 
         for s in range(args.warmup):
             e2e_step(s)

@@ -172,6 +172,13 @@ int phm_instance_class_c(phm_instance inst, int64_t cls, double* out /* P x P */
 /* y = K(theta) x, host buffers, n_rows must equal n (length check before
  * any launch, phmatrix.cpp:228); m right-hand sides, column-major. */
 int phm_apply(phm_instance inst, const double* x, int64_t n_rows, double* y, int64_t m);
+/* reinstantiate(theta) followed by apply(x) in one call (the HPO step): the
+ * class stage and the H^2 far chain overlap the near-field instantiate
+ * stream; results equal phm_reinstantiate + phm_apply. */
+int phm_instantiate_apply(phm_instance inst, const double* theta, int n_theta, const double* x, int64_t n_rows,
+                          double* y, int64_t m);
+int phm_instantiate_apply_device(phm_instance inst, const double* theta, int n_theta, const double* x_dev,
+                                 double* y_dev, int64_t m);
 /* Device buffers, asynchronous on the context stream. */
 int phm_apply_device(phm_instance inst, const double* x_dev, double* y_dev, int64_t m);
 /* Row-sharded apply: this shard's rows [row_begin, row_end) of y in tree

@@ -128,6 +128,8 @@ SIGNATURES = {
     "phm_instance_class_c": ([_P, C.c_int64, _DP], C.c_int),
     "phm_apply": ([_P, _DP, C.c_int64, _DP, C.c_int64], C.c_int),
     "phm_apply_device": ([_P, _P, _P, C.c_int64], C.c_int),
+    "phm_instantiate_apply": ([_P, _DP, C.c_int, _DP, C.c_int64, _DP, C.c_int64], C.c_int),
+    "phm_instantiate_apply_device": ([_P, _DP, C.c_int, _P, _P, C.c_int64], C.c_int),
     "phm_apply_rows_device": ([_P, _P, _P, C.c_int64], C.c_int),
     "phm_unpermute_device": ([_P, _P, _P, C.c_int64], C.c_int),
     "phm_to_dense": ([_P, _DP, C.c_int64], C.c_int),
@@ -466,6 +468,25 @@ class InstantiatedMatrix:
         y = np.empty((self.parent.n(), m), dtype=np.float64, order="F")
         _check(lib().phm_apply(self._h, xf.ctypes.data_as(_DP), n_rows, y.ctypes.data_as(_DP), m))
         return y[:, 0].copy() if vec else y
+
+    def instantiate_apply(self, theta, x) -> np.ndarray:
+        """reinstantiate(theta) then apply(x) as one overlapped schedule."""
+        th = _f64(theta).ravel()
+        xa = np.asarray(x, dtype=np.float64)
+        vec = xa.ndim == 1
+        n_rows = xa.shape[0]
+        m = 1 if vec else xa.shape[1]
+        xf = np.asfortranarray(xa.reshape(n_rows, m))
+        y = np.empty((self.parent.n(), m), dtype=np.float64, order="F")
+        _check(lib().phm_instantiate_apply(self._h, _dp(th), th.size, xf.ctypes.data_as(_DP), n_rows,
+                                           y.ctypes.data_as(_DP), m))
+        self.theta = list(th)
+        return y[:, 0].copy() if vec else y
+
+    def instantiate_apply_device(self, theta, x_ptr: int, y_ptr: int, m: int = 1) -> None:
+        th = _f64(theta).ravel()
+        _check(lib().phm_instantiate_apply_device(self._h, _dp(th), th.size, _P(x_ptr), _P(y_ptr), m))
+        self.theta = list(th)
 
     def apply_device(self, x_ptr: int, y_ptr: int, m: int = 1) -> None:
         _check(lib().phm_apply_device(self._h, _P(x_ptr), _P(y_ptr), m))

@@ -550,6 +550,31 @@ int phm_apply(phm_instance inst, const double* x, int64_t n_rows, double* y, int
     phm::apply_host(*inst->inst, x, y, m);
   });
 }
+int phm_instantiate_apply(phm_instance inst, const double* theta, int n_theta, const double* x, int64_t n_rows,
+                          double* y, int64_t m) {
+  return guarded([&] {
+    need(inst, "instance");
+    need(theta, "theta");
+    need(x, "x");
+    need(y, "y");
+    auto& H = const_cast<phm::HostMatrix&>(phm::matrix_host(*inst->m));
+    (void)phm::parametric_vectors(H.grids, theta, n_theta);  // domain check first
+    if (n_rows != H.n()) throw std::invalid_argument("mvm: length mismatch");
+    if (m < 1) throw std::invalid_argument("mvm: m must be >= 1");
+    phm::instantiate_apply_host(*inst->inst, theta, n_theta, x, y, m, &H.counters);
+  });
+}
+int phm_instantiate_apply_device(phm_instance inst, const double* theta, int n_theta, const double* x, double* y,
+                                 int64_t m) {
+  return guarded([&] {
+    need(inst, "instance");
+    need(theta, "theta");
+    need(x, "x");
+    need(y, "y");
+    auto& H = const_cast<phm::HostMatrix&>(phm::matrix_host(*inst->m));
+    phm::instantiate_apply_device(*inst->inst, theta, n_theta, x, y, m, &H.counters);
+  });
+}
 int phm_apply_device(phm_instance inst, const double* x, double* y, int64_t m) {
   return guarded([&] {
     need(inst, "instance");

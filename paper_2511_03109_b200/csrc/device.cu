@@ -141,6 +141,7 @@ struct Context {
     for (auto e : pool) cudaEventDestroy(e);
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (join_ev) cudaEventDestroy(join_ev);
+    if (aux_ev) cudaEventDestroy(aux_ev);
     if (side) cudaStreamDestroy(side);
     if (own) cudaStreamDestroy(own);
   }
@@ -177,7 +178,7 @@ struct Context {
   // Second stream for the H^2 far-field chain, which overlaps the near-field
   // GEMV (compute-bound DMMA next to an HBM stream); fork/join by events.
   cudaStream_t side = nullptr;
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, aux_ev = nullptr;
   void fork() {
     CK(cudaEventRecord(fork_ev, stream));
     CK(cudaStreamWaitEvent(side, fork_ev, 0));
@@ -217,6 +218,7 @@ std::shared_ptr<Context> context_create(int device) {
   CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->aux_ev, cudaEventDisableTiming));
   ctx->stream = ctx->own;
   return ctx;
 }
@@ -998,25 +1000,22 @@ std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const doub
 // ----------------------------------------------------------- instantiate
 namespace {
 
-void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCounters* counters) {
+// Class stage of instantiate: H_k(theta) and C_k = L_k H_k R_k^T (K2).
+void inst_classes(DevInstance& I, const dev::ThetaV& tv, cudaStream_t s) {
   DevMatrix& M = *I.M;
-  const HostMatrix& H = *M.hm;
-  Context& ctx = *M.ctx;
-  CK(cudaSetDevice(ctx.device));
-  cudaStream_t st = ctx.stream;
-  // theta box check before any launch (farfield.cpp:23-24)
-  const auto v = parametric_vectors(H.grids, theta, n_theta);
-  I.theta.assign(theta, theta + n_theta);
-  const dev::ThetaV tv = make_theta_v(v);
-
-  // far: H_k (and C_k) per class. (Overlapping it with the near stream on the
-  // side stream measured slower: its CTAs displace K1's and K1 lost 1.8 ms.)
-  ctx.run("class_inst", [&] {
-    dev::launch_class_inst(st, M.cmeta.as<dev::ClassMeta>(), M.ncls, M.class_mid.as<double>(),
+  M.ctx->run_on(s, "class_inst", [&] {
+    dev::launch_class_inst(s, M.cmeta.as<dev::ClassMeta>(), M.ncls, M.class_mid.as<double>(),
                            M.class_mid_dims.as<std::int32_t>(), M.class_L.as<double>(), M.class_R.as<double>(), tv, M.P,
                            M.h2, M.capA, M.capB, M.capT, I.H.as<double>(), I.C.as<double>());
   });
-  // near
+}
+
+// Near stage of instantiate: every stored D_b(theta) (K1).
+void inst_near(DevInstance& I, const double* theta, const std::vector<std::vector<double>>& v,
+               const dev::ThetaV& tv, cudaStream_t s, StageCounters* counters) {
+  DevMatrix& M = *I.M;
+  const HostMatrix& H = *M.hm;
+  Context& ctx = *M.ctx;
   if (M.mode == NearMode::Snapshot) {
     // w = v_shape (x) ... times the amplitude interpolant sum_j v_j s_j
     dev::ThetaV shape = tv;
@@ -1028,17 +1027,17 @@ void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCoun
       amp = 0.0;
       for (int j = 0; j < g.p; ++j) amp += v[spec.shape_params()][j] * g.nodes[j];
     }
-    ctx.run("near_w", [&] { dev::launch_set_vec(st, I.w.as<double>(), M.R_snap, shape, amp); });
-    ctx.run("near_inst", [&] {
-      dev::launch_inst_flat(st, M.G.as<double>(), M.E, M.R_snap, I.w.as<double>(), I.D.as<double>());
+    ctx.run_on(s, "near_w", [&] { dev::launch_set_vec(s, I.w.as<double>(), M.R_snap, shape, amp); });
+    ctx.run_on(s, "near_inst", [&] {
+      dev::launch_inst_flat(s, M.G.as<double>(), M.E, M.R_snap, I.w.as<double>(), I.D.as<double>());
     });
   } else if (M.mode == NearMode::TT) {
-    ctx.run("near_w", [&] {
-      dev::launch_near_w(st, M.near_w_meta.as<dev::NearW>(), M.n_near_local, M.near_cores.as<double>(),
+    ctx.run_on(s, "near_w", [&] {
+      dev::launch_near_w(s, M.near_w_meta.as<dev::NearW>(), M.n_near_local, M.near_cores.as<double>(),
                          M.near_core_dims.as<std::int32_t>(), tv, I.w.as<double>());
     });
-    ctx.run("near_inst", [&] {
-      dev::launch_inst_tiles(st, M.inst_tiles.as<dev::InstTile>(), M.n_inst_tiles, M.G.as<double>(),
+    ctx.run_on(s, "near_inst", [&] {
+      dev::launch_inst_tiles(s, M.inst_tiles.as<dev::InstTile>(), M.n_inst_tiles, M.G.as<double>(),
                              I.w.as<double>(), I.D.as<double>());
     });
   } else {
@@ -1047,14 +1046,28 @@ void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCoun
     for (int k = 0; k < H.cfg.spec.shape_params(); ++k) th[k] = theta[k];
     double amp = H.cfg.spec.amplitude ? theta[H.cfg.spec.shape_params()] : 1.0;
     if (!I.w.p) I.w.alloc(3 * sizeof(double));
-    CK(cudaMemcpyAsync(I.w.p, th.data(), 3 * sizeof(double), cudaMemcpyHostToDevice, st));
-    ctx.run("near_direct", [&] {
-      dev::launch_snapshot(st, M.snap_tiles.as<dev::SnapTile>(), M.n_snap_tiles, M.geo.as<dev::BlockGeom>(),
+    CK(cudaMemcpyAsync(I.w.p, th.data(), 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+    ctx.run_on(s, "near_direct", [&] {
+      dev::launch_snapshot(s, M.snap_tiles.as<dev::SnapTile>(), M.n_snap_tiles, M.geo.as<dev::BlockGeom>(),
                            M.pts.as<double>(), M.n, M.d, H.cfg.spec.family, 1, I.w.as<double>(), amp, I.D.as<double>());
     });
-    CK(cudaStreamSynchronize(st));  // th lives on this stack frame
+    CK(cudaStreamSynchronize(s));  // th lives on this stack frame
     if (counters) counters->online.add(static_cast<std::uint64_t>(M.E_raw));
   }
+}
+
+void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCounters* counters) {
+  DevMatrix& M = *I.M;
+  const HostMatrix& H = *M.hm;
+  CK(cudaSetDevice(M.ctx->device));
+  // theta box check before any launch (farfield.cpp:23-24)
+  const auto v = parametric_vectors(H.grids, theta, n_theta);
+  I.theta.assign(theta, theta + n_theta);
+  const dev::ThetaV tv = make_theta_v(v);
+  // (Overlapping the class stage with K1 on the side stream measured
+  // slower: its CTAs displaced K1's and K1 lost 1.8 ms.)
+  inst_classes(I, tv, M.ctx->stream);
+  inst_near(I, theta, v, tv, M.ctx->stream, counters);
 }
 
 }  // namespace
@@ -1134,70 +1147,70 @@ void instance_class_c(DevInstance& I, Index k, std::vector<double>& out) {
 // ------------------------------------------------------------------ apply
 namespace {
 
-// Computes this shard's rows of y in tree order into M.yp (n x m layout;
-// only rows [row_begin, row_end) are defined) from xp (tree order).
-void apply_tree_order(DevInstance& I, Index m) {
+// H^2 far-field chain on stream fs: forward (K3, K4), coupling (K5),
+// downward (K7 internal). Reads xp and C_k; writes yhat.
+void far_chain(DevInstance& I, Index m, cudaStream_t fs) {
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   Context& ctx = *M.ctx;
-  cudaStream_t st = ctx.stream;
   const int P = M.P;
   const int mm = static_cast<int>(m);
-  if (M.h2) {
-    // Far-field chain (forward, coupling, downward) on the side stream,
-    // concurrent with the near-field GEMV on the main stream.
-    ctx.fork();
-    cudaStream_t fs = ctx.side;
-    ctx.run_on(fs, "leaf_fwd", [&] {
-      dev::launch_leaf_fwd(fs, M.leaves_all.as<std::int32_t>(), M.n_leaves_all, M.node_begin.as<std::int64_t>(),
-                           M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, P, M.xp.as<double>(), mm,
-                           M.xhat.as<double>());
+  ctx.run_on(fs, "leaf_fwd", [&] {
+    dev::launch_leaf_fwd(fs, M.leaves_all.as<std::int32_t>(), M.n_leaves_all, M.node_begin.as<std::int64_t>(),
+                         M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, P, M.xp.as<double>(), mm,
+                         M.xhat.as<double>());
+  });
+  for (int l = H.tree->l_max - 1; l >= 0; --l) {
+    const auto r = M.up_range[l];
+    if (r.second == r.first) continue;
+    ctx.run_on(fs, "up", [&] {
+      dev::launch_up(fs, M.up_nodes.as<std::int32_t>() + r.first, r.second - r.first,
+                     M.node_first_child.as<std::int32_t>(), M.node_count.as<std::int32_t>(), M.Etr.as<double>(), M.d,
+                     M.ps, P, mm, M.xhat.as<double>());
     });
-    for (int l = H.tree->l_max - 1; l >= 0; --l) {
-      const auto r = M.up_range[l];
-      if (r.second == r.first) continue;
-      ctx.run_on(fs, "up", [&] {
-        dev::launch_up(fs, M.up_nodes.as<std::int32_t>() + r.first, r.second - r.first,
-                       M.node_first_child.as<std::int32_t>(), M.node_count.as<std::int32_t>(), M.Etr.as<double>(), M.d,
-                       M.ps, P, mm, M.xhat.as<double>());
-      });
-    }
-    CK(cudaMemsetAsync(M.yhat.p, 0, sizeof(double) * M.nnodes * P * m, fs));
-    if (M.cp_mma) {
-      for (int c = 0; c < mm; ++c) {
-        ctx.run_on(fs, "coupling", [&] {
-          dev::launch_coupling_mma(fs, M.cg_items.as<dev::CouplingItem>(), M.n_cg_items, M.cg_cls.as<std::int32_t>(),
-                                   M.cg_tau.as<std::int32_t>(), I.C.as<double>(), P, M.xhat.as<double>(), mm, c,
-                                   M.cg_partial.as<double>());
-        });
-        ctx.run_on(fs, "coupling_reduce", [&] {
-          dev::launch_coupling_reduce(fs, M.cg_grp_sigma.as<std::int32_t>(), M.cg_grp_items.as<std::int32_t>(),
-                                      M.n_cg_groups, M.cg_partial.as<double>(), P, mm, c, M.yhat.as<double>());
-        });
-      }
-    } else {
-      ctx.run_on(fs, "coupling", [&] {
-        dev::launch_coupling(fs, M.cp_sig.as<std::int32_t>(), M.n_cp_sig, M.cp_beg.as<std::int64_t>(),
-                             M.cp_tau.as<std::int32_t>(), M.cp_cls.as<std::int32_t>(), I.C.as<double>(), P, mm,
-                             M.xhat.as<double>(), M.yhat.as<double>());
-      });
-    }
-    for (int l = 1; l <= H.tree->l_max; ++l) {
-      const auto r = M.down_range[l];
-      if (r.second == r.first) continue;
-      ctx.run_on(fs, "down", [&] {
-        dev::launch_down(fs, M.down_nodes.as<std::int32_t>() + r.first, r.second - r.first,
-                         M.node_parent.as<std::int32_t>(), M.Etr.as<double>(), M.d, M.ps, P, mm, M.yhat.as<double>());
-      });
-    }
   }
+  CK(cudaMemsetAsync(M.yhat.p, 0, sizeof(double) * M.nnodes * P * m, fs));
+  if (M.cp_mma) {
+    for (int c = 0; c < mm; ++c) {
+      ctx.run_on(fs, "coupling", [&] {
+        dev::launch_coupling_mma(fs, M.cg_items.as<dev::CouplingItem>(), M.n_cg_items, M.cg_cls.as<std::int32_t>(),
+                                 M.cg_tau.as<std::int32_t>(), I.C.as<double>(), P, M.xhat.as<double>(), mm, c,
+                                 M.cg_partial.as<double>());
+      });
+      ctx.run_on(fs, "coupling_reduce", [&] {
+        dev::launch_coupling_reduce(fs, M.cg_grp_sigma.as<std::int32_t>(), M.cg_grp_items.as<std::int32_t>(),
+                                    M.n_cg_groups, M.cg_partial.as<double>(), P, mm, c, M.yhat.as<double>());
+      });
+    }
+  } else {
+    ctx.run_on(fs, "coupling", [&] {
+      dev::launch_coupling(fs, M.cp_sig.as<std::int32_t>(), M.n_cp_sig, M.cp_beg.as<std::int64_t>(),
+                           M.cp_tau.as<std::int32_t>(), M.cp_cls.as<std::int32_t>(), I.C.as<double>(), P, mm,
+                           M.xhat.as<double>(), M.yhat.as<double>());
+    });
+  }
+  for (int l = 1; l <= H.tree->l_max; ++l) {
+    const auto r = M.down_range[l];
+    if (r.second == r.first) continue;
+    ctx.run_on(fs, "down", [&] {
+      dev::launch_down(fs, M.down_nodes.as<std::int32_t>() + r.first, r.second - r.first,
+                       M.node_parent.as<std::int32_t>(), M.Etr.as<double>(), M.d, M.ps, P, mm, M.yhat.as<double>());
+    });
+  }
+}
+
+// Near-field product on stream st: writes this shard's rows of yp.
+void near_product(DevInstance& I, Index m, cudaStream_t st) {
+  DevMatrix& M = *I.M;
+  Context& ctx = *M.ctx;
+  const int mm = static_cast<int>(m);
   if ((M.sym ? M.n_gather_leaves : M.n_row_items) == 0 || M.n_k9_items == 0)
     CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
   // Block right-hand sides: the near product is a dense contraction, so it
   // runs on fp64 tensor cores (K9); single vectors stay on the HBM GEMV.
   const bool block_rhs = m >= kMrhsMin;
   if (block_rhs)
-    ctx.run("near_mrhs", [&] {
+    ctx.run_on(st, "near_mrhs", [&] {
       dev::launch_near_mrhs(st, M.k9_items.as<dev::MrhsItem>(), M.n_k9_items, M.k9_tb.as<std::int64_t>(),
                             M.k9_tn.as<std::int32_t>(), M.k9_doff.as<std::int64_t>(), M.k9_ld.as<std::int32_t>(),
                             M.k9_tr.as<std::int32_t>(), I.D.as<double>(), M.xp.as<double>(), M.n, mm,
@@ -1205,46 +1218,68 @@ void apply_tree_order(DevInstance& I, Index m) {
     });
   for (Index c = 0; c < (block_rhs ? 0 : m); ++c) {
     if (M.sym) {
-      ctx.run("near_mvm", [&] {
+      ctx.run_on(st, "near_mvm", [&] {
         dev::launch_near_mvm_symcsr(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
                                     M.sym_blocks.as<dev::SymBlock>(), I.D.as<double>(), M.xp.as<double>() + c * M.n,
                                     M.sym_part.as<double>());
       });
-      ctx.run("near_gather", [&] {
+      ctx.run_on(st, "near_gather", [&] {
         dev::launch_near_gather(st, M.n_gather_leaves, M.g_row0.as<std::int64_t>(), M.g_rows.as<std::int32_t>(),
                                 M.g_sbeg.as<std::int32_t>(), M.g_segs.as<dev::GatherSeg>(), M.sym_part.as<double>(),
                                 M.yp.as<double>() + c * M.n);
       });
     } else {
-      ctx.run("near_mvm", [&] {
+      ctx.run_on(st, "near_mvm", [&] {
         dev::launch_near_mvm(st, M.row_items.as<dev::RowItem>(), M.n_row_items, M.nb_tb.as<std::int64_t>(),
                              M.nb_tn.as<std::int32_t>(), M.nb_doff.as<std::int64_t>(), I.D.as<double>(),
                              M.xp.as<double>() + c * M.n, M.yp.as<double>() + c * M.n);
       });
     }
   }
+}
+
+// Far-field contribution added into yp on stream st: the leaf step of the
+// downward pass (H^2, after far_chain) or the S H T^T products (H form).
+void far_finish(DevInstance& I, Index m, cudaStream_t st) {
+  DevMatrix& M = *I.M;
+  const HostMatrix& H = *M.hm;
+  Context& ctx = *M.ctx;
+  const int mm = static_cast<int>(m);
   if (M.h2) {
-    ctx.join();
-    ctx.run("leaf_bwd", [&] {
+    ctx.run_on(st, "leaf_bwd", [&] {
       dev::launch_leaf_bwd(st, M.leaves_local.as<std::int32_t>(), M.n_leaves_local, M.node_begin.as<std::int64_t>(),
-                           M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, P, M.yhat.as<double>(),
-                           mm, H.row_begin, H.row_end, M.yp.as<double>());
+                           M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, M.P,
+                           M.yhat.as<double>(), mm, H.row_begin, H.row_end, M.yp.as<double>());
     });
-  } else {
-    for (int l = 0; l <= H.tree->l_max; ++l) {
-      const auto r = M.fh_level_range[l];
-      if (r.second == r.first) continue;
-      for (Index c = 0; c < m; ++c)
-        ctx.run("far_h", [&] {
-          dev::launch_far_h(st, M.fh_items.as<dev::FarHItem>() + r.first, r.second - r.first, M.fh_level_maxrows[l],
-                            M.fh_tb.as<std::int64_t>(), M.fh_tn.as<std::int32_t>(), M.fh_cls.as<std::int32_t>(),
-                            M.fh_soff.as<std::int64_t>(), M.fh_toff.as<std::int64_t>(),
-                            M.cmeta.as<dev::ClassMeta>(), M.fh_S.as<double>(), M.fh_T.as<double>(),
-                            I.H.as<double>(), M.xp.as<double>() + c * M.n, H.row_begin, H.row_end,
-                            M.yp.as<double>() + c * M.n);
-        });
-    }
+    return;
   }
+  for (int l = 0; l <= H.tree->l_max; ++l) {
+    const auto r = M.fh_level_range[l];
+    if (r.second == r.first) continue;
+    for (Index c = 0; c < m; ++c)
+      ctx.run_on(st, "far_h", [&] {
+        dev::launch_far_h(st, M.fh_items.as<dev::FarHItem>() + r.first, r.second - r.first, M.fh_level_maxrows[l],
+                          M.fh_tb.as<std::int64_t>(), M.fh_tn.as<std::int32_t>(), M.fh_cls.as<std::int32_t>(),
+                          M.fh_soff.as<std::int64_t>(), M.fh_toff.as<std::int64_t>(), M.cmeta.as<dev::ClassMeta>(),
+                          M.fh_S.as<double>(), M.fh_T.as<double>(), I.H.as<double>(), M.xp.as<double>() + c * M.n,
+                          H.row_begin, H.row_end, M.yp.as<double>() + c * M.n);
+      });
+  }
+}
+
+// Computes this shard's rows of y in tree order into M.yp (n x m layout;
+// only rows [row_begin, row_end) are defined) from xp (tree order). The H^2
+// far chain runs on the side stream, concurrent with the near GEMV.
+void apply_tree_order(DevInstance& I, Index m) {
+  DevMatrix& M = *I.M;
+  Context& ctx = *M.ctx;
+  if (M.h2) {
+    ctx.fork();
+    far_chain(I, m, ctx.side);
+  }
+  near_product(I, m, ctx.stream);
+  if (M.h2) ctx.join();
+  far_finish(I, m, ctx.stream);
 }
 
 }  // namespace
@@ -1270,6 +1305,55 @@ void apply_host(DevInstance& I, const double* x, double* y, Index m) {
   cudaStream_t st = M.st();
   CK(cudaMemcpyAsync(M.xdev.p, x, sizeof(double) * M.n * m, cudaMemcpyHostToDevice, st));
   apply_device(I, M.xdev.as<double>(), M.ydev.as<double>(), m);
+  CK(cudaMemcpyAsync(y, M.ydev.p, sizeof(double) * M.n * m, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+// instantiate(theta) followed by apply(x), scheduled as one graph of work:
+// the class stage and the whole H^2 far chain (compute-bound: K2, K3-K5, K7)
+// run on the side stream while K1 streams the near field on the main
+// stream; the near GEMV then waits for the gathered x and the far chain.
+// Results are identical to reinstantiate() + apply_device().
+void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, const double* x_dev, double* y_dev,
+                              Index m, StageCounters* counters) {
+  DevMatrix& M = *I.M;
+  const HostMatrix& H = *M.hm;
+  PHM_CHECK(m >= 1, "apply: m must be >= 1");
+  if (H.row_begin != 0 || H.row_end != M.n)
+    throw std::logic_error("fused instantiate+apply on a row shard: use the sharded apply");
+  CK(cudaSetDevice(M.ctx->device));
+  const auto v = parametric_vectors(H.grids, theta, n_theta);
+  const dev::ThetaV tv = make_theta_v(v);
+  ensure_workspace(M, m);
+  if (!M.h2 || M.mode == NearMode::Direct) {
+    run_instantiate(I, theta, n_theta, counters);
+    apply_device(I, x_dev, y_dev, m);
+    return;
+  }
+  I.theta.assign(theta, theta + n_theta);
+  Context& ctx = *M.ctx;
+  cudaStream_t st = ctx.stream, fs = ctx.side;
+  ctx.fork();  // side stream sees x (and everything before) as ready
+  ctx.run_on(fs, "gather", [&] { dev::launch_gather(fs, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
+  CK(cudaEventRecord(ctx.aux_ev, fs));
+  inst_classes(I, tv, fs);
+  far_chain(I, m, fs);
+  inst_near(I, theta, v, tv, st, counters);
+  CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
+  near_product(I, m, st);
+  ctx.join();
+  far_finish(I, m, st);
+  ctx.run("scatter", [&] { dev::launch_scatter(st, M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev); });
+}
+
+void instantiate_apply_host(DevInstance& I, const double* theta, int n_theta, const double* x, double* y, Index m,
+                            StageCounters* counters) {
+  DevMatrix& M = *I.M;
+  CK(cudaSetDevice(M.ctx->device));
+  ensure_workspace(M, m);
+  cudaStream_t st = M.st();
+  CK(cudaMemcpyAsync(M.xdev.p, x, sizeof(double) * M.n * m, cudaMemcpyHostToDevice, st));
+  instantiate_apply_device(I, theta, n_theta, M.xdev.as<double>(), M.ydev.as<double>(), m, counters);
   CK(cudaMemcpyAsync(y, M.ydev.p, sizeof(double) * M.n * m, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
 }

@@ -62,6 +62,12 @@ void instance_class_c(DevInstance& inst, Index cls, std::vector<double>& out);
 // order. Host variants copy in/out and synchronise; device variants are
 // asynchronous on the context stream.
 void apply_host(DevInstance& inst, const double* x, double* y, Index m);
+// instantiate(theta) then apply(x) as one schedule: the class stage and the
+// H^2 far chain overlap the near-field instantiate stream.
+void instantiate_apply_device(DevInstance& inst, const double* theta, int n_theta, const double* x_dev, double* y_dev,
+                              Index m, StageCounters* counters);
+void instantiate_apply_host(DevInstance& inst, const double* theta, int n_theta, const double* x, double* y, Index m,
+                            StageCounters* counters);
 void apply_device(DevInstance& inst, const double* x_dev, double* y_dev, Index m);
 // Sharded pieces: rows [row_begin, row_end) of y in tree order, and the
 // final un-permute of a gathered tree-order vector.

@@ -3,7 +3,9 @@
 // is laid out so each warp load instruction touches contiguous 256-512 B.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -1267,7 +1269,15 @@ void launch_snapshot(cudaStream_t st, const SnapTile* tiles, std::int64_t ntiles
 void launch_inst_flat(cudaStream_t st, const double* G, std::int64_t E, int R, const double* w, double* D) {
   const std::int64_t E4 = E / 4;
   if (E4 == 0) return;
-  const int grid = static_cast<int>(std::min<std::int64_t>((E4 + 255) / 256, 148 * 8));
+  // Grid of 148 x k resident CTAs (grid-stride). k = 4 leaves half of each
+  // SM's warp slots to the compute-bound far-field chain that runs on the
+  // side stream during the fused instantiate+apply; PHM_K1_CTAS overrides.
+  static const int per_sm = [] {
+    const char* e = std::getenv("PHM_K1_CTAS");
+    const int k = e ? std::atoi(e) : 4;
+    return k >= 1 && k <= 8 ? k : 4;
+  }();
+  const int grid = static_cast<int>(std::min<std::int64_t>((E4 + 255) / 256, 148 * per_sm));
   switch (R) {
     case 1: k_inst_flat<1><<<grid, 256, 0, st>>>(G, E, w, D); break;
     case 2: k_inst_flat<2><<<grid, 256, 0, st>>>(G, E, w, D); break;

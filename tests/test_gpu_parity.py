@@ -270,6 +270,26 @@ def test_row_sharded_apply_on_one_gpu(ph, fmt):
     assert rel(y, y_ref) <= 1e-13
 
 
+@pytest.mark.parametrize("fmt,mode", [("h2", "snapshot"), ("h2", "tt"), ("h", "snapshot")])
+def test_fused_instantiate_apply_equals_separate_calls(ph, po, fmt, mode):
+    pts = ph.generate_points(2000, 3, 14)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT if mode == "snapshot" else ph.NearMode.TT)
+    pm = ph.offline_h2(pts, cfg) if fmt == "h2" else ph.offline_h(pts, cfg)
+    inst = ph.instantiate(pm, [0.4])
+    x = ph.generate_normal(2000, 4)
+    X = np.stack([x, 2 * x, ph.generate_normal(2000, 5), x, x], axis=1)
+    for theta in ([0.11], [0.37]):
+        y_fused = inst.instantiate_apply(theta, x)
+        ref = ph.instantiate(pm, theta)
+        assert np.array_equal(y_fused, ref.apply(x))
+        assert np.array_equal(inst.instantiate_apply(theta, X), ref.apply(X))
+    om = po.from_product(pm, pts)
+    assert rel(inst.instantiate_apply([0.2], x), om.instantiate([0.2]).apply(x)) <= TOL_Y
+    with pytest.raises(ph.DomainError):
+        inst.instantiate_apply([0.9], x)
+
+
 def test_reinstantiate_in_place(ph, po):
     pts = ph.generate_points(2000, 3, 1)
     cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
