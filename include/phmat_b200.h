@@ -141,6 +141,16 @@ int phm_matrix_build(phm_context ctx, const double* points, int64_t n, int d, co
 /* Host-only build (no device): structure + offline TT data for inspection;
  * instantiate / apply on such a handle fail with PHM_ERR_LOGIC. */
 int phm_matrix_build_host(const double* points, int64_t n, int d, const phm_config* cfg, phm_matrix* out);
+/* HMAT v1 artifacts, byte-compatible with the reference's save_parametric /
+ * load_parametric_{h,h2} / artifact_is_h2 (serialize.cpp:108-294): load
+ * rebuilds and validates the tree and block lists, then uploads the stored
+ * TT data (threads = host threads for the L/R assembly, 0 = all). */
+int phm_matrix_load(phm_context ctx, const char* path, int threads, phm_matrix* out);
+int phm_matrix_load_host(const char* path, int threads, phm_matrix* out); /* no device (inspection) */
+int phm_matrix_save(phm_matrix m, const char* path);
+int phm_artifact_is_h2(const char* path, int* is_h2);
+/* The matrix's configuration (e.g. after phm_matrix_load). */
+int phm_matrix_config(phm_matrix m, phm_config* out);
 int phm_matrix_destroy(phm_matrix m);
 int phm_matrix_info(phm_matrix m, phm_info* info);
 /* Structure views (bit-exact with the reference's tree and block lists). */

@@ -105,6 +105,11 @@ SIGNATURES = {
     "phm_context_launches": ([_P, _I64P], C.c_int),
     "phm_matrix_build": ([_P, _DP, C.c_int64, C.c_int, C.POINTER(_Config), C.POINTER(_P)], C.c_int),
     "phm_matrix_build_host": ([_DP, C.c_int64, C.c_int, C.POINTER(_Config), C.POINTER(_P)], C.c_int),
+    "phm_matrix_load": ([_P, C.c_char_p, C.c_int, C.POINTER(_P)], C.c_int),
+    "phm_matrix_save": ([_P, C.c_char_p], C.c_int),
+    "phm_matrix_load_host": ([C.c_char_p, C.c_int, C.POINTER(_P)], C.c_int),
+    "phm_artifact_is_h2": ([C.c_char_p, C.POINTER(C.c_int)], C.c_int),
+    "phm_matrix_config": ([_P, C.POINTER(_Config)], C.c_int),
     "phm_matrix_destroy": ([_P], C.c_int),
     "phm_matrix_info": ([_P, C.POINTER(_Info)], C.c_int),
     "phm_matrix_perm": ([_P, _I32P], C.c_int),
@@ -555,6 +560,52 @@ def offline_structure(points, config: PHConfig, fmt: int = Format.H2) -> Paramet
     cfg = config.to_c(fmt)
     _check(lib().phm_matrix_build_host(_dp(p), p.shape[0], p.shape[1], C.byref(cfg), C.byref(h)))
     return ParametricMatrix(h, None, fmt, config, p.shape[0], p.shape[1])
+
+
+def _config_from_c(c: _Config) -> PHConfig:
+    box = [(c.theta_lo[k], c.theta_hi[k]) for k in range(c.d_theta)]
+    return PHConfig(spec=KernelSpec(c.family, box, bool(c.amplitude)), l_max=c.l_max, p_s=c.p_s,
+                    p_theta=[c.p_theta[k] for k in range(c.d_theta)], eps=c.eps, eta=c.eta, r_max_far=c.r_max_far,
+                    r_max_near=c.r_max_near, seed=c.seed, near_mode=c.near_mode,
+                    translation_cache=bool(c.translation_cache), threads=c.threads, shard_rank=c.shard_rank,
+                    shard_count=c.shard_count, symmetric_near=bool(c.symmetric_near))
+
+
+def load_parametric(path: str, ctx: Optional[Context] = None, threads: int = 0) -> ParametricMatrix:
+    """load_parametric_h / _h2 (phmatrix.hpp:160-164): HMAT v1 artifact
+    written by the reference's `phmat build --artifact` (or save_parametric)."""
+    ctx = ctx or Context.default()
+    h = _P()
+    _check(lib().phm_matrix_load(ctx._h, os.fsencode(path), threads, C.byref(h)))
+    c = _Config()
+    _check(lib().phm_matrix_config(h, C.byref(c)))
+    pm = ParametricMatrix(h, ctx, c.format, _config_from_c(c), 0, 0)
+    inf = pm.info()
+    pm._n, pm._d = inf["n"], inf["d"]
+    return pm
+
+
+def load_parametric_structure(path: str, threads: int = 0) -> ParametricMatrix:
+    """Host-only load of an HMAT v1 artifact (no GPU): structure + TT data."""
+    h = _P()
+    _check(lib().phm_matrix_load_host(os.fsencode(path), threads, C.byref(h)))
+    c = _Config()
+    _check(lib().phm_matrix_config(h, C.byref(c)))
+    pm = ParametricMatrix(h, None, c.format, _config_from_c(c), 0, 0)
+    inf = pm.info()
+    pm._n, pm._d = inf["n"], inf["d"]
+    return pm
+
+
+def save_parametric(pm: ParametricMatrix, path: str) -> None:
+    """save_parametric (phmatrix.hpp:157-158), HMAT v1."""
+    _check(lib().phm_matrix_save(pm._h, os.fsencode(path)))
+
+
+def artifact_is_h2(path: str) -> bool:
+    v = C.c_int()
+    _check(lib().phm_artifact_is_h2(os.fsencode(path), C.byref(v)))
+    return bool(v.value)
 
 
 def instantiate(pm: ParametricMatrix, theta) -> InstantiatedMatrix:

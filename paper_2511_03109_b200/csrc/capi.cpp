@@ -286,6 +286,74 @@ int phm_matrix_build_host(const double* points, int64_t n, int d, const phm_conf
     *out = m.release();
   });
 }
+int phm_matrix_load(phm_context ctx, const char* path, int threads, phm_matrix* out) {
+  return guarded([&] {
+    need(ctx, "context");
+    need(path, "path");
+    need(out, "out");
+    auto m = std::make_unique<phm_matrix_s>();
+    m->ctx = ctx->ctx;
+    m->m = phm::matrix_load(ctx->ctx, path, threads);
+    *out = m.release();
+  });
+}
+int phm_matrix_load_host(const char* path, int threads, phm_matrix* out) {
+  return guarded([&] {
+    need(path, "path");
+    need(out, "out");
+    auto m = std::make_unique<phm_matrix_s>();
+    m->m = phm::matrix_load_host_only(path, threads);
+    *out = m.release();
+  });
+}
+int phm_matrix_save(phm_matrix m, const char* path) {
+  return guarded([&] {
+    need(m, "matrix");
+    need(path, "path");
+    if (!phm::matrix_on_device(*m->m) && phm::matrix_host(*m->m).cfg.near_mode == phm::NearMode::Snapshot)
+      throw std::logic_error("snapshot near data lives on the device; save from a device matrix");
+    phm::matrix_save(*m->m, path);
+  });
+}
+int phm_matrix_config(phm_matrix m, phm_config* out) {
+  return guarded([&] {
+    need(m, "matrix");
+    need(out, "out");
+    const phm::Config& c = phm::matrix_host(*m->m).cfg;
+    phm_config_default(out);
+    out->family = c.spec.family;
+    out->amplitude = c.spec.amplitude ? 1 : 0;
+    out->d_theta = c.spec.d_theta();
+    for (int k = 0; k < c.spec.d_theta(); ++k) {
+      out->theta_lo[k] = c.spec.box[k].lo;
+      out->theta_hi[k] = c.spec.box[k].hi;
+      out->p_theta[k] = c.p_theta.size() == 1 ? c.p_theta[0] : c.p_theta[k];
+    }
+    out->format = c.format == phm::Format::H2 ? PHM_FORMAT_H2 : PHM_FORMAT_H;
+    out->l_max = c.l_max;
+    out->p_s = c.p_s;
+    out->near_mode = c.near_mode == phm::NearMode::Direct     ? PHM_NEAR_DIRECT
+                     : c.near_mode == phm::NearMode::Snapshot ? PHM_NEAR_SNAPSHOT
+                                                              : PHM_NEAR_TT;
+    out->eps = c.eps;
+    out->eta = c.eta;
+    out->r_max_far = c.r_max_far;
+    out->r_max_near = c.r_max_near;
+    out->seed = c.seed;
+    out->translation_cache = c.translation_cache ? 1 : 0;
+    out->threads = c.threads;
+    out->shard_rank = c.shard_rank;
+    out->shard_count = c.shard_count;
+    out->symmetric_near = c.symmetric_near ? 1 : 0;
+  });
+}
+int phm_artifact_is_h2(const char* path, int* is_h2) {
+  return guarded([&] {
+    need(path, "path");
+    need(is_h2, "out");
+    *is_h2 = phm::artifact_is_h2(path) ? 1 : 0;
+  });
+}
 int phm_matrix_destroy(phm_matrix m) {
   return guarded([&] { delete m; });
 }

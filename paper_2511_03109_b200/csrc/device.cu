@@ -392,17 +392,67 @@ void matrix_near_column(const DevMatrix& m, Index b, Index kap, double* out) {
     for (Index i = 0; i < ns; ++i) out[i + j * ns] = m.near_trans[b] ? tmp[j + i * nt] : tmp[i + j * ns];
 }
 
+std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::unique_ptr<HostMatrix> hm);
+
 std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const double* points, Index n, int d,
                                         const Config& cfg) {
+  CK(cudaSetDevice(ctx->device));
+  if (cfg.spec.family == kMatern && cfg.near_mode == NearMode::Direct)
+    throw std::invalid_argument("direct near mode needs a closed-form kernel family on the GPU");
+  return matrix_upload(ctx, build_host(points, n, d, cfg));
+}
+
+void matrix_save(const DevMatrix& M, const std::string& path) {
+  const HostMatrix& H = *M.hm;
+  const Tree& T = *H.tree;
+  write_artifact(H, path, [&](Index b) {
+    if (H.cfg.near_mode == NearMode::TT) return H.near_tt[b];
+    // Snapshot mode: the full-rank NearBlockTT (G1 = the R snapshot columns,
+    // identity theta cores), SURVEY.md §8(a).
+    const Block blk = H.blocks.near[b];
+    const Index N = T.nodes[blk.sigma].count * T.nodes[blk.tau].count;
+    const Index R = matrix_near_rank(M, b);
+    TTTensor tt;
+    TTCore g1 = TTCore::zeros(1, N, R);
+    for (Index k = 0; k < R; ++k) matrix_near_column(M, b, k, g1.data.data() + k * N);
+    tt.cores.push_back(std::move(g1));
+    Index rin = R;
+    for (const Grid1D& g : H.grids.grids) {
+      const Index p = g.p;
+      TTCore c = TTCore::zeros(rin, p, rin / p);
+      for (Index rest = 0; rest < rin / p; ++rest)
+        for (Index j = 0; j < p; ++j) c.data[(j + p * rest) + j * c.r0 + rest * c.r0 * c.m] = 1.0;
+      tt.cores.push_back(std::move(c));
+      rin /= p;
+    }
+    return tt;
+  });
+}
+
+std::shared_ptr<DevMatrix> matrix_load_host_only(const std::string& path, int threads) {
+  auto M = std::make_shared<DevMatrix>();
+  M->hm = read_artifact(path, threads);
+  M->n = M->hm->n();
+  M->d = M->hm->d();
+  return M;
+}
+
+std::shared_ptr<DevMatrix> matrix_load(std::shared_ptr<Context> ctx, const std::string& path, int threads) {
+  CK(cudaSetDevice(ctx->device));
+  return matrix_upload(ctx, read_artifact(path, threads));
+}
+
+std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::unique_ptr<HostMatrix> hm) {
   CK(cudaSetDevice(ctx->device));
   auto Mp = std::make_shared<DevMatrix>();
   DevMatrix& M = *Mp;
   M.ctx = ctx;
-  if (cfg.near_mode == NearMode::Snapshot || cfg.near_mode == NearMode::Direct) {
-    if (cfg.spec.family == kMatern && cfg.near_mode == NearMode::Direct)
-      throw std::invalid_argument("direct near mode needs a closed-form kernel family on the GPU");
-  }
-  M.hm = build_host(points, n, d, cfg);
+  M.hm = std::move(hm);
+  const Config& cfg = M.hm->cfg;
+  const Index n = M.hm->n();
+  const int d = M.hm->d();
+  if (cfg.spec.family == kMatern && cfg.near_mode == NearMode::Direct)
+    throw std::invalid_argument("direct near mode needs a closed-form kernel family on the GPU");
   const auto t_up = std::chrono::steady_clock::now();
   HostMatrix& H = *M.hm;
   const Tree& T = *H.tree;

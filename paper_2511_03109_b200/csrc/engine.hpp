@@ -30,6 +30,12 @@ std::int64_t context_launches(Context& ctx);  // kernels launched so far
 // NearMode::Snapshot the GPU snapshot generator (K11).
 std::shared_ptr<DevMatrix> matrix_build(std::shared_ptr<Context> ctx, const double* points, Index n, int d,
                                         const Config& cfg);
+// HMAT v1 artifact (proj/src/serialize.cpp format): load = rebuild +
+// validate the structure, take the stored TT data, upload; save writes the
+// reference-readable file (snapshot near data as full-rank TTs).
+std::shared_ptr<DevMatrix> matrix_load(std::shared_ptr<Context> ctx, const std::string& path, int threads);
+void matrix_save(const DevMatrix& m, const std::string& path);
+std::shared_ptr<DevMatrix> matrix_load_host_only(const std::string& path, int threads);
 // Host-only build: structure and offline TT data, no device (CPU tests).
 std::shared_ptr<DevMatrix> matrix_build_host_only(const double* points, Index n, int d, const Config& cfg);
 bool matrix_on_device(const DevMatrix& m);

@@ -217,6 +217,8 @@ bool robust_cross(const EntryFn& f, const CrossOptions& co, CrossResult& r) {
 
 }  // namespace
 
+void assemble_lr_public(const Coupling& cp, Mat& L, Mat& R) { assemble_lr(cp, L, R); }
+
 Index HostMatrix::P() const {
   Index p = 1;
   for (int k = 0; k < tree->d; ++k) p *= cfg.p_s;

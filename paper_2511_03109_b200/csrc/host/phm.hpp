@@ -311,6 +311,13 @@ struct HostMatrix {
 
 // Offline build on the host (everything except GPU snapshot generation).
 std::unique_ptr<HostMatrix> build_host(const double* points, Index n, int d, const Config& cfg);
+// Explicit L (P x r_d) and R (P x r_{d+dt}) of a coupling (farfield.cpp:157-184).
+void assemble_lr_public(const Coupling& cp, Mat& L, Mat& R);
+
+// HMAT v1 artifacts, byte-compatible with proj/src/serialize.cpp.
+bool artifact_is_h2(const std::string& path);
+void write_artifact(const HostMatrix& M, const std::string& path, const std::function<TTTensor(Index)>& near_tt);
+std::unique_ptr<HostMatrix> read_artifact(const std::string& path, int threads);
 
 // Seeded generators (harness.cpp:174-181 and the new mixture generator).
 void generate_points(Index n, int d, std::uint64_t seed, double* out);

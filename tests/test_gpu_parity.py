@@ -290,6 +290,31 @@ def test_fused_instantiate_apply_equals_separate_calls(ph, po, fmt, mode):
         inst.instantiate_apply([0.9], x)
 
 
+def test_artifact_round_trip_on_device(ph, tmp_path):
+    """test_phmatrix.cpp:289-323: save -> load preserves the instantiated
+    matrices (bitwise for TT mode; snapshot mode is written as full-rank TTs
+    and reloads into the TT path with identical D_b)."""
+    pts = ph.generate_points(1500, 3, 77)
+    for mode in (ph.NearMode.TT, ph.NearMode.SNAPSHOT):
+        cfg = ph.PHConfig(spec=ph.KernelSpec.default(ph.Family.MC), l_max=2, p_s=4, p_theta=5, eps=1e-4,
+                          near_mode=mode)
+        pm = ph.offline_h2(pts, cfg)
+        path = str(tmp_path / f"a{mode}.phm")
+        ph.save_parametric(pm, path)
+        lm = ph.load_parametric(path)
+        x = ph.generate_normal(1500, 2)
+        a, b = ph.instantiate(pm, [0.63]), ph.instantiate(lm, [0.63])
+        near, _, _ = pm.blocks()
+        sizes = _node_sizes(pm)
+        for k in range(0, len(near), 9):
+            s, t = near[k]
+            assert np.array_equal(a.near_d(k, (sizes[s], sizes[t])), b.near_d(k, (sizes[s], sizes[t])))
+        if mode == ph.NearMode.TT:
+            assert np.array_equal(a.apply(x), b.apply(x))
+        else:
+            assert rel(a.apply(x), b.apply(x)) <= 1e-14
+
+
 def test_reinstantiate_in_place(ph, po):
     pts = ph.generate_points(2000, 3, 1)
     cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
