@@ -38,6 +38,10 @@ CONFIGS = {
     # BASELINE.json configs[0] (CPU-runnable PR1 case; param-H)
     "c1": dict(n=4096, d=2, family="gauss", box=(0.1, 1.0), l_max=3, p_s=6, p_theta=8, eta=1.0, fmt="h",
                points="uniform"),
+    # BASELINE.json configs[4] (C5): the C3 matrix, 4096 thetas sharded over
+    # GPUs with no communication, each instantiated and applied to 10 vectors
+    "c5": dict(n=262144, d=3, family="e", box=(0.05, 0.5), l_max=4, p_s=4, p_theta=8, eta=1.0, fmt="h2",
+               points="uniform", sweep=True, rhs=10, n_theta=4096),
 }
 
 
@@ -51,6 +55,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=16, help="1/f of near/far blocks timed on the CPU")
+    ap.add_argument("--rhs", type=int, default=0, help="right-hand sides per MVM (default: the config's)")
     return ap.parse_args()
 
 
@@ -211,6 +216,11 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = CONFIGS[args.config]
+    sweep = c.get("sweep", False)          # C5: thetas sharded over ranks, no communication
+    m = args.rhs or c.get("rhs", 1)        # right-hand sides per MVM
+    row_shard = world > 1 and not sweep    # C3 at N GPUs: leaf rows sharded, y all-gathered
+    if row_shard and m != 1:
+        raise SystemExit("row-sharded bench supports one right-hand side")
     ctx = ph.Context(local)
     # A real (non-legacy) stream shared by torch (events, NCCL ordering) and
     # every kernel the library launches.
@@ -218,29 +228,33 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     pts = make_points(ph, c, args.seed)
-    cfg = make_cfg(ph, c, rank, world)
+    cfg = make_cfg(ph, c, rank if row_shard else 0, world if row_shard else 1)
     t0 = time.time()
     pm = ph.offline_h2(pts, cfg, ctx) if c["fmt"] == "h2" else ph.offline_h(pts, cfg, ctx)
     build_s = time.time() - t0
     info = pm.info()
     n = c["n"]
-    thetas = theta_draws(c["box"][0], c["box"][1], 32, args.seed)
-    x_host = torch.from_numpy(ph.generate_normal(n, args.seed + 1)).pin_memory()
+    thetas = theta_draws(c["box"][0], c["box"][1], c.get("n_theta", 32), args.seed)
+    xs = np.stack([ph.generate_normal(n, args.seed + 1 + j) for j in range(m)])  # (m, n) = column-major n x m
+    x_host = torch.from_numpy(xs).pin_memory()
     x_dev = x_host.cuda()
-    y_dev = torch.empty(n, dtype=torch.float64, device="cuda")
+    y_dev = torch.empty((m, n), dtype=torch.float64, device="cuda")
     rows = info["row_end"] - info["row_begin"]
-    if world > 1:
+    if row_shard:
         from paper_2511_03109_b200.dist import RowGather, row_counts
 
         rg = RowGather(row_counts(rows), 1, device="cuda")
     inst = ph.instantiate(pm, [thetas[0]])
 
+    def theta_of(s):
+        return thetas[(s * world + rank) % len(thetas)] if sweep else thetas[s % len(thetas)]
+
     def step(s):
-        if world == 1:
+        if not row_shard:
             # instantiate(theta_s) + MVM as one overlapped schedule
-            inst.instantiate_apply_device([thetas[s % len(thetas)]], x_dev.data_ptr(), y_dev.data_ptr(), 1)
+            inst.instantiate_apply_device([theta_of(s)], x_dev.data_ptr(), y_dev.data_ptr(), m)
         else:
-            inst.reinstantiate([thetas[s % len(thetas)]])
+            inst.reinstantiate([theta_of(s)])
             inst.apply_rows_device(x_dev.data_ptr(), rg.send.data_ptr(), 1)
             yperm = rg.gather(rg.send)  # NCCL all-gather(v) of the row blocks
             ph.lib().phm_unpermute_device(pm._h, ph._P(yperm.data_ptr()), ph._P(y_dev.data_ptr()), 1)
@@ -270,8 +284,8 @@ def run_ours(args):
     ms = ev0.elapsed_time(ev1)
     k1_ms, k1_n = ctx.timer("near_inst")
     timers = {}
-    for name in ("near_inst", "class_inst", "near_w", "near_mvm", "coupling", "leaf_fwd", "up", "down",
-                 "leaf_bwd", "gather", "scatter", "far_h"):
+    for name in ("near_inst", "class_inst", "near_w", "near_mvm", "near_gather", "near_mrhs", "coupling",
+                 "coupling_reduce", "leaf_fwd", "up", "down", "leaf_bwd", "gather", "scatter", "far_h"):
         t, cnt = ctx.timer(name)
         if cnt:
             timers[name] = {"ms_per_launch": t / cnt, "launches": cnt}
@@ -288,25 +302,26 @@ def run_ours(args):
         return a.elapsed_time(b) / args.steps
 
     # phase split of the same step (same stream, CUDA events)
-    inst_ms = time_loop(lambda s: inst.reinstantiate([thetas[s % len(thetas)]]))
-    apply_ms = time_loop(lambda s: inst.apply_device(x_dev.data_ptr(), y_dev.data_ptr(), 1)) if world == 1 else None
+    inst_ms = time_loop(lambda s: inst.reinstantiate([theta_of(s)]))
+    apply_ms = (time_loop(lambda s: inst.apply_device(x_dev.data_ptr(), y_dev.data_ptr(), m))
+                if not row_shard else None)
     t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms = float(t_max.item())
 
-    # e2e through the public API with host buffers (rank-local; N=1 path)
+    # e2e through the public API with host buffers (rank-local)
     e2e = None
-    if world == 1:
-        y_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    if not row_shard:
+        y_host = torch.empty((m, n), dtype=torch.float64).pin_memory()
         xh, yh = x_host.numpy(), y_host.numpy()
-        from ctypes import c_double, POINTER
+        from ctypes import POINTER, c_double
 
         def e2e_step(s):
-            th = np.array([thetas[s % len(thetas)]])
+            th = np.array([theta_of(s)])
             ph._check(ph.lib().phm_instantiate_apply(inst._h, th.ctypes.data_as(POINTER(c_double)), 1,
                                                      xh.ctypes.data_as(POINTER(c_double)), n,
-                                                     yh.ctypes.data_as(POINTER(c_double)), 1))
+                                                     yh.ctypes.data_as(POINTER(c_double)), m))
 
         for s in range(args.warmup):
             e2e_step(s)
@@ -318,11 +333,15 @@ def run_ours(args):
         b.record(stream)
         torch.cuda.synchronize()
         e_ms = a.elapsed_time(b)
-        e2e = {"value": args.steps * 1000.0 / e_ms, "unit": "theta/s", "h2d_bytes_per_step": 8 * n + 8,
-               "d2h_bytes_per_step": 8 * n}
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": (world if sweep else 1) * args.steps * 1000.0 / e_ms, "unit": "theta/s",
+               "h2d_bytes_per_step": 8 * n * m + 8, "d2h_bytes_per_step": 8 * n * m}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and c["fmt"] == "h2" and m == 1:
         host_pm = ph.offline_structure(pts, make_cfg(ph, c))
         cpu = cpu_baseline(ph, c, pts, host_pm, 3, args.cpu_sample, args.seed)
 
@@ -337,25 +356,38 @@ def run_ours(args):
             cls_bytes += 8 * (mid.size + info["P"] * (rl + rr) + rl * rr + info["P"] ** 2)
         b_inst, b_mvm = algorithmic_bytes(info, c, cls_bytes)
         k1_avg = k1_ms / max(1, k1_n)
-        k1_bytes = 8 * info["near_stream_elems"]  # read R+1 slabs... (R reads + 1 write) per near entry
+        k1_bytes = 8 * info["near_stream_elems"]  # R slab reads + 1 write per stored near entry
         achieved = k1_bytes / (k1_avg * 1e-3) / 1e9
         mvm_ms = apply_ms
+        # fp64 tensor-core (DMMA) work of the MVM: coupling GEMMs and, for
+        # block right-hand sides, the near-field contraction
+        cp = timers.get("coupling")
+        k9 = timers.get("near_mrhs")
+        dmma = {
+            "coupling_tflops": (2.0 * info["n_far"] * info["P"] ** 2 * m / (cp["ms_per_launch"] * 1e-3) / 1e12)
+            if cp else None,
+            "near_mrhs_tflops": (2.0 * info["near_entries"] * m / (k9["ms_per_launch"] * 1e-3) / 1e12) if k9 else None,
+        }
+        what = ("theta/s (instantiate + %d-RHS H2 MVM per theta), theta sweep sharded over GPUs" % m if sweep else
+                "theta-instantiations/s (instantiate + H2 MVM per theta) at n=2^18, 3D" if m == 1 else
+                "theta/s (instantiate + %d-RHS H2 MVM per theta) at n=2^18, 3D" % m)
         line = {
-            "metric": "theta-instantiations/s (instantiate + H2 MVM per theta) at n=2^18, 3D",
-            "value": args.steps * 1000.0 / ms,  # every rank processes the same thetas (rows sharded)
+            "metric": what,
+            "value": (world if sweep else 1) * args.steps * 1000.0 / ms,
             "unit": "theta/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": ms / args.steps,
             "higher_is_better": True,
-            "scaling": "strong",
+            "scaling": "weak" if sweep else "strong",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded uniform points, harness theta draws, x~N(0,1))",
             "config": {"workload": f"{args.config}: n={n} d={c['d']} {c['fmt']} kernel={c['family']} "
                                    f"l_max={c['l_max']} p_s={c['p_s']} p_theta={c['p_theta']} eta={c['eta']} "
-                                   f"near=snapshot", "rows_sharded_over": world,
+                                   f"near=snapshot rhs={m}",
+                       "parallelism": ("theta-sharded replicas" if sweep else f"rows sharded over {world}"),
                        "l2": "inputs (near snapshots) larger than L2; no flush needed"},
             "roofline": {"bound": "hbm", "kernel": "k_inst_flat (K1 near instantiate)", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
@@ -365,6 +397,7 @@ def run_ours(args):
             "mvm": {"ms": mvm_ms, "algorithmic_bytes": b_mvm,
                     "GB_s": b_mvm / (mvm_ms * 1e-3) / 1e9 if mvm_ms else None,
                     "frac_of_hbm": (b_mvm / (mvm_ms * 1e-3) / 1e9) / peak if mvm_ms else None},
+            "dmma": dmma,
             "instantiate_algorithmic_bytes": b_inst,
             "kernels": timers,
             "gpu_launches": launches,

@@ -44,8 +44,8 @@ void launch_coupling(cudaStream_t, const std::int32_t*, int, const std::int64_t*
                      const std::int32_t*, const double*, int, int, const double*, double*);
 bool coupling_mma_supported(int P);
 void launch_coupling_mma(cudaStream_t, const CouplingItem*, int, const std::int32_t*, const std::int32_t*,
-                         const double*, int, const double*, int, int, double*);
-void launch_coupling_reduce(cudaStream_t, const std::int32_t*, const std::int32_t*, int, const double*, int, int, int,
+                         const double*, int, const double*, int, double*);
+void launch_coupling_reduce(cudaStream_t, const std::int32_t*, const std::int32_t*, int, const double*, int, int,
                             double*);
 void launch_near_mvm(cudaStream_t, const RowItem*, int, const std::int64_t*, const std::int32_t*,
                      const std::int64_t*, const double*, const double*, double*);
@@ -1221,17 +1221,17 @@ void far_chain(DevInstance& I, Index m, cudaStream_t fs) {
   }
   CK(cudaMemsetAsync(M.yhat.p, 0, sizeof(double) * M.nnodes * P * m, fs));
   if (M.cp_mma) {
-    for (int c = 0; c < mm; ++c) {
-      ctx.run_on(fs, "coupling", [&] {
-        dev::launch_coupling_mma(fs, M.cg_items.as<dev::CouplingItem>(), M.n_cg_items, M.cg_cls.as<std::int32_t>(),
-                                 M.cg_tau.as<std::int32_t>(), I.C.as<double>(), P, M.xhat.as<double>(), mm, c,
-                                 M.cg_partial.as<double>());
-      });
-      ctx.run_on(fs, "coupling_reduce", [&] {
-        dev::launch_coupling_reduce(fs, M.cg_grp_sigma.as<std::int32_t>(), M.cg_grp_items.as<std::int32_t>(),
-                                    M.n_cg_groups, M.cg_partial.as<double>(), P, mm, c, M.yhat.as<double>());
-      });
-    }
+    const size_t need = sizeof(double) * std::max(1, M.n_cg_items) * m * dev::kGroupSlots * P;
+    if (M.cg_partial.bytes < need) M.cg_partial.alloc(need);
+    ctx.run_on(fs, "coupling", [&] {
+      dev::launch_coupling_mma(fs, M.cg_items.as<dev::CouplingItem>(), M.n_cg_items, M.cg_cls.as<std::int32_t>(),
+                               M.cg_tau.as<std::int32_t>(), I.C.as<double>(), P, M.xhat.as<double>(), mm,
+                               M.cg_partial.as<double>());
+    });
+    ctx.run_on(fs, "coupling_reduce", [&] {
+      dev::launch_coupling_reduce(fs, M.cg_grp_sigma.as<std::int32_t>(), M.cg_grp_items.as<std::int32_t>(),
+                                  M.n_cg_groups, M.cg_partial.as<double>(), P, mm, M.yhat.as<double>());
+    });
   } else {
     ctx.run_on(fs, "coupling", [&] {
       dev::launch_coupling(fs, M.cp_sig.as<std::int32_t>(), M.n_cp_sig, M.cp_beg.as<std::int64_t>(),

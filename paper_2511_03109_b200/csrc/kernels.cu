@@ -509,32 +509,42 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int P>
+// MC right-hand-side columns per CTA share every C_k fragment load
+// (grid.y walks the column chunks); X holds MC gathered 32-slot panels.
+template <int P, int MC>
 __global__ void __launch_bounds__(P / 16 * 32) k_coupling_mma(const CouplingItem* __restrict__ items,
                                                               const std::int32_t* __restrict__ item_cls,
                                                               const std::int32_t* __restrict__ cls_tau,
                                                               const double* __restrict__ C,
-                                                              const double* __restrict__ xhat, int m, int col,
+                                                              const double* __restrict__ xhat, int m,
                                                               double* __restrict__ partial) {
   constexpr int LD = P + 4;           // conflict-free B-fragment reads
   constexpr int KS = P / 4;           // k-steps of the m16n8k4 MMA
   constexpr int NT = kGroupSlots / 8; // n-tiles of 8 slots
-  extern __shared__ double smem[];    // 2 x [32][LD]
+  constexpr int PANEL = kGroupSlots * LD;
+  extern __shared__ double smem[];    // 2 stages x MC panels of [32][LD]
   const CouplingItem it = items[blockIdx.x];
+  const int col0 = blockIdx.y * MC;
+  const int ncol = min(MC, m - col0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t0 = lane & 3;
   const int row0 = warp * 16;
-  double acc[NT][4];
+  double acc[MC][NT][4];
 #pragma unroll
-  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+  for (int c = 0; c < MC; ++c)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[c][j][0] = acc[c][j][1] = acc[c][j][2] = acc[c][j][3] = 0.0;
 
   auto gather = [&](int e, int buf) {
-    double* X = smem + buf * kGroupSlots * LD;
     const std::int32_t* taus = cls_tau + static_cast<std::int64_t>(e) * kGroupSlots;
-    for (int c = threadIdx.x; c < kGroupSlots * (P / 2); c += blockDim.x) {
-      const int slot = c / (P / 2), q = c % (P / 2);
-      const int tau = taus[slot];
-      const double* src = xhat + (static_cast<std::int64_t>(tau < 0 ? 0 : tau) * m + col) * P + 2 * q;
-      cp_async16(X + slot * LD + 2 * q, src, tau >= 0);
+    for (int c = 0; c < ncol; ++c) {
+      double* X = smem + (buf * MC + c) * PANEL;
+      for (int q2 = threadIdx.x; q2 < kGroupSlots * (P / 2); q2 += blockDim.x) {
+        const int slot = q2 / (P / 2), q = q2 % (P / 2);
+        const int tau = taus[slot];
+        const double* src =
+            xhat + (static_cast<std::int64_t>(tau < 0 ? 0 : tau) * m + col0 + c) * P + 2 * q;
+        cp_async16(X + slot * LD + 2 * q, src, tau >= 0);
+      }
     }
     cp_async_commit();
   };
@@ -551,43 +561,52 @@ __global__ void __launch_bounds__(P / 16 * 32) k_coupling_mma(const CouplingItem
     }
     __syncthreads();
     const double* Ck = C + static_cast<std::int64_t>(item_cls[e]) * P * P;
-    const double* X = smem + buf * kGroupSlots * LD;
     double a[KS][2];
 #pragma unroll
-    for (int s = 0; s < KS; ++s) {
-      const std::int64_t k = 4 * s + t0;
-      a[s][0] = __ldg(Ck + (row0 + g) + k * P);
-      a[s][1] = __ldg(Ck + (row0 + g + 8) + k * P);
+    for (int s2 = 0; s2 < KS; ++s2) {
+      const std::int64_t k = 4 * s2 + t0;
+      a[s2][0] = __ldg(Ck + (row0 + g) + k * P);
+      a[s2][1] = __ldg(Ck + (row0 + g + 8) + k * P);
     }
 #pragma unroll
-    for (int s = 0; s < KS; ++s) {
-      const int k = 4 * s + t0;
+    for (int c = 0; c < MC; ++c) {
+      if (c >= ncol) break;
+      const double* X = smem + (buf * MC + c) * PANEL;
 #pragma unroll
-      for (int j = 0; j < NT; ++j) dmma_16x8x4(acc[j], a[s][0], a[s][1], X[(8 * j + g) * LD + k]);
+      for (int s2 = 0; s2 < KS; ++s2) {
+        const int k = 4 * s2 + t0;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma_16x8x4(acc[c][j], a[s2][0], a[s2][1], X[(8 * j + g) * LD + k]);
+      }
     }
     __syncthreads();  // X[buf] is refilled two classes later
   }
-  double* out = partial + static_cast<std::int64_t>(blockIdx.x) * kGroupSlots * P;
 #pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    const int n0 = 8 * j + 2 * t0;
-    out[n0 * P + row0 + g] = acc[j][0];
-    out[(n0 + 1) * P + row0 + g] = acc[j][1];
-    out[n0 * P + row0 + g + 8] = acc[j][2];
-    out[(n0 + 1) * P + row0 + g + 8] = acc[j][3];
+  for (int c = 0; c < MC; ++c) {
+    if (c >= ncol) break;
+    double* out = partial + (static_cast<std::int64_t>(blockIdx.x) * m + col0 + c) * kGroupSlots * P;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int n0 = 8 * j + 2 * t0;
+      out[n0 * P + row0 + g] = acc[c][j][0];
+      out[(n0 + 1) * P + row0 + g] = acc[c][j][1];
+      out[n0 * P + row0 + g + 8] = acc[c][j][2];
+      out[(n0 + 1) * P + row0 + g + 8] = acc[c][j][3];
+    }
   }
 }
 
+// yhat_sigma for one (group, column): fixed-order sum over the group's items.
 __global__ void k_coupling_reduce(const std::int32_t* __restrict__ grp_sigma, const std::int32_t* __restrict__ grp_items,
-                                  const double* __restrict__ partial, int P, int m, int col, double* __restrict__ yhat) {
-  const int grp = blockIdx.x;
+                                  const double* __restrict__ partial, int P, int m, double* __restrict__ yhat) {
+  const int grp = blockIdx.x, col = blockIdx.y;
   const int ib = grp_items[grp], ie = grp_items[grp + 1];
   for (int e = threadIdx.x; e < kGroupSlots * P; e += blockDim.x) {
     const int slot = e / P, a = e % P;
     const int sigma = grp_sigma[grp * kGroupSlots + slot];
     if (sigma < 0) continue;
     double s = 0.0;
-    for (int i = ib; i < ie; ++i) s += partial[static_cast<std::int64_t>(i) * kGroupSlots * P + e];
+    for (int i = ib; i < ie; ++i) s += partial[(static_cast<std::int64_t>(i) * m + col) * kGroupSlots * P + e];
     yhat[(static_cast<std::int64_t>(sigma) * m + col) * P + a] = s;
   }
 }
@@ -1391,34 +1410,38 @@ void launch_near_mrhs(cudaStream_t st, const MrhsItem* items, int nitems, const 
 bool coupling_mma_supported(int P) { return P == 16 || P == 32 || P == 64 || P == 128; }
 
 void launch_coupling_mma(cudaStream_t st, const CouplingItem* items, int nitems, const std::int32_t* item_cls,
-                         const std::int32_t* cls_tau, const double* C, int P, const double* xhat, int m, int col,
+                         const std::int32_t* cls_tau, const double* C, int P, const double* xhat, int m,
                          double* partial) {
   if (nitems == 0) return;
-  const size_t smem = 2 * kGroupSlots * (P + 4) * sizeof(double);
-  switch (P) {
-#define PHM_CASE(PP)                                                                                     \
-  case PP: {                                                                                             \
-    static bool attr = false;                                                                            \
-    if (!attr) {                                                                                         \
-      cudaFuncSetAttribute(k_coupling_mma<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); \
-      attr = true;                                                                                       \
-    }                                                                                                    \
-    k_coupling_mma<PP><<<nitems, PP / 16 * 32, smem, st>>>(items, item_cls, cls_tau, C, xhat, m, col, partial); \
-    break;                                                                                               \
+  const int mc = m >= 2 ? 2 : 1;
+  const size_t smem = 2 * mc * kGroupSlots * (P + 4) * sizeof(double);
+  const dim3 grid(static_cast<unsigned>(nitems), static_cast<unsigned>((m + mc - 1) / mc));
+#define PHM_CASE(PP, MC)                                                                                    \
+  if (P == PP && mc == MC) {                                                                                \
+    static bool attr = false;                                                                               \
+    if (!attr) {                                                                                            \
+      cudaFuncSetAttribute(k_coupling_mma<PP, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+      attr = true;                                                                                          \
+    }                                                                                                       \
+    k_coupling_mma<PP, MC><<<grid, PP / 16 * 32, smem, st>>>(items, item_cls, cls_tau, C, xhat, m, partial); \
+    return;                                                                                                 \
   }
-    PHM_CASE(16)
-    PHM_CASE(32)
-    PHM_CASE(64)
-    PHM_CASE(128)
+  PHM_CASE(16, 1)
+  PHM_CASE(16, 2)
+  PHM_CASE(32, 1)
+  PHM_CASE(32, 2)
+  PHM_CASE(64, 1)
+  PHM_CASE(64, 2)
+  PHM_CASE(128, 1)
+  PHM_CASE(128, 2)
 #undef PHM_CASE
-    default: break;
-  }
 }
 
 void launch_coupling_reduce(cudaStream_t st, const std::int32_t* grp_sigma, const std::int32_t* grp_items, int ngroups,
-                            const double* partial, int P, int m, int col, double* yhat) {
+                            const double* partial, int P, int m, double* yhat) {
   if (ngroups == 0) return;
-  k_coupling_reduce<<<ngroups, 256, 0, st>>>(grp_sigma, grp_items, partial, P, m, col, yhat);
+  k_coupling_reduce<<<dim3(static_cast<unsigned>(ngroups), static_cast<unsigned>(m)), 256, 0, st>>>(
+      grp_sigma, grp_items, partial, P, m, yhat);
 }
 
 void launch_near_mvm(cudaStream_t st, const RowItem* items, int nitems, const std::int64_t* tb, const std::int32_t* tn,
