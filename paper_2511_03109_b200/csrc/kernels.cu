@@ -364,7 +364,8 @@ __global__ void k_leaf_fwd(const std::int32_t* __restrict__ leaves, const std::i
   const int cnt = count[leaf];
   double* su = sm;                 // 64 x d x ps
   double* sx = su + 64 * d * ps;   // 64
-  for (int c = 0; c < m; ++c) {
+  {
+    const int c = blockIdx.y;  // one right-hand side per grid row
     double acc[4] = {0.0, 0.0, 0.0, 0.0};  // up to 4 outputs per thread (P <= 4 * blockDim)
     for (int i0 = 0; i0 < cnt; i0 += 64) {
       const int len = min(64, cnt - i0);
@@ -625,8 +626,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
 }
 
-constexpr int kK9Rows = 64, kK9Cols = 64, kK9Kc = 32;
+constexpr int kK9Rows = 64, kK9Kc = 32;
 
+// kK9Cols (8..64) is the right-hand-side tile: small m uses a narrow tile so
+// no MMA work is spent on zero-padded columns.
+template <int kK9Cols>
 __global__ void __launch_bounds__(128) k_near_mrhs(const MrhsItem* __restrict__ items, const std::int64_t* __restrict__ tb,
                                                    const std::int32_t* __restrict__ tn,
                                                    const std::int64_t* __restrict__ doff,
@@ -641,9 +645,10 @@ __global__ void __launch_bounds__(128) k_near_mrhs(const MrhsItem* __restrict__ 
   const MrhsItem it = items[blockIdx.x];
   const int c0 = blockIdx.y * kK9Cols;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t0 = lane & 3;
-  double acc[8][4];
+  constexpr int NT = kK9Cols / 8;
+  double acc[NT][4];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
 
   auto stage = [&](int b, int k0, int buf) {
     const int kc = min(kK9Kc, tn[b] - k0);
@@ -691,7 +696,7 @@ __global__ void __launch_bounds__(128) k_near_mrhs(const MrhsItem* __restrict__ 
       const double a0 = A[(16 * warp + g) * LDA + 4 * s + t0];
       const double a1 = A[(16 * warp + g + 8) * LDA + 4 * s + t0];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) dmma_16x8x4(acc[j], a0, a1, B[(4 * s + t0) * LDB + 8 * j + g]);
+      for (int j = 0; j < NT; ++j) dmma_16x8x4(acc[j], a0, a1, B[(4 * s + t0) * LDB + 8 * j + g]);
     }
     __syncthreads();
     b = nb;
@@ -699,7 +704,7 @@ __global__ void __launch_bounds__(128) k_near_mrhs(const MrhsItem* __restrict__ 
     buf ^= 1;
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
+  for (int j = 0; j < NT; ++j)
 #pragma unroll
     for (int r2 = 0; r2 < 2; ++r2)
 #pragma unroll
@@ -1152,7 +1157,8 @@ __global__ void k_up2(const std::int32_t* __restrict__ nodes, const std::int32_t
   double* za = se + fsz;         // ping
   double* zb = za + P;           // pong
   double* acc = zb + P;          // P
-  for (int c = 0; c < m; ++c) {
+  {
+    const int c = blockIdx.y;  // one right-hand side per grid row
     for (int e = threadIdx.x; e < P; e += blockDim.x) acc[e] = 0.0;
     for (int ch = 0; ch < nc; ++ch) {
       if (count[fc + ch] == 0) continue;
@@ -1195,7 +1201,8 @@ __global__ void k_down2(const std::int32_t* __restrict__ nodes, const std::int32
   double* zb = za + P;
   double* yc = zb + P;
   for (int e = threadIdx.x; e < fsz; e += blockDim.x) se[e] = E[static_cast<std::int64_t>(ch) * fsz + e];
-  for (int c = 0; c < m; ++c) {
+  {
+    const int c = blockIdx.y;  // one right-hand side per grid row
     __syncthreads();
     for (int e = threadIdx.x; e < P; e += blockDim.x) {
       za[e] = yhat[(static_cast<std::int64_t>(p) * m + c) * P + e];
@@ -1237,7 +1244,8 @@ __global__ void k_leaf_bwd2(const std::int32_t* __restrict__ leaves, const std::
   double* yh = sm;                 // P
   double* ta = yh + P;             // kChunk x P/ps
   double* tb = ta + kChunk * (P / ps);
-  for (int c = 0; c < m; ++c) {
+  {
+    const int c = blockIdx.y;  // one right-hand side per grid row
     __syncthreads();
     for (int e = threadIdx.x; e < P; e += blockDim.x) yh[e] = yhat[(static_cast<std::int64_t>(leaf) * m + c) * P + e];
     __syncthreads();
@@ -1360,14 +1368,14 @@ void launch_leaf_fwd(cudaStream_t st, const std::int32_t* leaves, int nleaves, c
                      int m, double* xhat) {
   if (nleaves == 0) return;
   const size_t smem = (64 * d * ps + 64) * sizeof(double);
-  k_leaf_fwd<<<nleaves, threads_for(P), smem, st>>>(leaves, begin, count, U, n, d, ps, P, xp, m, xhat);
+  k_leaf_fwd<<<dim3(nleaves, m), threads_for(P), smem, st>>>(leaves, begin, count, U, n, d, ps, P, xp, m, xhat);
 }
 void launch_up(cudaStream_t st, const std::int32_t* nodes, int cnt, const std::int32_t* first_child,
                const std::int32_t* count, const double* E, int d, int ps, int P, int m, double* xhat) {
   if (cnt == 0) return;
   const int nc = 1 << d;
   const size_t smem = (d * ps * ps + 3 * P) * sizeof(double);
-  k_up2<<<cnt, threads_for(P), smem, st>>>(nodes, first_child, count, E, d, ps, P, nc, m, xhat);
+  k_up2<<<dim3(cnt, m), threads_for(P), smem, st>>>(nodes, first_child, count, E, d, ps, P, nc, m, xhat);
 }
 void launch_coupling(cudaStream_t st, const std::int32_t* sig, int nsig, const std::int64_t* fbeg,
                      const std::int32_t* ftau, const std::int32_t* fcls, const double* C, int P, int m,
@@ -1397,14 +1405,23 @@ void launch_near_mrhs(cudaStream_t st, const MrhsItem* items, int nitems, const 
                       const std::int64_t* doff, const std::int32_t* ld, const std::int32_t* tr, const double* D,
                       const double* X, std::int64_t n, int m, double* Y) {
   if (nitems == 0) return;
-  const size_t smem = 2 * (kK9Rows * (kK9Kc + 4) + kK9Kc * (kK9Cols + 4)) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_near_mrhs, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr = true;
+#define PHM_K9(NC)                                                                                          \
+  {                                                                                                         \
+    const size_t smem = 2 * (kK9Rows * (kK9Kc + 4) + kK9Kc * (NC + 4)) * sizeof(double);                   \
+    static bool attr = false;                                                                               \
+    if (!attr) {                                                                                            \
+      cudaFuncSetAttribute(k_near_mrhs<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);        \
+      attr = true;                                                                                          \
+    }                                                                                                       \
+    const dim3 grid(static_cast<unsigned>(nitems), static_cast<unsigned>((m + NC - 1) / NC));               \
+    k_near_mrhs<NC><<<grid, 128, smem, st>>>(items, tb, tn, doff, ld, tr, D, X, n, m, Y);                   \
+    return;                                                                                                 \
   }
-  const dim3 grid(static_cast<unsigned>(nitems), static_cast<unsigned>((m + kK9Cols - 1) / kK9Cols));
-  k_near_mrhs<<<grid, 128, smem, st>>>(items, tb, tn, doff, ld, tr, D, X, n, m, Y);
+  if (m <= 8) PHM_K9(8)
+  if (m <= 16) PHM_K9(16)
+  if (m <= 32) PHM_K9(32)
+  PHM_K9(64)
+#undef PHM_K9
 }
 
 bool coupling_mma_supported(int P) { return P == 16 || P == 32 || P == 64 || P == 128; }
@@ -1453,14 +1470,14 @@ void launch_down(cudaStream_t st, const std::int32_t* nodes, int cnt, const std:
                  int d, int ps, int P, int m, double* yhat) {
   if (cnt == 0) return;
   const size_t smem = (d * ps * ps + 3 * P) * sizeof(double);
-  k_down2<<<cnt, threads_for(P), smem, st>>>(nodes, parent, E, d, ps, P, m, yhat);
+  k_down2<<<dim3(cnt, m), threads_for(P), smem, st>>>(nodes, parent, E, d, ps, P, m, yhat);
 }
 void launch_leaf_bwd(cudaStream_t st, const std::int32_t* leaves, int nleaves, const std::int64_t* begin,
                      const std::int32_t* count, const double* U, std::int64_t n, int d, int ps, int P,
                      const double* yhat, int m, std::int64_t row_lo, std::int64_t row_hi, double* yp) {
   if (nleaves == 0) return;
   const size_t smem = (P + 2 * 32 * (P / ps)) * sizeof(double);
-  k_leaf_bwd2<<<nleaves, 128, smem, st>>>(leaves, begin, count, U, n, d, ps, P, yhat, m, row_lo, row_hi, yp);
+  k_leaf_bwd2<<<dim3(nleaves, m), 128, smem, st>>>(leaves, begin, count, U, n, d, ps, P, yhat, m, row_lo, row_hi, yp);
 }
 void launch_far_h(cudaStream_t st, const FarHItem* items, int nitems, int max_rows, const std::int64_t* tbeg,
                   const std::int32_t* tcnt, const std::int32_t* cls, const std::int64_t* s_off,
