@@ -52,6 +52,8 @@ void launch_near_mvm(cudaStream_t, const RowItem*, int, const std::int64_t*, con
 void launch_near_mvm_sym(cudaStream_t, const SymItem*, int, const double*, const double*, double*);
 void launch_near_mvm_symcsr(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
                             double*);
+bool launch_near_inst_mvm(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, std::int64_t, int,
+                          const double*, double*, const double*, double*);
 void launch_near_mrhs(cudaStream_t, const MrhsItem*, int, const std::int64_t*, const std::int32_t*,
                       const std::int64_t*, const std::int32_t*, const std::int32_t*, const double*, const double*,
                       std::int64_t, int, double*);
@@ -679,10 +681,12 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     M.E_rank = M.E_raw;
   }
 
-  if (M.sym) {
-    // K6 on symmetric storage, CSR by owner leaf: one item per (leaf, 128-row
-    // chunk) over the stored blocks the leaf owns; partial segments are
-    // gathered per leaf in a fixed order.
+  {
+    // K6, CSR by owner leaf: one item per (leaf, 128-row chunk) over the
+    // stored blocks the leaf owns (all of its blocks with full storage);
+    // with symmetric storage each stored block also yields the column
+    // product for its partner leaf. Partial segments are gathered per leaf
+    // in a fixed order.
     std::vector<std::vector<Index>> owned(M.nnodes);
     for (Index b = 0; b < nnear; ++b)
       if (M.near_doff[b] >= 0 && !M.near_trans[b]) owned[H.blocks.near[b].sigma].push_back(b);
@@ -708,7 +712,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
           sb.x_col0 = T.nodes[tau].begin;
           sb.ncol = nt;
           sb.p_col = -1;
-          if (tau != s) {
+          if (M.sym && tau != s) {
             sb.p_col = poff;
             segs_of[tau].push_back({poff, 0, nt});
             poff += nt;
@@ -1060,6 +1064,23 @@ void inst_classes(DevInstance& I, const dev::ThetaV& tv, cudaStream_t s) {
   });
 }
 
+// Snapshot weights w = v_shape (x) ... times the amplitude interpolant
+// sum_j v_j s_j (the full-rank NearBlockTT theta-core chain).
+void inst_snapshot_w(DevInstance& I, const std::vector<std::vector<double>>& v, const dev::ThetaV& tv,
+                     cudaStream_t s) {
+  DevMatrix& M = *I.M;
+  const KernelSpec& spec = M.hm->cfg.spec;
+  dev::ThetaV shape = tv;
+  shape.dt = spec.shape_params();
+  double amp = 1.0;
+  if (spec.amplitude) {
+    const auto& g = M.hm->grids.grids[spec.shape_params()];
+    amp = 0.0;
+    for (int j = 0; j < g.p; ++j) amp += v[spec.shape_params()][j] * g.nodes[j];
+  }
+  M.ctx->run_on(s, "near_w", [&] { dev::launch_set_vec(s, I.w.as<double>(), M.R_snap, shape, amp); });
+}
+
 // Near stage of instantiate: every stored D_b(theta) (K1).
 void inst_near(DevInstance& I, const double* theta, const std::vector<std::vector<double>>& v,
                const dev::ThetaV& tv, cudaStream_t s, StageCounters* counters) {
@@ -1067,17 +1088,7 @@ void inst_near(DevInstance& I, const double* theta, const std::vector<std::vecto
   const HostMatrix& H = *M.hm;
   Context& ctx = *M.ctx;
   if (M.mode == NearMode::Snapshot) {
-    // w = v_shape (x) ... times the amplitude interpolant sum_j v_j s_j
-    dev::ThetaV shape = tv;
-    const KernelSpec& spec = H.cfg.spec;
-    shape.dt = spec.shape_params();
-    double amp = 1.0;
-    if (spec.amplitude) {
-      const auto& g = H.grids.grids[spec.shape_params()];
-      amp = 0.0;
-      for (int j = 0; j < g.p; ++j) amp += v[spec.shape_params()][j] * g.nodes[j];
-    }
-    ctx.run_on(s, "near_w", [&] { dev::launch_set_vec(s, I.w.as<double>(), M.R_snap, shape, amp); });
+    inst_snapshot_w(I, v, tv, s);
     ctx.run_on(s, "near_inst", [&] {
       dev::launch_inst_flat(s, M.G.as<double>(), M.E, M.R_snap, I.w.as<double>(), I.D.as<double>());
     });
@@ -1250,12 +1261,21 @@ void far_chain(DevInstance& I, Index m, cudaStream_t fs) {
 }
 
 // Near-field product on stream st: writes this shard's rows of yp.
+// Fixed-order per-leaf sum of the near partials into column c of yp.
+void near_gather(DevInstance& I, Index c, cudaStream_t st) {
+  DevMatrix& M = *I.M;
+  M.ctx->run_on(st, "near_gather", [&] {
+    dev::launch_near_gather(st, M.n_gather_leaves, M.g_row0.as<std::int64_t>(), M.g_rows.as<std::int32_t>(),
+                            M.g_sbeg.as<std::int32_t>(), M.g_segs.as<dev::GatherSeg>(), M.sym_part.as<double>(),
+                            M.yp.as<double>() + c * M.n);
+  });
+}
+
 void near_product(DevInstance& I, Index m, cudaStream_t st) {
   DevMatrix& M = *I.M;
   Context& ctx = *M.ctx;
   const int mm = static_cast<int>(m);
-  if ((M.sym ? M.n_gather_leaves : M.n_row_items) == 0 || M.n_k9_items == 0)
-    CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
+  if (M.n_gather_leaves == 0 || M.n_k9_items == 0) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
   // Block right-hand sides: the near product is a dense contraction, so it
   // runs on fp64 tensor cores (K9); single vectors stay on the HBM GEMV.
   const bool block_rhs = m >= kMrhsMin;
@@ -1267,24 +1287,12 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
                             M.yp.as<double>());
     });
   for (Index c = 0; c < (block_rhs ? 0 : m); ++c) {
-    if (M.sym) {
-      ctx.run_on(st, "near_mvm", [&] {
-        dev::launch_near_mvm_symcsr(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
-                                    M.sym_blocks.as<dev::SymBlock>(), I.D.as<double>(), M.xp.as<double>() + c * M.n,
-                                    M.sym_part.as<double>());
-      });
-      ctx.run_on(st, "near_gather", [&] {
-        dev::launch_near_gather(st, M.n_gather_leaves, M.g_row0.as<std::int64_t>(), M.g_rows.as<std::int32_t>(),
-                                M.g_sbeg.as<std::int32_t>(), M.g_segs.as<dev::GatherSeg>(), M.sym_part.as<double>(),
-                                M.yp.as<double>() + c * M.n);
-      });
-    } else {
-      ctx.run_on(st, "near_mvm", [&] {
-        dev::launch_near_mvm(st, M.row_items.as<dev::RowItem>(), M.n_row_items, M.nb_tb.as<std::int64_t>(),
-                             M.nb_tn.as<std::int32_t>(), M.nb_doff.as<std::int64_t>(), I.D.as<double>(),
-                             M.xp.as<double>() + c * M.n, M.yp.as<double>() + c * M.n);
-      });
-    }
+    ctx.run_on(st, "near_mvm", [&] {
+      dev::launch_near_mvm_symcsr(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
+                                  M.sym_blocks.as<dev::SymBlock>(), I.D.as<double>(), M.xp.as<double>() + c * M.n,
+                                  M.sym_part.as<double>());
+    });
+    near_gather(I, c, st);
   }
 }
 
@@ -1388,9 +1396,27 @@ void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, 
   CK(cudaEventRecord(ctx.aux_ev, fs));
   inst_classes(I, tv, fs);
   far_chain(I, m, fs);
-  inst_near(I, theta, v, tv, st, counters);
-  CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
-  near_product(I, m, st);
+  bool fused = false;
+  if (M.mode == NearMode::Snapshot && m == 1) {
+    // one pass over the snapshots: D is formed, stored and multiplied at once
+    inst_snapshot_w(I, v, tv, st);
+    CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
+    ctx.run_on(st, "near_inst_mvm", [&] {
+      fused = dev::launch_near_inst_mvm(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
+                                        M.sym_blocks.as<dev::SymBlock>(), M.G.as<double>(), M.E, M.R_snap,
+                                        I.w.as<double>(), I.D.as<double>(), M.xp.as<double>(),
+                                        M.sym_part.as<double>());
+    });
+    if (fused) {
+      if (M.n_gather_leaves == 0) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
+      near_gather(I, 0, st);
+    }
+  }
+  if (!fused) {
+    inst_near(I, theta, v, tv, st, counters);
+    CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
+    near_product(I, m, st);
+  }
   ctx.join();
   far_finish(I, m, st);
   ctx.run("scatter", [&] { dev::launch_scatter(st, M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev); });

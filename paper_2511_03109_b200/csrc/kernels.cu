@@ -988,6 +988,114 @@ __global__ void __launch_bounds__(256) k_near_mvm_symcsr(const SymRowItem* __res
   }
 }
 
+// K1 + K6 fused (snapshot mode, instantiate followed by apply): the CTA of
+// a leaf streams the R snapshot slabs of the stored blocks it owns, forms
+// D = sum_k w_k S_k in registers (same FMA order as k_inst_flat, so D is
+// bit-identical), writes D, and uses it at once for the row and column
+// products of k_near_mvm_symcsr. The near field then costs one pass over the
+// snapshots: the MVM no longer re-reads D.
+template <int R>
+__global__ void __launch_bounds__(256) k_near_inst_mvm(const SymRowItem* __restrict__ items,
+                                                       const SymBlock* __restrict__ blocks,
+                                                       const double* __restrict__ G, std::int64_t E,
+                                                       const double* __restrict__ w, double* __restrict__ D,
+                                                       const double* __restrict__ xp, double* __restrict__ part) {
+  __shared__ double red[8][128];
+  const SymRowItem it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double wr[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) wr[k] = w[k];
+  double racc[4] = {0.0, 0.0, 0.0, 0.0};
+  double xs[4];
+  bool live[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    live[q] = lane + 32 * q < it.rows;
+    xs[q] = live[q] ? xp[it.x_row0 + lane + 32 * q] : 0.0;
+  }
+  const std::int64_t ld = it.ld;
+  for (int b = it.bbeg; b < it.bend; ++b) {
+    const SymBlock blk = blocks[b];
+    const std::int64_t base = blk.d_off + it.i0 + lane;
+    const double* xt = xp + blk.x_col0;
+    const bool diag = blk.p_col < 0;
+    int j = warp;
+    for (; j + 8 < blk.ncol; j += 16) {
+      const double x0 = xt[j], x1 = xt[j + 8];
+      double v0[4], v1[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        v0[q] = 0.0;
+        v1[q] = 0.0;
+        if (live[q]) {
+          const std::int64_t o0 = base + j * ld + 32 * q, o1 = o0 + 8 * ld;
+          double s0[R], s1[R];
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            s0[k] = ld_stream(G + k * E + o0);
+            s1[k] = ld_stream(G + k * E + o1);
+          }
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            v0[q] += s0[k] * wr[k];
+            v1[q] += s1[k] * wr[k];
+          }
+          D[o0] = v0[q];
+          D[o1] = v1[q];
+        }
+      }
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        racc[q] += v0[q] * x0 + v1[q] * x1;
+        c0 += v0[q] * xs[q];
+        c1 += v1[q] * xs[q];
+      }
+      if (!diag) {
+        c0 = warp_sum(c0);
+        c1 = warp_sum(c1);
+        if (lane == 0) {
+          part[blk.p_col + j] = c0;
+          part[blk.p_col + j + 8] = c1;
+        }
+      }
+    }
+    for (; j < blk.ncol; j += 8) {
+      const double x0 = xt[j];
+      double c0 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double v = 0.0;
+        if (live[q]) {
+          const std::int64_t o = base + j * ld + 32 * q;
+          double s[R];
+#pragma unroll
+          for (int k = 0; k < R; ++k) s[k] = ld_stream(G + k * E + o);
+#pragma unroll
+          for (int k = 0; k < R; ++k) v += s[k] * wr[k];
+          D[o] = v;
+        }
+        racc[q] += v * x0;
+        c0 += v * xs[q];
+      }
+      if (!diag) {
+        c0 = warp_sum(c0);
+        if (lane == 0) part[blk.p_col + j] = c0;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) red[warp][lane + 32 * q] = racc[q];
+  __syncthreads();
+  if (threadIdx.x < it.rows) {
+    double s = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < 8; ++w2) s += red[w2][threadIdx.x];
+    part[it.p_row + threadIdx.x] = s;
+  }
+}
+
 // y[rows of leaf] = sum of the leaf's partial segments, in list order.
 __global__ void k_near_gather(const std::int64_t* __restrict__ leaf_row0, const std::int32_t* __restrict__ leaf_rows,
                               const std::int32_t* __restrict__ seg_beg, const GatherSeg* __restrict__ segs,
@@ -1394,6 +1502,18 @@ void launch_near_mvm_symcsr(cudaStream_t st, const SymRowItem* items, int nitems
                             const double* D, const double* xp, double* part) {
   if (nitems == 0) return;
   k_near_mvm_symcsr<<<nitems, 256, 0, st>>>(items, blocks, D, xp, part);
+}
+bool launch_near_inst_mvm(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks,
+                          const double* G, std::int64_t E, int R, const double* w, double* D, const double* xp,
+                          double* part) {
+  if (nitems == 0) return true;
+  switch (R) {
+    case 4: k_near_inst_mvm<4><<<nitems, 256, 0, st>>>(items, blocks, G, E, w, D, xp, part); return true;
+    case 6: k_near_inst_mvm<6><<<nitems, 256, 0, st>>>(items, blocks, G, E, w, D, xp, part); return true;
+    case 8: k_near_inst_mvm<8><<<nitems, 256, 0, st>>>(items, blocks, G, E, w, D, xp, part); return true;
+    case 10: k_near_inst_mvm<10><<<nitems, 256, 0, st>>>(items, blocks, G, E, w, D, xp, part); return true;
+    default: return false;
+  }
 }
 void launch_near_gather(cudaStream_t st, int nleaves, const std::int64_t* leaf_row0, const std::int32_t* leaf_rows,
                         const std::int32_t* seg_beg, const GatherSeg* segs, const double* part, double* yp) {
