@@ -195,6 +195,13 @@ int phm_apply_device(phm_instance inst, const double* x_dev, double* y_dev, int6
  * order (rows x m, column-major); gather across ranks, then unpermute. */
 int phm_apply_rows_device(phm_instance inst, const double* x_dev, double* yrows_dev, int64_t m);
 int phm_unpermute_device(phm_matrix m, const double* yperm_dev, double* y_dev, int64_t mcols);
+/* estimate_error of the reference harness (harness.cpp:183-236): probe rows
+ * sampled without replacement and x ~ U[0,1) from the reference's Rng
+ * stream, exact rows (K x)_J by direct kernel evaluation on the GPU (audit
+ * counted), ||exact - approx|| / ||exact|| over J. Outputs other than err are
+ * optional (min(probe_rows, n) entries; x_out has n). */
+int phm_estimate_error(phm_instance inst, int64_t probe_rows, uint64_t seed, double* err, int64_t* rows_out,
+                       double* exact_out, double* approx_out, double* x_out);
 /* Induced dense matrix (n x n column-major), refuses n > guard. */
 int phm_to_dense(phm_instance inst, double* out, int64_t guard);
 

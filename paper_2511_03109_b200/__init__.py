@@ -138,6 +138,7 @@ SIGNATURES = {
     "phm_apply_rows_device": ([_P, _P, _P, C.c_int64], C.c_int),
     "phm_unpermute_device": ([_P, _P, _P, C.c_int64], C.c_int),
     "phm_to_dense": ([_P, _DP, C.c_int64], C.c_int),
+    "phm_estimate_error": ([_P, C.c_int64, C.c_uint64, _DP, _I64P, _DP, _DP, _DP], C.c_int),
     "phm_generate_points": ([C.c_int64, C.c_int, C.c_uint64, _DP], C.c_int),
     "phm_generate_mixture_points": ([C.c_int64, C.c_int, C.c_int, C.c_double, C.c_uint64, _DP], C.c_int),
     "phm_generate_normal": ([C.c_int64, C.c_uint64, _DP], C.c_int),
@@ -516,6 +517,19 @@ class InstantiatedMatrix:
         out = np.empty(P * P, dtype=np.float64)
         _check(lib().phm_instance_class_c(self._h, k, _dp(out)))
         return out.reshape((P, P), order="F")
+
+    def estimate_error(self, probe_rows: int = 200, seed: int = 0, details: bool = False):
+        """estimate_error of the reference harness (harness.cpp:183-236)."""
+        n = self.parent.n()
+        m = min(probe_rows, n)
+        err = C.c_double()
+        rows = np.empty(m, dtype=np.int64)
+        ex, ap, x = np.empty(m), np.empty(m), np.empty(n)
+        _check(lib().phm_estimate_error(self._h, probe_rows, seed, C.byref(err), rows.ctypes.data_as(_I64P),
+                                        _dp(ex), _dp(ap), _dp(x)))
+        if details:
+            return err.value, {"rows": rows, "exact": ex, "approx": ap, "x": x}
+        return err.value
 
     def to_dense(self, guard: int = 8192) -> np.ndarray:
         n = self.parent.n()

@@ -643,6 +643,21 @@ int phm_instantiate_apply_device(phm_instance inst, const double* theta, int n_t
     phm::instantiate_apply_device(*inst->inst, theta, n_theta, x, y, m, &H.counters);
   });
 }
+int phm_estimate_error(phm_instance inst, int64_t probe_rows, uint64_t seed, double* err, int64_t* rows_out,
+                       double* exact_out, double* approx_out, double* x_out) {
+  return guarded([&] {
+    need(inst, "instance");
+    need(err, "err");
+    auto& H = const_cast<phm::HostMatrix&>(phm::matrix_host(*inst->m));
+    std::vector<phm::Index> rows;
+    std::vector<double> ex, ap, xs;
+    *err = phm::estimate_error(*inst->inst, probe_rows, seed, &H.counters, &rows, &ex, &ap, &xs);
+    if (rows_out) std::memcpy(rows_out, rows.data(), rows.size() * sizeof(int64_t));
+    if (exact_out) std::memcpy(exact_out, ex.data(), ex.size() * sizeof(double));
+    if (approx_out) std::memcpy(approx_out, ap.data(), ap.size() * sizeof(double));
+    if (x_out) std::memcpy(x_out, xs.data(), xs.size() * sizeof(double));
+  });
+}
 int phm_apply_device(phm_instance inst, const double* x, double* y, int64_t m) {
   return guarded([&] {
     need(inst, "instance");

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -54,6 +55,8 @@ void launch_near_mvm_symcsr(cudaStream_t, const SymRowItem*, int, const SymBlock
                             double*);
 bool launch_near_inst_mvm(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, std::int64_t, int,
                           const double*, double*, const double*, double*);
+void launch_exact_rows(cudaStream_t, const std::int64_t*, int, const double*, std::int64_t, int, int, const double*,
+                       double, const double*, double*);
 void launch_near_mrhs(cudaStream_t, const MrhsItem*, int, const std::int64_t*, const std::int32_t*,
                       const std::int64_t*, const std::int32_t*, const std::int32_t*, const double*, const double*,
                       std::int64_t, int, double*);
@@ -1397,7 +1400,14 @@ void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, 
   inst_classes(I, tv, fs);
   far_chain(I, m, fs);
   bool fused = false;
-  if (M.mode == NearMode::Snapshot && m == 1) {
+  // The fused K1+K6 kernel (k_near_inst_mvm) measured 17.4 ms against 11.0 ms
+  // for K1 (flat 256-bit stream) + K6 at C3: the per-column block walk keeps
+  // too few bytes in flight. Kept behind PHM_FUSED_NEAR=1 for tuning.
+  static const bool use_fused = [] {
+    const char* e = std::getenv("PHM_FUSED_NEAR");
+    return e && std::atoi(e) == 1;
+  }();
+  if (use_fused && M.mode == NearMode::Snapshot && m == 1) {
     // one pass over the snapshots: D is formed, stored and multiplied at once
     inst_snapshot_w(I, v, tv, st);
     CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
@@ -1420,6 +1430,65 @@ void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, 
   ctx.join();
   far_finish(I, m, st);
   ctx.run("scatter", [&] { dev::launch_scatter(st, M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev); });
+}
+
+// estimate_error (harness.cpp:183-236) for this instance: probe rows J
+// sampled without replacement and x ~ U[0,1) from Rng(mix_seed(seed,
+// "erro")), exact rows (K x)_J evaluated directly on the GPU (charged to the
+// audit counter), approximate rows from the GPU MVM; returns
+// ||exact - approx||_J / ||exact||_J.
+double estimate_error(DevInstance& I, Index probe_rows, std::uint64_t seed, StageCounters* counters,
+                      std::vector<Index>* rows_out, std::vector<double>* exact_out, std::vector<double>* approx_out,
+                      std::vector<double>* x_out) {
+  DevMatrix& M = *I.M;
+  const HostMatrix& H = *M.hm;
+  const Tree& T = *H.tree;
+  const KernelSpec& spec = H.cfg.spec;
+  if (spec.family == kMatern) throw std::invalid_argument("estimate_error on the GPU needs a closed-form kernel");
+  PHM_CHECK(probe_rows >= 1, "estimate_error: probe_rows must be >= 1");
+  const Index n = M.n;
+  Rng rng(mix_seed(seed, 0x6572726fULL));
+  std::vector<Index> all(static_cast<size_t>(n));
+  for (Index i = 0; i < n; ++i) all[i] = i;
+  const Index m = std::min<Index>(probe_rows, n);
+  for (Index i = 0; i < m; ++i) std::swap(all[i], all[i + static_cast<Index>(rng.integer(n - i))]);
+  all.resize(static_cast<size_t>(m));
+  std::vector<double> x(static_cast<size_t>(n)), y(static_cast<size_t>(n));
+  for (Index i = 0; i < n; ++i) x[i] = rng.uniform();
+  apply_host(I, x.data(), y.data(), 1);  // leaves x in tree order in M.xp
+  std::vector<Index> inv(static_cast<size_t>(n));
+  for (Index p = 0; p < n; ++p) inv[T.perm[p]] = p;
+  std::vector<std::int64_t> pos(static_cast<size_t>(m));
+  for (Index j = 0; j < m; ++j) pos[j] = inv[all[j]];
+  std::vector<double> th(3, 1.0);
+  for (int k = 0; k < spec.shape_params(); ++k) th[k] = I.theta[k];
+  const double amp = spec.amplitude ? I.theta[spec.shape_params()] : 1.0;
+  DBuf dpos, dth, dout;
+  cudaStream_t st = M.st();
+  upload(dpos, pos, st);
+  upload(dth, th, st);
+  dout.alloc(sizeof(double) * m);
+  M.ctx->run("exact_rows", [&] {
+    dev::launch_exact_rows(st, dpos.as<std::int64_t>(), static_cast<int>(m), M.pts.as<double>(), n, M.d, spec.family,
+                           dth.as<double>(), amp, M.xp.as<double>(), dout.as<double>());
+  });
+  std::vector<double> exact(static_cast<size_t>(m));
+  CK(cudaMemcpyAsync(exact.data(), dout.p, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (counters) counters->audit.add(static_cast<std::uint64_t>(m * n));
+  double num = 0.0, den = 0.0;
+  std::vector<double> approx(static_cast<size_t>(m));
+  for (Index j = 0; j < m; ++j) {
+    approx[j] = y[all[j]];
+    const double diff = exact[j] - approx[j];
+    num += diff * diff;
+    den += exact[j] * exact[j];
+  }
+  if (rows_out) *rows_out = all;
+  if (exact_out) *exact_out = exact;
+  if (approx_out) *approx_out = approx;
+  if (x_out) *x_out = x;
+  return den > 0.0 ? std::sqrt(num / den) : std::sqrt(num);
 }
 
 void instantiate_apply_host(DevInstance& I, const double* theta, int n_theta, const double* x, double* y, Index m,

@@ -74,6 +74,11 @@ void instantiate_apply_device(DevInstance& inst, const double* theta, int n_thet
                               Index m, StageCounters* counters);
 void instantiate_apply_host(DevInstance& inst, const double* theta, int n_theta, const double* x, double* y, Index m,
                             StageCounters* counters);
+// estimate_error of harness.cpp:183-236 on the GPU (exact probe rows by
+// direct kernel evaluation; audit-counted).
+double estimate_error(DevInstance& inst, Index probe_rows, std::uint64_t seed, StageCounters* counters,
+                      std::vector<Index>* rows_out, std::vector<double>* exact_out, std::vector<double>* approx_out,
+                      std::vector<double>* x_out);
 void apply_device(DevInstance& inst, const double* x_dev, double* y_dev, Index m);
 // Sharded pieces: rows [row_begin, row_end) of y in tree order, and the
 // final un-permute of a gathered tree-order vector.

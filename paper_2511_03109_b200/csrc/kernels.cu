@@ -1393,7 +1393,42 @@ __global__ void k_leaf_bwd2(const std::int32_t* __restrict__ leaves, const std::
   }
 }
 
+// estimate_error (harness.cpp:183-236): exact rows (K x)_J for the probe
+// rows J by direct kernel evaluation, one CTA per probe row, fixed-order
+// block reduction.
+__global__ void __launch_bounds__(256) k_exact_rows(const std::int64_t* __restrict__ rows, const double* __restrict__ pts,
+                                                    std::int64_t n, int d, int fam, const double* __restrict__ theta,
+                                                    double amp, const double* __restrict__ xp,
+                                                    double* __restrict__ out) {
+  __shared__ double red[256];
+  const std::int64_t r = rows[blockIdx.x];
+  double pr[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < d; ++k) pr[k] = pts[k * n + r];
+  double th[3] = {theta[0], theta[1], theta[2]};
+  double s = 0.0;
+  for (std::int64_t l = threadIdx.x; l < n; l += blockDim.x) {
+    double r2 = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double dl = __dsub_rn(pr[k], pts[k * n + l]);
+      r2 = __dadd_rn(r2, __dmul_rn(dl, dl));
+    }
+    s += amp * kernel_profile(fam, sqrt(r2), th) * xp[l];
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = red[0];
+}
+
 // ------------------------------------------------------------ launchers
+void launch_exact_rows(cudaStream_t st, const std::int64_t* rows, int nrows, const double* pts, std::int64_t n, int d,
+                       int fam, const double* theta, double amp, const double* xp, double* out) {
+  if (nrows == 0) return;
+  k_exact_rows<<<nrows, 256, 0, st>>>(rows, pts, n, d, fam, theta, amp, xp, out);
+}
 void launch_snapshot(cudaStream_t st, const SnapTile* tiles, std::int64_t ntiles, const BlockGeom* geo,
                      const double* pts, std::int64_t n, int d, int fam, int R, const double* theta_nodes, double amp,
                      double* out) {

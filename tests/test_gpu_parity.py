@@ -315,6 +315,27 @@ def test_artifact_round_trip_on_device(ph, tmp_path):
             assert rel(a.apply(x), b.apply(x)) <= 1e-14
 
 
+def test_estimate_error_matches_oracle_rows(ph, po):
+    """harness.cpp:183-236 on the GPU: exact probe rows equal the oracle's
+    dense kernel rows, approx rows equal the oracle MVM, and the error of a
+    well-resolved matrix is small."""
+    pts = ph.generate_points(1200, 3, 9)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT, seed=0)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    inst = ph.instantiate(pm, [0.21])
+    err, det = inst.estimate_error(200, seed=3, details=True)
+    rows = det["rows"]
+    assert len(set(rows.tolist())) == 200  # without replacement
+    K = po.dense_kernel(pts, ph.Family.E, [0.21])
+    exact = K[rows] @ det["x"]
+    assert np.max(np.abs(det["exact"] - exact)) <= 1e-12 * np.max(np.abs(exact))
+    approx = om.instantiate([0.21]).apply(det["x"])[rows]
+    assert rel(det["approx"], approx) <= TOL_Y
+    assert err == pytest.approx(np.linalg.norm(exact - approx) / np.linalg.norm(exact), rel=1e-9)
+    assert err < 1e-2
+
+
 def test_reinstantiate_in_place(ph, po):
     pts = ph.generate_points(2000, 3, 1)
     cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
