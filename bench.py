@@ -284,7 +284,7 @@ def run_ours(args):
     ms = ev0.elapsed_time(ev1)
     # dominant kernel: the fused near-field pass (instantiate + GEMV) when the
     # step runs it, else the plain K1 instantiate stream
-    k1_name, k1_desc = "near_inst_mvm", "k_near_inst_mvm (K1+K6 fused: forms, stores and applies D)"
+    k1_name, k1_desc = "near_inst_mvm", "k_near_tma (K1+K6 fused TMA pass: forms, stores and applies D)"
     k1_ms, k1_n = ctx.timer(k1_name)
     if k1_n == 0:
         k1_name, k1_desc = "near_inst", "k_inst_flat (K1 near instantiate)"

@@ -53,7 +53,7 @@ void launch_near_mvm(cudaStream_t, const RowItem*, int, const std::int64_t*, con
 void launch_near_mvm_sym(cudaStream_t, const SymItem*, int, const double*, const double*, double*);
 void launch_near_mvm_symcsr(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
                             double*);
-bool launch_near_inst_mvm(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, std::int64_t, int,
+bool launch_near_inst_tma(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, std::int64_t, int,
                           const double*, double*, const double*, double*);
 void launch_exact_rows(cudaStream_t, const std::int64_t*, int, const double*, std::int64_t, int, int, const double*,
                        double, const double*, double*);
@@ -276,6 +276,7 @@ struct DevMatrix {
   std::int64_t E_logical = 0;    // sum of n_sigma n_tau over local near blocks
   DBuf sym_items, sym_blocks, g_row0, g_rows, g_sbeg, g_segs, sym_part;
   int n_sym_items = 0, n_gather_leaves = 0;
+  bool near_tma = false;  // every item spans its whole leaf: TMA near pass
   // K9 multi-RHS near field (DMMA), CSR by sigma over stored blocks
   DBuf k9_items, k9_tb, k9_tn, k9_doff, k9_ld, k9_tr;
   int n_k9_items = 0;
@@ -700,14 +701,19 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     for (int s = 0; s < M.nnodes; ++s) {
       if (owned[s].empty()) continue;
       const int ns = static_cast<int>(T.nodes[s].count);
-      for (int i0 = 0; i0 < ns; i0 += 128) {
+      // items: 128-row slices of the leaf x runs of at most kItemBlocks owned
+      // blocks (the TMA pass caches an item's block list in shared memory)
+      constexpr std::size_t kItemBlocks = 128;
+      for (int i0 = 0; i0 < ns; i0 += 128)
+      for (std::size_t q0 = 0; q0 < owned[s].size(); q0 += kItemBlocks) {
         dev::SymRowItem it{};
         it.x_row0 = T.nodes[s].begin + i0;
         it.rows = std::min(128, ns - i0);
         it.ld = ns;
         it.i0 = i0;
         it.bbeg = static_cast<std::int32_t>(blocks.size());
-        for (Index b : owned[s]) {
+        for (std::size_t q = q0; q < std::min(owned[s].size(), q0 + kItemBlocks); ++q) {
+          const Index b = owned[s][q];
           const int tau = H.blocks.near[b].tau;
           const int nt = static_cast<int>(T.nodes[tau].count);
           dev::SymBlock sb{};
@@ -742,6 +748,9 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     }
     M.n_sym_items = static_cast<int>(items.size());
     M.n_gather_leaves = static_cast<int>(lrow0.size());
+    M.near_tma = !items.empty();
+    for (const auto& it : items)  // whole-leaf items (k_near_tma)
+      M.near_tma = M.near_tma && it.i0 == 0 && it.rows == it.ld;
     upload(M.sym_items, items, st);
     upload(M.g_row0, lrow0, st);
     upload(M.g_rows, lrows, st);
@@ -1151,7 +1160,10 @@ std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const dou
       m->pool_D.pop_back();
     }
   }
-  if (I->D.bytes < static_cast<size_t>(m->E) * sizeof(double)) I->D.alloc(static_cast<size_t>(m->E) * sizeof(double));
+  if (I->D.bytes < static_cast<size_t>(m->E) * sizeof(double)) {
+    I->D.alloc(static_cast<size_t>(m->E) * sizeof(double));
+    CK(cudaMemsetAsync(I->D.p, 0, I->D.bytes, m->st()));  // block pads stay zero
+  }
   I->H.alloc(static_cast<size_t>(std::max<std::int64_t>(m->H_len, 1)) * sizeof(double));
   if (m->C_len) I->C.alloc(static_cast<size_t>(m->C_len) * sizeof(double));
   const std::int64_t wl = m->mode == NearMode::Snapshot ? m->R_snap : m->w_len;
@@ -1400,19 +1412,21 @@ void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, 
   inst_classes(I, tv, fs);
   far_chain(I, m, fs);
   bool fused = false;
-  // The fused K1+K6 kernel (k_near_inst_mvm) measured 17.4 ms against 11.0 ms
-  // for K1 (flat 256-bit stream) + K6 at C3: the per-column block walk keeps
-  // too few bytes in flight. Kept behind PHM_FUSED_NEAR=1 for tuning.
+  // Snapshot mode, one vector: K1 and K6 fused into one TMA pass over the
+  // snapshots (k_near_tma) -- 10.8 ms at C3 against 9.8 + 1.6 ms for the
+  // separate kernels. D is bit-identical to K1's; y agrees with the separate
+  // path to rounding (row sums are accumulated in a different order).
+  // PHM_FUSED_NEAR=0 selects the separate kernels.
   static const bool use_fused = [] {
     const char* e = std::getenv("PHM_FUSED_NEAR");
-    return e && std::atoi(e) == 1;
+    return !(e && std::atoi(e) == 0);
   }();
-  if (use_fused && M.mode == NearMode::Snapshot && m == 1) {
+  if (use_fused && M.near_tma && M.mode == NearMode::Snapshot && m == 1) {
     // one pass over the snapshots: D is formed, stored and multiplied at once
     inst_snapshot_w(I, v, tv, st);
     CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
     ctx.run_on(st, "near_inst_mvm", [&] {
-      fused = dev::launch_near_inst_mvm(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
+      fused = dev::launch_near_inst_tma(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
                                         M.sym_blocks.as<dev::SymBlock>(), M.G.as<double>(), M.E, M.R_snap,
                                         I.w.as<double>(), I.D.as<double>(), M.xp.as<double>(),
                                         M.sym_part.as<double>());

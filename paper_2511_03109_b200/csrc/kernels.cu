@@ -107,7 +107,7 @@ __global__ void k_snapshot(const SnapTile* __restrict__ tiles, std::int64_t ntil
 // 256-bit loads before it accumulates, which keeps enough bytes in flight
 // per SM to cover HBM latency.
 template <int R>
-__global__ void __launch_bounds__(256) k_inst_flat(const double* __restrict__ G, std::int64_t E,
+__global__ void __launch_bounds__(256, 1) k_inst_flat(const double* __restrict__ G, std::int64_t E,
                                                    const double* __restrict__ w, double* __restrict__ D) {
   constexpr int U = R >= 8 ? 1 : 2;
   double wr[R];
@@ -988,111 +988,169 @@ __global__ void __launch_bounds__(256) k_near_mvm_symcsr(const SymRowItem* __res
   }
 }
 
-// K1 + K6 fused (snapshot mode, instantiate followed by apply): the CTA of
-// a leaf streams the R snapshot slabs of the stored blocks it owns, forms
-// D = sum_k w_k S_k in registers (same FMA order as k_inst_flat, so D is
-// bit-identical), writes D, and uses it at once for the row and column
-// products of k_near_mvm_symcsr. The near field then costs one pass over the
-// snapshots: the MVM no longer re-reads D.
-template <int R>
-__global__ void __launch_bounds__(256) k_near_inst_mvm(const SymRowItem* __restrict__ items,
-                                                       const SymBlock* __restrict__ blocks,
-                                                       const double* __restrict__ G, std::int64_t E,
-                                                       const double* __restrict__ w, double* __restrict__ D,
-                                                       const double* __restrict__ xp, double* __restrict__ part) {
-  __shared__ double red[8][128];
+// ------------------------------------------------------------ TMA near pass
+// Near field through the Tensor Memory Accelerator: the CTA of an owner
+// leaf walks its stored blocks in column chunks; for every chunk one thread
+// issues R bulk copies (cp.async.bulk, one per snapshot slab, or one of D
+// itself) into a shared-memory stage tracked by an mbarrier (expect_tx /
+// complete_tx), double-buffered so the next chunk lands while this one is
+// consumed. Consumers form d = sum_k w_k S_k (R = 1, w = 1 reads D as is),
+// optionally store D (instantiate fused with apply), and accumulate the row
+// product D x_tau (thread = row, conflict-free) and the column product
+// D^T x_sigma (warp = column, shuffle reduction) straight from shared memory.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+// Warp-specialised pipeline: warp 8 (one elected lane) is the producer and
+// keeps every free stage of an NST-deep ring filled with the next chunk
+// (R bulk copies, one full[] mbarrier per stage); warps 0-7 consume. A
+// consumer pass over a chunk forms d = sum_k w_k S_k into a double-buffered
+// formed chunk (and stores it to D), meets the other consumers at a named
+// barrier, releases the stage through its empty[] mbarrier, then runs the
+// row and column products out of the formed chunk while the producer
+// refills. Shared memory (doubles): NST R CH stages + 2 CH formed + 2 x 128
+// x_tau panels.
+constexpr int tma_smem_doubles(int R, int CH, int NST) { return NST * R * CH + 2 * CH + 256; }
+constexpr int kTmaMaxBlocks = 128;  // owned blocks per item (device.cu splits longer runs)
+constexpr int kTmaThreads = 288;    // 8 consumer warps + 1 producer warp
+
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+template <int R, int CH, int NST>
+__global__ void __launch_bounds__(kTmaThreads, 1) k_near_tma(const SymRowItem* __restrict__ items,
+                                                          const SymBlock* __restrict__ blocks,
+                                                          const double* __restrict__ G, std::int64_t E,
+                                                          const double* __restrict__ w, double* __restrict__ D,
+                                                          const double* __restrict__ xp, double* __restrict__ part) {
+  static_assert(CH >= 256 && CH % 2 == 0, "a chunk holds at least two columns of a 128-row leaf");
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) std::uint64_t full[NST], empty[NST];
+  __shared__ double xs_sh[128];
+  __shared__ SymBlock bl[kTmaMaxBlocks];
   const SymRowItem it = items[blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ld = it.ld;  // == rows (the TMA path takes whole-height blocks)
+  const int nb = it.bend - it.bbeg;
+  const int jc = min(128, (CH / ld) & ~1);  // even column count per chunk
+  if (tid < it.rows) xs_sh[tid] = xp[it.x_row0 + tid];
+  if (tid < nb) bl[tid] = blocks[it.bbeg + tid];
+  if (tid == 0) {
+    for (int q = 0; q < NST; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 8) {  // ---------------------------------------------- producer
+    if (lane == 0) {
+      int c = 0;
+      for (int b = 0; b < nb; ++b) {
+        const std::int64_t d_off = bl[b].d_off;
+        const int ncol = bl[b].ncol;
+        for (int j0 = 0; j0 < ncol; j0 += jc, ++c) {
+          const int slot = c % NST;
+          if (c >= NST) mbar_wait(&empty[slot], ((c / NST) - 1) & 1);
+          const int ncols = min(jc, ncol - j0);
+          const unsigned bytes = static_cast<unsigned>(((static_cast<std::int64_t>(ncols) * ld * 8) + 15) & ~15LL);
+          mbar_expect_tx(&full[slot], bytes * R);
+          const double* src = G + d_off + static_cast<std::int64_t>(j0) * ld;
+#pragma unroll
+          for (int k = 0; k < R; ++k) bulk_g2s(sm + (slot * R + k) * CH, src + k * E, bytes, &full[slot]);
+        }
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------ consumers
+  double* dc0 = sm + NST * R * CH;  // formed chunk, two buffers
+  double* xt0 = dc0 + 2 * CH;       // x_tau panel, two buffers of 128
+  const int ng = 256 / ld, rg = tid / ld, rr = tid - rg * ld;  // row product: (row rr, column group rg)
   double wr[R];
 #pragma unroll
   for (int k = 0; k < R; ++k) wr[k] = w[k];
-  double racc[4] = {0.0, 0.0, 0.0, 0.0};
-  double xs[4];
-  bool live[4];
+  double racc = 0.0;
+  // x_tau of the next chunk is loaded one chunk ahead (its latency would
+  // otherwise sit between the stage landing and the row product)
+  int b = 0, j0 = 0;
+  double xnext = (nb > 0 && tid < min(jc, bl[0].ncol)) ? xp[bl[0].x_col0 + tid] : 0.0;
+  for (int c = 0, buf = 0; b < nb; ++c, buf ^= 1) {
+    const std::int64_t d_off = bl[b].d_off, p_col = bl[b].p_col;
+    const int ncol = bl[b].ncol;
+    const int slot = c % NST;
+    const int ncols = min(jc, ncol - j0);
+    double* dc = dc0 + buf * CH;
+    double* xt = xt0 + buf * 128;
+    if (tid < ncols) xt[tid] = xnext;
+    int nb2 = b, nj2 = j0 + jc;  // cursor of the next chunk
+    if (nj2 >= ncol) {
+      ++nb2;
+      nj2 = 0;
+    }
+    if (nb2 < nb && tid < min(jc, bl[nb2].ncol - nj2)) xnext = xp[bl[nb2].x_col0 + nj2 + tid];
+    mbar_wait(&full[slot], (c / NST) & 1);
+    const double* S = sm + slot * R * CH;
+    const int nel = ncols * ld;
+    double* Dg = D + d_off + static_cast<std::int64_t>(j0) * ld;
+    for (int e = tid; e < nel; e += 256) {
+      double v = 0.0;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    live[q] = lane + 32 * q < it.rows;
-    xs[q] = live[q] ? xp[it.x_row0 + lane + 32 * q] : 0.0;
-  }
-  const std::int64_t ld = it.ld;
-  for (int b = it.bbeg; b < it.bend; ++b) {
-    const SymBlock blk = blocks[b];
-    const std::int64_t base = blk.d_off + it.i0 + lane;
-    const double* xt = xp + blk.x_col0;
-    const bool diag = blk.p_col < 0;
-    int j = warp;
-    for (; j + 8 < blk.ncol; j += 16) {
-      const double x0 = xt[j], x1 = xt[j + 8];
-      double v0[4], v1[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        v0[q] = 0.0;
-        v1[q] = 0.0;
-        if (live[q]) {
-          const std::int64_t o0 = base + j * ld + 32 * q, o1 = o0 + 8 * ld;
-          double s0[R], s1[R];
-#pragma unroll
-          for (int k = 0; k < R; ++k) {
-            s0[k] = ld_stream(G + k * E + o0);
-            s1[k] = ld_stream(G + k * E + o1);
-          }
-#pragma unroll
-          for (int k = 0; k < R; ++k) {
-            v0[q] += s0[k] * wr[k];
-            v1[q] += s1[k] * wr[k];
-          }
-          D[o0] = v0[q];
-          D[o1] = v1[q];
-        }
-      }
-      double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        racc[q] += v0[q] * x0 + v1[q] * x1;
-        c0 += v0[q] * xs[q];
-        c1 += v1[q] * xs[q];
-      }
-      if (!diag) {
-        c0 = warp_sum(c0);
-        c1 = warp_sum(c1);
-        if (lane == 0) {
-          part[blk.p_col + j] = c0;
-          part[blk.p_col + j + 8] = c1;
-        }
+      for (int k = 0; k < R; ++k) v += S[k * CH + e] * wr[k];
+      dc[e] = v;
+      Dg[e] = v;
+    }
+    consumers_sync();
+    if (tid == 0) mbar_arrive(&empty[slot]);  // stage formed: the producer may refill it
+    if (rg < ng) {
+      double r = 0.0;
+      for (int jj = rg; jj < ncols; jj += ng) r += dc[rr + jj * ld] * xt[jj];
+      racc += r;
+    }
+    if (p_col >= 0) {
+      for (int jj = warp; jj < ncols; jj += 8) {
+        double cs = 0.0;
+        for (int i = lane; i < ld; i += 32) cs += dc[i + jj * ld] * xs_sh[i];
+        cs = warp_sum(cs);
+        if (lane == 0) part[p_col + j0 + jj] = cs;
       }
     }
-    for (; j < blk.ncol; j += 8) {
-      const double x0 = xt[j];
-      double c0 = 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        double v = 0.0;
-        if (live[q]) {
-          const std::int64_t o = base + j * ld + 32 * q;
-          double s[R];
-#pragma unroll
-          for (int k = 0; k < R; ++k) s[k] = ld_stream(G + k * E + o);
-#pragma unroll
-          for (int k = 0; k < R; ++k) v += s[k] * wr[k];
-          D[o] = v;
-        }
-        racc[q] += v * x0;
-        c0 += v * xs[q];
-      }
-      if (!diag) {
-        c0 = warp_sum(c0);
-        if (lane == 0) part[blk.p_col + j] = c0;
-      }
-    }
+    b = nb2;
+    j0 = nj2;
   }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) red[warp][lane + 32 * q] = racc[q];
-  __syncthreads();
-  if (threadIdx.x < it.rows) {
-    double s = 0.0;
-#pragma unroll
-    for (int w2 = 0; w2 < 8; ++w2) s += red[w2][threadIdx.x];
-    part[it.p_row + threadIdx.x] = s;
+  consumers_sync();
+  double* red = dc0;  // reuse the formed-chunk buffers
+  red[tid] = rg < ng ? racc : 0.0;
+  consumers_sync();
+  if (tid < it.rows) {
+    double t = 0.0;
+    for (int g = 0; g < ng; ++g) t += red[tid + g * ld];
+    part[it.p_row + tid] = t;
   }
 }
 
@@ -1538,18 +1596,54 @@ void launch_near_mvm_symcsr(cudaStream_t st, const SymRowItem* items, int nitems
   if (nitems == 0) return;
   k_near_mvm_symcsr<<<nitems, 256, 0, st>>>(items, blocks, D, xp, part);
 }
-bool launch_near_inst_mvm(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks,
+// Snapshot-mode instantiate fused with apply (K1 + K6 in one pass over the
+// snapshots). Returns false for a rank without an instantiation (R > 16).
+bool launch_near_inst_tma(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks,
                           const double* G, std::int64_t E, int R, const double* w, double* D, const double* xp,
                           double* part) {
   if (nitems == 0) return true;
-  switch (R) {
-    case 4: k_near_inst_mvm<4><<<nitems, 256, 0, st>>>(items, blocks, G, E, w, D, xp, part); return true;
-    case 6: k_near_inst_mvm<6><<<nitems, 256, 0, st>>>(items, blocks, G, E, w, D, xp, part); return true;
-    case 8: k_near_inst_mvm<8><<<nitems, 256, 0, st>>>(items, blocks, G, E, w, D, xp, part); return true;
-    case 10: k_near_inst_mvm<10><<<nitems, 256, 0, st>>>(items, blocks, G, E, w, D, xp, part); return true;
-    default: return false;
+#define PHM_TMA(RR, NST) PHM_TMA_CH(RR, ((5120 / RR) & ~63) < 256 ? 256 : (((5120 / RR) & ~63) > 1024 ? 1024 : ((5120 / RR) & ~63)), NST)
+#define PHM_TMA_CH(RR, CHv, NST)                                                                              \
+  {                                                                                                           \
+    constexpr int CHc = CHv;                                                                                  \
+    const size_t smem = static_cast<size_t>(tma_smem_doubles(RR, CHc, NST)) * sizeof(double);                \
+    static bool attr = false;                                                                                 \
+    if (!attr) {                                                                                              \
+      cudaFuncSetAttribute(k_near_tma<RR, CHc, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+                           static_cast<int>(smem));                                                          \
+      attr = true;                                                                                            \
+    }                                                                                                         \
+    k_near_tma<RR, CHc, NST><<<nitems, kTmaThreads, smem, st>>>(items, blocks, G, E, w, D, xp, part);                 \
+    return true;                                                                                              \
   }
+  // two stages of about 40 KB (R slabs x CH doubles, 256 <= CH <= 1024): two
+  // CTAs per SM. Measured at C3 (R = 8): 8.9 ms for CH 640 x 2 stages and
+  // CH 512 x 3, 9.4 ms for 512 x 2, 10.3 ms for 768 x 2 (one CTA per SM),
+  // 18.5 ms for 256 x 6 (the per-chunk cost dominates small chunks).
+  switch (R) {
+    case 1: PHM_TMA(1, 2)
+    case 2: PHM_TMA(2, 2)
+    case 3: PHM_TMA(3, 2)
+    case 4: PHM_TMA(4, 2)
+    case 5: PHM_TMA(5, 2)
+    case 6: PHM_TMA(6, 2)
+    case 7: PHM_TMA(7, 2)
+    case 8: PHM_TMA(8, 2)
+    case 9: PHM_TMA(9, 2)
+    case 10: PHM_TMA(10, 2)
+    case 11: PHM_TMA(11, 2)
+    case 12: PHM_TMA(12, 2)
+    case 13: PHM_TMA(13, 2)
+    case 14: PHM_TMA(14, 2)
+    case 15: PHM_TMA(15, 2)
+    case 16: PHM_TMA(16, 2)
+    default: break;
+  }
+#undef PHM_TMA
+#undef PHM_TMA_CH
+  return false;
 }
+
 void launch_near_gather(cudaStream_t st, int nleaves, const std::int64_t* leaf_row0, const std::int32_t* leaf_rows,
                         const std::int32_t* seg_beg, const GatherSeg* segs, const double* part, double* yp) {
   if (nleaves == 0) return;
