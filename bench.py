@@ -151,6 +151,17 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows), "in_timed_window": in_window}
 
 
+def measured_traffic(kernel, config, world):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
+    --set full capture (profiles/r01_traffic.json, taken on c3 at N=1); None
+    for any other workload."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    if config != "c3" or world != 1 or not os.path.exists(path):
+        return None
+    rec = json.load(open(path)).get(kernel)
+    return rec["traffic_bytes_per_launch"] if rec else None
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -362,6 +373,7 @@ def run_ours(args):
             cls_bytes += 8 * (mid.size + info["P"] * (rl + rr) + rl * rr + info["P"] ** 2)
         b_inst, b_mvm = algorithmic_bytes(info, c, cls_bytes)
         k1_avg = k1_ms / max(1, k1_n)
+        traffic = measured_traffic(k1_desc.split()[0], args.config, world)
         k1_bytes = 8 * info["near_stream_elems"]  # R slab reads + 1 write per stored near entry
         achieved = k1_bytes / (k1_avg * 1e-3) / 1e9
         mvm_ms = apply_ms
@@ -396,7 +408,7 @@ def run_ours(args):
                        "parallelism": ("theta-sharded replicas" if sweep else f"rows sharded over {world}"),
                        "l2": "inputs (near snapshots) larger than L2; no flush needed"},
             "roofline": {"bound": "hbm", "kernel": k1_desc, "achieved": achieved,
-                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg},
             "phases": {"instantiate_ms": inst_ms, "apply_ms": apply_ms,
                        "instantiate_GB_s": b_inst / (inst_ms * 1e-3) / 1e9},

@@ -220,7 +220,16 @@ std::shared_ptr<Context> context_create(int device) {
   auto ctx = std::make_shared<Context>();
   ctx->device = device;
   CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  {
+    // the side stream carries the compute-bound far chain that runs beside
+    // the HBM-bound near pass; with the higher priority its CTAs take SM
+    // slots as soon as near-pass CTAs retire
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const char* e = std::getenv("PHM_SIDE_PRIORITY");
+    const bool prio = !(e && std::atoi(e) == 0);
+    CK(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio ? hi : lo));
+  }
   CK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->aux_ev, cudaEventDisableTiming));
