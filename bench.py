@@ -322,6 +322,18 @@ def run_ours(args):
     inst_ms = time_loop(lambda s: inst.reinstantiate([theta_of(s)]))
     apply_ms = (time_loop(lambda s: inst.apply_device(x_dev.data_ptr(), y_dev.data_ptr(), m))
                 if not row_shard else None)
+    # per-kernel split of the apply phase (separate loop: the timers add events)
+    apply_timers = {}
+    if not row_shard:
+        ctx.enable_timing(True)
+        ctx.reset_timers()
+        time_loop(lambda s: inst.apply_device(x_dev.data_ptr(), y_dev.data_ptr(), m))
+        for name in ("near_mvm", "near_gather", "near_mrhs", "coupling", "coupling_reduce", "leaf_fwd", "up", "down",
+                     "leaf_bwd", "gather", "scatter", "far_h"):
+            t, cnt = ctx.timer(name)
+            if cnt:
+                apply_timers[name] = {"ms_per_launch": t / cnt, "launches": cnt}
+        ctx.enable_timing(False)
     t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
@@ -377,6 +389,13 @@ def run_ours(args):
         k1_bytes = 8 * info["near_stream_elems"]  # R slab reads + 1 write per stored near entry
         achieved = k1_bytes / (k1_avg * 1e-3) / 1e9
         mvm_ms = apply_ms
+        # the near-field GEMV kernel of apply alone: reads every stored entry once
+        nm = apply_timers.get("near_mvm")
+        near_gemv = None
+        if nm and m == 1:
+            gb = 8 * info["near_stored"] / (nm["ms_per_launch"] * 1e-3) / 1e9
+            near_gemv = {"kernel": "k_near_tma_apply (K6 over TMA)", "ms": nm["ms_per_launch"],
+                         "bytes": 8 * info["near_stored"], "GB_s": gb, "frac": gb / peak}
         # fp64 tensor-core (DMMA) work of the MVM: coupling GEMMs and, for
         # block right-hand sides, the near-field contraction
         cp = timers.get("coupling")
@@ -415,6 +434,8 @@ def run_ours(args):
             "mvm": {"ms": mvm_ms, "algorithmic_bytes": b_mvm,
                     "GB_s": b_mvm / (mvm_ms * 1e-3) / 1e9 if mvm_ms else None,
                     "frac_of_hbm": (b_mvm / (mvm_ms * 1e-3) / 1e9) / peak if mvm_ms else None},
+            "near_gemv": near_gemv,
+            "apply_kernels": apply_timers,
             "dmma": dmma,
             "instantiate_algorithmic_bytes": b_inst,
             "kernels": timers,

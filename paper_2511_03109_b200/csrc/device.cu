@@ -51,6 +51,8 @@ void launch_coupling_reduce(cudaStream_t, const std::int32_t*, const std::int32_
 void launch_near_mvm(cudaStream_t, const RowItem*, int, const std::int64_t*, const std::int32_t*,
                      const std::int64_t*, const double*, const double*, double*);
 void launch_near_mvm_sym(cudaStream_t, const SymItem*, int, const double*, const double*, double*);
+void launch_near_tma_apply(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
+                           double*, int*);
 void launch_near_mvm_symcsr(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
                             double*);
 bool launch_near_inst_tma(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, std::int64_t, int,
@@ -286,6 +288,7 @@ struct DevMatrix {
   DBuf sym_items, sym_blocks, g_row0, g_rows, g_sbeg, g_segs, sym_part;
   int n_sym_items = 0, n_gather_leaves = 0;
   bool near_tma = false;  // every item spans its whole leaf: TMA near pass
+  DBuf work_ctr;          // persistent near kernels' item counter
   // K9 multi-RHS near field (DMMA), CSR by sigma over stored blocks
   DBuf k9_items, k9_tb, k9_tn, k9_doff, k9_ld, k9_tr;
   int n_k9_items = 0;
@@ -758,6 +761,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     M.n_sym_items = static_cast<int>(items.size());
     M.n_gather_leaves = static_cast<int>(lrow0.size());
     M.near_tma = !items.empty();
+    M.work_ctr.alloc(sizeof(int));
     for (const auto& it : items)  // whole-leaf items (k_near_tma)
       M.near_tma = M.near_tma && it.i0 == 0 && it.rows == it.ld;
     upload(M.sym_items, items, st);
@@ -1312,9 +1316,18 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
     });
   for (Index c = 0; c < (block_rhs ? 0 : m); ++c) {
     ctx.run_on(st, "near_mvm", [&] {
-      dev::launch_near_mvm_symcsr(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
-                                  M.sym_blocks.as<dev::SymBlock>(), I.D.as<double>(), M.xp.as<double>() + c * M.n,
-                                  M.sym_part.as<double>());
+      static const bool tma = [] {
+        const char* e = std::getenv("PHM_NEAR_TMA");
+        return !(e && std::atoi(e) == 0);
+      }();
+      if (M.near_tma && tma)
+        dev::launch_near_tma_apply(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
+                                   M.sym_blocks.as<dev::SymBlock>(), I.D.as<double>(), M.xp.as<double>() + c * M.n,
+                                   M.sym_part.as<double>(), M.work_ctr.as<int>());
+      else
+        dev::launch_near_mvm_symcsr(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
+                                    M.sym_blocks.as<dev::SymBlock>(), I.D.as<double>(), M.xp.as<double>() + c * M.n,
+                                    M.sym_part.as<double>());
     });
     near_gather(I, c, st);
   }
@@ -1355,6 +1368,22 @@ void far_finish(DevInstance& I, Index m, cudaStream_t st) {
 void apply_tree_order(DevInstance& I, Index m) {
   DevMatrix& M = *I.M;
   Context& ctx = *M.ctx;
+  static const int overlap = [] {
+    const char* e = std::getenv("PHM_APPLY_OVERLAP");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (M.h2 && overlap == 0) {  // serial: far chain, then the near GEMV
+    far_chain(I, m, ctx.stream);
+    near_product(I, m, ctx.stream);
+    far_finish(I, m, ctx.stream);
+    return;
+  }
+  if (M.h2 && overlap == 2) {  // serial: near GEMV first
+    near_product(I, m, ctx.stream);
+    far_chain(I, m, ctx.stream);
+    far_finish(I, m, ctx.stream);
+    return;
+  }
   if (M.h2) {
     ctx.fork();
     far_chain(I, m, ctx.side);

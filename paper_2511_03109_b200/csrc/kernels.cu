@@ -1154,6 +1154,187 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_near_tma(const SymRowItem* _
   }
 }
 
+// K6 over TMA (apply alone, one RHS): the producer / consumer split of
+// k_near_tma with D itself as the only slab, chunks of up to 64 columns of a
+// block. Persistent: a fixed grid (one CTA per SM by default, so the far
+// chain's kernels can sit beside it on every SM) takes items from a work
+// counter; the producer warp fetches the next item's block list into a
+// double-buffered slot while the consumers finish the current one, so the
+// stage ring never drains at item boundaries.
+// The consumers work register-tiled so that each D element costs a few
+// instructions: thread t owns rows rt + 16 q (rt = t mod 16, q < 8) and the
+// 4 columns 4 cg .. 4 cg + 3 of the chunk (cg = t / 16). Row partials
+// (D x_tau) stay in registers across the item; column partials (D^T x_sigma)
+// are reduced over the 16 lanes of a half-warp with a transpose-reduce (5
+// shuffles for 4 columns). Each warp releases a stage on its own (empty[]
+// counts 8 warp arrivals). 96 registers: 9 warps x 2 CTAs fit the per-SMSP
+// register file.
+template <int CH, int NST>
+__global__ void __maxnreg__(96) k_near_tma_apply(const SymRowItem* __restrict__ items, int nitems,
+                                                 const SymBlock* __restrict__ blocks, const double* __restrict__ D,
+                                                 const double* __restrict__ xp, double* __restrict__ part,
+                                                 int* __restrict__ counter) {
+  static_assert(CH >= 128 * 16, "a chunk holds 16 columns of a 128-row leaf");
+  // stage = D chunk (CH + 2 doubles, shifted by one when it starts on an odd
+  // element) + the chunk's x_tau panel (64 + 2); then 8 x 128 row partials
+  constexpr int kStage = CH + 2 + 66;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) std::uint64_t full[NST], empty[NST], ifull[2], iempty[2];
+  __shared__ SymBlock bl[2][kTmaMaxBlocks];
+  __shared__ SymRowItem itm[2];
+  __shared__ int iidx[2];
+  __shared__ double xs_item[2][128];  // x_sigma of the item's rows
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int q = 0; q < NST; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 8);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&ifull[q], 1);
+      mbar_init(&iempty[q], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 8) {  // ------------------------------------------------ producer
+    int c = 0;
+    for (int n = 0;; ++n) {
+      const int ib = n & 1;
+      if (n >= 2) mbar_wait(&iempty[ib], ((n >> 1) - 1) & 1);
+      int idx = 0;
+      if (lane == 0) idx = atomicAdd(counter, 1);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      if (idx < nitems) {
+        const SymRowItem it = items[idx];
+        for (int t = lane; t < it.bend - it.bbeg; t += 32) bl[ib][t] = blocks[it.bbeg + t];
+        for (int t = lane; t < 128; t += 32) xs_item[ib][t] = t < it.rows ? xp[it.x_row0 + t] : 0.0;
+        if (lane == 0) itm[ib] = it;
+      }
+      if (lane == 0) iidx[ib] = idx;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ifull[ib]);
+      if (idx >= nitems) break;
+      if (lane == 0) {
+        const SymRowItem& it = itm[ib];
+        const int ld = it.ld, nb = it.bend - it.bbeg, jc = min(64, CH / ld);
+        for (int b = 0; b < nb; ++b) {
+          const std::int64_t d_off = bl[ib][b].d_off, x_col0 = bl[ib][b].x_col0;
+          const int ncol = bl[ib][b].ncol;
+          for (int j0 = 0; j0 < ncol; j0 += jc, ++c) {
+            const int slot = c % NST;
+            if (c >= NST) mbar_wait(&empty[slot], ((c / NST) - 1) & 1);
+            const int ncols = min(jc, ncol - j0);
+            // the source may start 8 bytes past a 16-byte boundary (odd ld):
+            // copy from the aligned address below and shift in shared memory
+            const std::int64_t e0 = d_off + static_cast<std::int64_t>(j0) * ld;
+            const std::int64_t ea = e0 & ~std::int64_t(1);
+            const std::int64_t nbytes = (((e0 + static_cast<std::int64_t>(ncols) * ld - ea) + 1) & ~std::int64_t(1)) * 8;
+            // x_tau panel: xp + column may sit on an odd element (odd n, RHS > 0)
+            const double* xsrc = xp + x_col0 + j0;
+            const int xsh = static_cast<int>((reinterpret_cast<std::uintptr_t>(xsrc) >> 3) & 1);
+            const unsigned xbytes = static_cast<unsigned>(((ncols + xsh + 1) & ~1) * 8);
+            mbar_expect_tx(&full[slot], static_cast<unsigned>(nbytes) + xbytes);
+            bulk_g2s(sm + slot * kStage, D + ea, static_cast<unsigned>(nbytes), &full[slot]);
+            bulk_g2s(sm + slot * kStage + CH + 2, xsrc - xsh, xbytes, &full[slot]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  double* red = sm + NST * kStage;
+  const int rt = tid & 15, cg = tid >> 4;  // row lane, column group
+  const int l16 = lane & 15;
+  int c = 0;
+  for (int n = 0;; ++n) {
+    const int ib = n & 1;
+    mbar_wait(&ifull[ib], (n >> 1) & 1);
+    if (iidx[ib] >= nitems) break;
+    const SymRowItem it = itm[ib];
+    const SymBlock* B = bl[ib];
+    const int ld = it.ld, nb = it.bend - it.bbeg, jc = min(64, CH / ld);
+    double xs[8], racc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      xs[q] = xs_item[ib][rt + 16 * q];
+      racc[q] = 0.0;
+    }
+    for (int b = 0, j0 = 0; b < nb; ++c) {
+      const std::int64_t p_col = B[b].p_col;
+      const int ncol = B[b].ncol;
+      const int slot = c % NST;
+      const int ncols = min(jc, ncol - j0);
+      int nb2 = b, nj2 = j0 + jc;
+      if (nj2 >= ncol) {
+        ++nb2;
+        nj2 = 0;
+      }
+      mbar_wait(&full[slot], (c / NST) & 1);
+      const double* Dc = sm + slot * kStage + ((B[b].d_off + static_cast<std::int64_t>(j0) * ld) & 1);
+      const double* Xc = sm + slot * kStage + CH + 2 +
+                         ((reinterpret_cast<std::uintptr_t>(xp + B[b].x_col0 + j0) >> 3) & 1);
+      double xt[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) xt[k] = Xc[4 * cg + k];  // past ncols: finite, never used
+      double cacc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = 4 * cg + k;
+        if (j < ncols) {
+          const double* col = Dc + j * ld;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int r = rt + 16 * q;
+            if (r < ld) {
+              const double v = col[r];
+              racc[q] += v * xt[k];
+              cacc[k] += v * xs[q];
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the stage
+      if (p_col >= 0) {  // warp-uniform (one block per chunk)
+        // transpose-reduce 4 column partials over the 16 lanes of the half-warp
+        const bool b3 = l16 & 8, b2 = l16 & 4;
+        double k0 = b3 ? cacc[2] : cacc[0], k1 = b3 ? cacc[3] : cacc[1];
+        const double s0 = b3 ? cacc[0] : cacc[2], s1 = b3 ? cacc[1] : cacc[3];
+        k0 += __shfl_xor_sync(0xffffffffu, s0, 8);
+        k1 += __shfl_xor_sync(0xffffffffu, s1, 8);
+        double kk = b2 ? k1 : k0;
+        kk += __shfl_xor_sync(0xffffffffu, b2 ? k0 : k1, 4);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+        const int j = 4 * cg + (l16 >> 2);
+        if ((l16 & 3) == 0 && j < ncols) part[p_col + j0 + j] = kk;
+      }
+      b = nb2;
+      j0 = nj2;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&iempty[ib]);  // block list no longer read
+    // row sums over the 16 column groups: the two half-warps first, then the
+    // 8 warps in warp order
+#pragma unroll
+    for (int q = 0; q < 8; ++q) racc[q] += __shfl_xor_sync(0xffffffffu, racc[q], 16);
+    consumers_sync();
+    if (lane < 16) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) red[warp * 128 + rt + 16 * q] = racc[q];
+    }
+    consumers_sync();
+    if (tid < it.rows) {
+      double t = 0.0;
+      for (int g = 0; g < 8; ++g) t += red[g * 128 + tid];
+      part[it.p_row + tid] = t;
+    }
+  }
+}
+
 // y[rows of leaf] = sum of the leaf's partial segments, in list order.
 __global__ void k_near_gather(const std::int64_t* __restrict__ leaf_row0, const std::int32_t* __restrict__ leaf_rows,
                               const std::int32_t* __restrict__ seg_beg, const GatherSeg* __restrict__ segs,
@@ -1591,6 +1772,31 @@ void launch_near_mvm_sym(cudaStream_t st, const SymItem* items, int nitems, cons
   // than this CTA-per-block version at C3 (242 registers, low occupancy).
   k_near_mvm_sym<<<nitems, 256, 0, st>>>(items, D, xp, part);
 }
+void launch_near_tma_apply(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks,
+                           const double* D, const double* xp, double* part, int* counter) {
+  if (nitems == 0) return;
+  // 3 stages of 24 KB (48 columns of a 64-row leaf): two CTAs per SM
+  constexpr int CH = 3072, NST = 3;
+  const size_t smem = static_cast<size_t>(NST * (CH + 2 + 66) + 8 * 128) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_near_tma_apply<CH, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cudaFuncSetAttribute(k_near_tma_apply<CH, NST>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    attr = true;
+  }
+  static const int per_sm = [] {
+    const char* e = std::getenv("PHM_NEAR_CTAS_PER_SM");
+    const int k = e ? std::atoi(e) : 2;
+    return k >= 1 && k <= 2 ? k : 2;
+  }();
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaMemsetAsync(counter, 0, sizeof(int), st);
+  const int grid = std::min(nitems, sms * per_sm);
+  k_near_tma_apply<CH, NST><<<grid, kTmaThreads, smem, st>>>(items, nitems, blocks, D, xp, part, counter);
+}
 void launch_near_mvm_symcsr(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks,
                             const double* D, const double* xp, double* part) {
   if (nitems == 0) return;
@@ -1611,6 +1817,8 @@ bool launch_near_inst_tma(cudaStream_t st, const SymRowItem* items, int nitems, 
     if (!attr) {                                                                                              \
       cudaFuncSetAttribute(k_near_tma<RR, CHc, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
                            static_cast<int>(smem));                                                          \
+      cudaFuncSetAttribute(k_near_tma<RR, CHc, NST>, cudaFuncAttributePreferredSharedMemoryCarveout,          \
+                           cudaSharedmemCarveoutMaxShared);                                                  \
       attr = true;                                                                                            \
     }                                                                                                         \
     k_near_tma<RR, CHc, NST><<<nitems, kTmaThreads, smem, st>>>(items, blocks, G, E, w, D, xp, part);                 \
