@@ -355,3 +355,48 @@ def test_reinstantiate_in_place(ph, po):
     b = ph.instantiate(pm, [0.1])
     b.reinstantiate([0.4])
     assert np.array_equal(b.apply(x), ya)
+
+
+@pytest.mark.parametrize("n,l_max", [(2999, 2), (2001, 1)])
+def test_near_gemv_paths_odd_n_and_large_leaves(ph, po, n, l_max):
+    """The TMA near passes take whole leaves of <= 128 rows (l_max 2 here);
+    larger leaves (l_max 1: ~250 rows) fall back to the row-sliced kernel.
+    Odd n puts the x panels of RHS columns > 0 on odd elements."""
+    pts = ph.generate_points(n, 3, 31)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=l_max, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    sizes = _node_sizes(pm)
+    ints, _ = pm.nodes()
+    leaf_max = max(int(sizes[i]) for i in range(len(sizes)) if ints[i, 0] == l_max)
+    assert (leaf_max <= 128) == (l_max == 2)
+    inst = ph.instantiate(pm, [0.19])
+    oi = om.instantiate([0.19])
+    rng = np.random.default_rng(n)
+    for m in (1, 2, 3):
+        X = rng.standard_normal((n, m)) if m > 1 else rng.standard_normal(n)
+        assert rel(inst.apply(X), oi.apply(X)) <= TOL_Y
+    x = rng.standard_normal(n)
+    y = inst.instantiate_apply([0.44], x)
+    assert rel(y, om.instantiate([0.44]).apply(x)) <= TOL_Y
+
+
+@pytest.mark.parametrize("p_theta", [3, 5, 10, 13, 20])
+def test_fused_near_pass_across_snapshot_ranks(ph, po, p_theta):
+    """Each snapshot rank R <= 16 has its own k_near_tma instantiation (stage
+    geometry depends on R); R > 16 takes the separate K1 + K6 kernels."""
+    pts = ph.generate_points(2400, 3, 17)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.MATERN32, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=p_theta, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    inst = ph.instantiate(pm, [0.3])
+    x = ph.generate_normal(2400, 6)
+    near, _, _ = pm.blocks()
+    sizes = _node_sizes(pm)
+    for theta in ([0.06], [0.377]):
+        y = inst.instantiate_apply(theta, x)
+        assert rel(y, om.instantiate(theta).apply(x)) <= TOL_Y
+        ref = ph.instantiate(pm, theta)
+        for k in range(0, len(near), 11):
+            sh = (sizes[near[k][0]], sizes[near[k][1]])
+            assert np.array_equal(inst.near_d(k, sh), ref.near_d(k, sh))
