@@ -223,9 +223,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the multi-rank path on a one-GPU box: every rank on
+    # cuda:0, gloo for the exchange (never a performance number)
+    same_gpu = os.environ.get("PHM_BENCH_FUNCTIONAL_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = CONFIGS[args.config]
     sweep = c.get("sweep", False)          # C5: thetas sharded over ranks, no communication
     m = args.rhs or c.get("rhs", 1)        # right-hand sides per MVM
@@ -252,9 +260,9 @@ def run_ours(args):
     y_dev = torch.empty((m, n), dtype=torch.float64, device="cuda")
     rows = info["row_end"] - info["row_begin"]
     if row_shard:
-        from paper_2511_03109_b200.dist import RowGather, row_counts
+        from paper_2511_03109_b200.dist import PartialSum
 
-        rg = RowGather(row_counts(rows), 1, device="cuda")
+        psum = PartialSum(n, 1, device="cuda")
     inst = ph.instantiate(pm, [thetas[0]])
 
     def theta_of(s):
@@ -265,10 +273,11 @@ def run_ours(args):
             # instantiate(theta_s) + MVM as one overlapped schedule
             inst.instantiate_apply_device([theta_of(s)], x_dev.data_ptr(), y_dev.data_ptr(), m)
         else:
-            inst.reinstantiate([theta_of(s)])
-            inst.apply_rows_device(x_dev.data_ptr(), rg.send.data_ptr(), 1)
-            yperm = rg.gather(rg.send)  # NCCL all-gather(v) of the row blocks
-            ph.lib().phm_unpermute_device(pm._h, ph._P(yperm.data_ptr()), ph._P(y_dev.data_ptr()), 1)
+            # this rank's partial y (its owner leaves' near pairs, both ways,
+            # and its rows' far field), summed over ranks by one all-reduce
+            inst.instantiate_apply_partial_device([theta_of(s)], x_dev.data_ptr(), psum.buf.data_ptr(), 1)
+            psum.reduce()
+            ph.lib().phm_unpermute_device(pm._h, ph._P(psum.buf.data_ptr()), ph._P(y_dev.data_ptr()), 1)
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -341,12 +350,19 @@ def run_ours(args):
 
     # e2e through the public API with host buffers (rank-local)
     e2e = None
-    if not row_shard:
+    if True:
         y_host = torch.empty((m, n), dtype=torch.float64).pin_memory()
         xh, yh = x_host.numpy(), y_host.numpy()
         from ctypes import POINTER, c_double
 
         def e2e_step(s):
+            if row_shard:
+                # host x -> every rank, sharded step + all-reduce, y -> host
+                x_dev.copy_(x_host, non_blocking=True)
+                step(s)
+                y_host.copy_(y_dev, non_blocking=True)
+                stream.synchronize()
+                return
             th = np.array([theta_of(s)])
             ph._check(ph.lib().phm_instantiate_apply(inst._h, th.ctypes.data_as(POINTER(c_double)), 1,
                                                      xh.ctypes.data_as(POINTER(c_double)), n,
@@ -405,9 +421,12 @@ def run_ours(args):
             if cp else None,
             "near_mrhs_tflops": (2.0 * info["near_entries"] * m / (k9["ms_per_launch"] * 1e-3) / 1e12) if k9 else None,
         }
-        what = ("theta/s (instantiate + %d-RHS H2 MVM per theta), theta sweep sharded over GPUs" % m if sweep else
-                "theta-instantiations/s (instantiate + H2 MVM per theta) at n=2^18, 3D" if m == 1 else
-                "theta/s (instantiate + %d-RHS H2 MVM per theta) at n=2^18, 3D" % m)
+        where = "n=2^%d, %dD" % (n.bit_length() - 1, c["d"]) if n & (n - 1) == 0 else "n=%d, %dD" % (n, c["d"])
+        fmt_name = "H2" if c["fmt"] == "h2" else "H"
+        what = ("theta/s (instantiate + %d-RHS %s MVM per theta) at %s, theta sweep sharded over GPUs"
+                % (m, fmt_name, where) if sweep else
+                "theta-instantiations/s (instantiate + %s MVM per theta) at %s" % (fmt_name, where) if m == 1 else
+                "theta/s (instantiate + %d-RHS %s MVM per theta) at %s" % (m, fmt_name, where))
         line = {
             "metric": what,
             "value": (world if sweep else 1) * args.steps * 1000.0 / ms,

@@ -194,6 +194,16 @@ int phm_apply_device(phm_instance inst, const double* x_dev, double* y_dev, int6
 /* Row-sharded apply: this shard's rows [row_begin, row_end) of y in tree
  * order (rows x m, column-major); gather across ranks, then unpermute. */
 int phm_apply_rows_device(phm_instance inst, const double* x_dev, double* yrows_dev, int64_t m);
+/* Row-sharded apply with symmetric near storage (each rank stores the near
+ * pairs its owner leaves hold, so its transposed products reach other
+ * ranks' rows): this shard's full-length partial y in tree order (n x m);
+ * sum the partials across ranks (all-reduce), then unpermute. Also valid on
+ * an unsharded matrix (the partial is then y itself, in tree order). */
+int phm_apply_partial_device(phm_instance inst, const double* x_dev, double* ypart_dev, int64_t m);
+/* phm_reinstantiate(theta) + phm_apply_partial_device in one schedule (the
+ * sharded HPO step). */
+int phm_instantiate_apply_partial_device(phm_instance inst, const double* theta, int n_theta, const double* x_dev,
+                                         double* ypart_dev, int64_t m);
 int phm_unpermute_device(phm_matrix m, const double* yperm_dev, double* y_dev, int64_t mcols);
 /* estimate_error of the reference harness (harness.cpp:183-236): probe rows
  * sampled without replacement and x ~ U[0,1) from the reference's Rng

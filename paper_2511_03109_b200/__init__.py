@@ -136,6 +136,8 @@ SIGNATURES = {
     "phm_instantiate_apply": ([_P, _DP, C.c_int, _DP, C.c_int64, _DP, C.c_int64], C.c_int),
     "phm_instantiate_apply_device": ([_P, _DP, C.c_int, _P, _P, C.c_int64], C.c_int),
     "phm_apply_rows_device": ([_P, _P, _P, C.c_int64], C.c_int),
+    "phm_apply_partial_device": ([_P, _P, _P, C.c_int64], C.c_int),
+    "phm_instantiate_apply_partial_device": ([_P, _DP, C.c_int, _P, _P, C.c_int64], C.c_int),
     "phm_unpermute_device": ([_P, _P, _P, C.c_int64], C.c_int),
     "phm_to_dense": ([_P, _DP, C.c_int64], C.c_int),
     "phm_estimate_error": ([_P, C.c_int64, C.c_uint64, _DP, _I64P, _DP, _DP, _DP], C.c_int),
@@ -499,6 +501,15 @@ class InstantiatedMatrix:
 
     def apply_rows_device(self, x_ptr: int, yrows_ptr: int, m: int = 1) -> None:
         _check(lib().phm_apply_rows_device(self._h, _P(x_ptr), _P(yrows_ptr), m))
+
+    def apply_partial_device(self, x_ptr: int, ypart_ptr: int, m: int = 1) -> None:
+        """This shard's full-length partial y (tree order, n x m); sum across ranks."""
+        _check(lib().phm_apply_partial_device(self._h, _P(x_ptr), _P(ypart_ptr), m))
+
+    def instantiate_apply_partial_device(self, theta, x_ptr: int, ypart_ptr: int, m: int = 1) -> None:
+        th = _f64(theta).ravel()
+        _check(lib().phm_instantiate_apply_partial_device(self._h, _dp(th), th.size, _P(x_ptr), _P(ypart_ptr), m))
+        self.theta = list(th)
 
     def far_h(self, i: int) -> np.ndarray:
         r, c = C.c_int64(), C.c_int64()

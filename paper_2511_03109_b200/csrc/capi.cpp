@@ -665,7 +665,7 @@ int phm_apply_device(phm_instance inst, const double* x, double* y, int64_t m) {
     need(y, "y");
     const auto& H = phm::matrix_host(*inst->m);
     if (H.row_begin != 0 || H.row_end != H.n())
-      throw std::logic_error("apply on a row shard: use phm_apply_rows_device and gather y");
+      throw std::logic_error("apply on a row shard: use phm_apply_partial_device (or phm_apply_rows_device) across ranks");
     phm::apply_device(*inst->inst, x, y, m);
   });
 }
@@ -675,6 +675,25 @@ int phm_apply_rows_device(phm_instance inst, const double* x, double* yrows, int
     need(x, "x");
     need(yrows, "y");
     phm::apply_device_rows(*inst->inst, x, yrows, m);
+  });
+}
+int phm_apply_partial_device(phm_instance inst, const double* x, double* ypart, int64_t m) {
+  return guarded([&] {
+    need(inst, "instance");
+    need(x, "x");
+    need(ypart, "y");
+    phm::apply_device_partial(*inst->inst, x, ypart, m);
+  });
+}
+int phm_instantiate_apply_partial_device(phm_instance inst, const double* theta, int n_theta, const double* x,
+                                         double* ypart, int64_t m) {
+  return guarded([&] {
+    need(inst, "instance");
+    need(theta, "theta");
+    need(x, "x");
+    need(ypart, "y");
+    auto& H = const_cast<phm::HostMatrix&>(phm::matrix_host(*inst->m));
+    phm::instantiate_apply_partial_device(*inst->inst, theta, n_theta, x, ypart, m, &H.counters);
   });
 }
 int phm_unpermute_device(phm_matrix m, const double* yperm, double* y, int64_t mcols) {

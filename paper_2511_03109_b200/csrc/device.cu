@@ -283,6 +283,7 @@ struct DevMatrix {
   int n_row_items = 0;
   // symmetric near storage (sigma <= tau blocks only)
   bool sym = false;
+  bool sharded = false;          // a row shard (rows [row_begin, row_end) of y)
   std::vector<char> near_trans;  // block stored as the transpose of its partner
   std::int64_t E_logical = 0;    // sum of n_sigma n_tau over local near blocks
   DBuf sym_items, sym_blocks, g_row0, g_rows, g_sbeg, g_segs, sym_part;
@@ -518,8 +519,11 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
   // family is radial, so with snapshots (or direct evaluation) D_{tau,sigma}
   // equals D_{sigma,tau}^T bit for bit (the squared distance accumulates the
   // same rounded squares). Only blocks with sigma <= tau are stored.
-  M.sym = M.mode == NearMode::Snapshot && cfg.symmetric_near &&
-          cfg.shard_count == 1;
+  // On a row shard the rank stores the pairs whose owner leaf it holds; the
+  // transposed products land on rows of other ranks, so a sharded apply
+  // yields a full-length partial y that the ranks sum (all-reduce).
+  M.sym = M.mode == NearMode::Snapshot && cfg.symmetric_near;
+  M.sharded = H.row_begin != 0 || H.row_end != n;
   M.near_trans.assign(nnear, 0);
   std::vector<Index> canon(nnear);
   for (Index b = 0; b < nnear; ++b) canon[b] = b;
@@ -1303,10 +1307,14 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
   DevMatrix& M = *I.M;
   Context& ctx = *M.ctx;
   const int mm = static_cast<int>(m);
-  if (M.n_gather_leaves == 0 || M.n_k9_items == 0) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
+  // A shard's gather touches only the leaves its blocks reach: clear the rest.
+  if (M.n_gather_leaves == 0 || M.n_k9_items == 0 || M.sharded)
+    CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
   // Block right-hand sides: the near product is a dense contraction, so it
   // runs on fp64 tensor cores (K9); single vectors stay on the HBM GEMV.
-  const bool block_rhs = m >= kMrhsMin;
+  // K9 computes rows sigma only, so a symmetric shard (whose transposed
+  // products belong to other ranks' rows) keeps the two-sided GEMV.
+  const bool block_rhs = m >= kMrhsMin && !(M.sym && M.sharded);
   if (block_rhs)
     ctx.run_on(st, "near_mrhs", [&] {
       dev::launch_near_mrhs(st, M.k9_items.as<dev::MrhsItem>(), M.n_k9_items, M.k9_tb.as<std::int64_t>(),
@@ -1425,20 +1433,23 @@ void apply_host(DevInstance& I, const double* x, double* y, Index m) {
 // run on the side stream while K1 streams the near field on the main
 // stream; the near GEMV then waits for the gathered x and the far chain.
 // Results are identical to reinstantiate() + apply_device().
-void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, const double* x_dev, double* y_dev,
-                              Index m, StageCounters* counters) {
+namespace {
+// instantiate(theta) + apply(x) leaving y (this shard's part) in tree order
+// in M.yp.
+void instantiate_apply_tree(DevInstance& I, const double* theta, int n_theta, const double* x_dev, Index m,
+                            StageCounters* counters) {
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   PHM_CHECK(m >= 1, "apply: m must be >= 1");
-  if (H.row_begin != 0 || H.row_end != M.n)
-    throw std::logic_error("fused instantiate+apply on a row shard: use the sharded apply");
   CK(cudaSetDevice(M.ctx->device));
   const auto v = parametric_vectors(H.grids, theta, n_theta);
   const dev::ThetaV tv = make_theta_v(v);
   ensure_workspace(M, m);
   if (!M.h2 || M.mode == NearMode::Direct) {
     run_instantiate(I, theta, n_theta, counters);
-    apply_device(I, x_dev, y_dev, m);
+    cudaStream_t st = M.st();
+    M.ctx->run("gather", [&] { dev::launch_gather(st, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
+    apply_tree_order(I, m);
     return;
   }
   I.theta.assign(theta, theta + n_theta);
@@ -1470,7 +1481,7 @@ void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, 
                                         M.sym_part.as<double>());
     });
     if (fused) {
-      if (M.n_gather_leaves == 0) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
+      if (M.n_gather_leaves == 0 || M.sharded) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
       near_gather(I, 0, st);
     }
   }
@@ -1481,7 +1492,25 @@ void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, 
   }
   ctx.join();
   far_finish(I, m, st);
-  ctx.run("scatter", [&] { dev::launch_scatter(st, M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev); });
+}
+}  // namespace
+
+void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, const double* x_dev, double* y_dev,
+                              Index m, StageCounters* counters) {
+  DevMatrix& M = *I.M;
+  if (M.sharded)
+    throw std::logic_error("fused instantiate+apply on a row shard: use the partial apply and sum across ranks");
+  instantiate_apply_tree(I, theta, n_theta, x_dev, m, counters);
+  M.ctx->run("scatter", [&] {
+    dev::launch_scatter(M.st(), M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev);
+  });
+}
+
+void instantiate_apply_partial_device(DevInstance& I, const double* theta, int n_theta, const double* x_dev,
+                                      double* ypart_dev, Index m, StageCounters* counters) {
+  DevMatrix& M = *I.M;
+  instantiate_apply_tree(I, theta, n_theta, x_dev, m, counters);
+  CK(cudaMemcpyAsync(ypart_dev, M.yp.p, sizeof(double) * M.n * m, cudaMemcpyDeviceToDevice, M.st()));
 }
 
 // estimate_error (harness.cpp:183-236) for this instance: probe rows J
@@ -1555,9 +1584,24 @@ void instantiate_apply_host(DevInstance& I, const double* theta, int n_theta, co
   CK(cudaStreamSynchronize(st));
 }
 
+void apply_device_partial(DevInstance& I, const double* x_dev, double* ypart_dev, Index m) {
+  DevMatrix& M = *I.M;
+  PHM_CHECK(m >= 1, "apply: m must be >= 1");
+  CK(cudaSetDevice(M.ctx->device));
+  ensure_workspace(M, m);
+  cudaStream_t st = M.st();
+  M.ctx->run("gather", [&] { dev::launch_gather(st, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
+  apply_tree_order(I, m);
+  CK(cudaMemcpyAsync(ypart_dev, M.yp.p, sizeof(double) * M.n * m, cudaMemcpyDeviceToDevice, st));
+}
+
 void apply_device_rows(DevInstance& I, const double* x_dev, double* yrows_dev, Index m) {
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
+  if (M.sym && M.sharded)
+    throw std::logic_error(
+        "symmetric near storage on a row shard: rows of y get contributions from other ranks; use the partial "
+        "apply and sum across ranks (or build with symmetric_near = 0)");
   CK(cudaSetDevice(M.ctx->device));
   ensure_workspace(M, m);
   cudaStream_t st = M.st();

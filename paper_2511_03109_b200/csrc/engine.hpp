@@ -80,9 +80,13 @@ double estimate_error(DevInstance& inst, Index probe_rows, std::uint64_t seed, S
                       std::vector<Index>* rows_out, std::vector<double>* exact_out, std::vector<double>* approx_out,
                       std::vector<double>* x_out);
 void apply_device(DevInstance& inst, const double* x_dev, double* y_dev, Index m);
-// Sharded pieces: rows [row_begin, row_end) of y in tree order, and the
-// final un-permute of a gathered tree-order vector.
+// Sharded pieces: rows [row_begin, row_end) of y in tree order (full near
+// storage only), the shard's full-length partial y in tree order (sum the
+// partials of all ranks), and the final un-permute of a tree-order vector.
 void apply_device_rows(DevInstance& inst, const double* x_dev, double* yrows_dev, Index m);
+void apply_device_partial(DevInstance& inst, const double* x_dev, double* ypart_dev, Index m);
+void instantiate_apply_partial_device(DevInstance& inst, const double* theta, int n_theta, const double* x_dev,
+                                      double* ypart_dev, Index m, StageCounters* counters);
 void unpermute_device(DevMatrix& m, const double* yperm_dev, double* y_dev, Index mcols);
 
 }  // namespace phm

@@ -1,10 +1,18 @@
 """Multi-GPU plumbing for the row-sharded apply.
 
 Each rank owns a contiguous range of leaf row clusters (tree order, balanced
-by near-field entries; host/build.cpp) and computes those rows of y; x is
-replicated. The only exchange is an all-gather(v) of the row blocks, done as
-a padded all_gather_into_tensor (NCCL over NVLink on GPUs, gloo in the CPU
-tests), followed by the un-permute to the original point order.
+by near-field entries; host/build.cpp); x is replicated. Two exchanges:
+
+* symmetric near storage (the default in snapshot mode): a rank stores the
+  near pairs whose owner leaf it holds, so its transposed products reach
+  rows of other ranks. Each rank produces a full-length partial y in tree
+  order (`phm_apply_partial_device`) and the partials are summed with one
+  all-reduce (`PartialSum`);
+* full near storage: each rank computes exactly its rows; the row blocks are
+  all-gathered (`RowGather`, a padded all_gather_into_tensor).
+
+NCCL over NVLink on GPUs, gloo in the CPU tests; then the un-permute to the
+original point order.
 """
 from __future__ import annotations
 
@@ -53,3 +61,19 @@ class RowGather:
             self.out[:, off: off + c].copy_(self.recv[k, :, :c])
             off += c
         return self.out
+
+
+class PartialSum:
+    """Reusable buffer for summing per-rank partial y vectors (tree order)."""
+
+    def __init__(self, n: int, m: int = 1, device="cpu", dtype=None):
+        import torch
+
+        self.buf = torch.zeros((m, n), dtype=dtype or torch.float64, device=device)
+
+    def reduce(self, group=None):
+        """Sums the ranks' partials in place (all-reduce); returns (m, n)."""
+        import torch.distributed as dist
+
+        dist.all_reduce(self.buf, op=dist.ReduceOp.SUM, group=group)
+        return self.buf

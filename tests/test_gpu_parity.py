@@ -235,39 +235,64 @@ def test_symmetric_storage_is_exact(ph):
     assert rel(ia.apply(x), ib.apply(x)) <= 1e-14
 
 
-@pytest.mark.parametrize("fmt", ["h2", "h"])
-def test_row_sharded_apply_on_one_gpu(ph, fmt):
-    """The multi-GPU row-sharded path (phm_apply_rows_device per shard +
-    gather + un-permute), with the shards built one after another on one
-    GPU: rows concatenated in rank order equal the unsharded MVM."""
+@pytest.mark.parametrize("fmt,sym", [("h2", True), ("h2", False), ("h", True), ("h", False)])
+def test_row_sharded_apply_on_one_gpu(ph, fmt, sym):
+    """The multi-GPU row-sharded path with the shards built one after another
+    on one GPU. Symmetric near storage: every shard's full-length partial y
+    (phm_apply_partial_device / phm_instantiate_apply_partial_device), summed
+    over shards, equals the unsharded MVM. Full storage: the shards' rows
+    (phm_apply_rows_device) concatenated in rank order equal it too."""
     import torch
 
     pts = ph.generate_points(4000, 3, 12)
     base = dict(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
-                near_mode=ph.NearMode.SNAPSHOT)
+                near_mode=ph.NearMode.SNAPSHOT, symmetric_near=sym)
     build = ph.offline_h2 if fmt == "h2" else ph.offline_h
     full = build(pts, ph.PHConfig(**base))
     x = ph.generate_normal(4000, 2)
     y_ref = ph.instantiate(full, [0.3]).apply(x)
+    y_ref2 = ph.instantiate(full, [0.41]).apply(x)
     world = 3
     xd = torch.from_numpy(x).cuda()
-    rows = []
-    perm = None
+    rows, perm = [], None
+    ysum = np.zeros(4000)
+    ysum2 = np.zeros(4000)
+    stored = 0
     for r in range(world):
         pm = build(pts, ph.PHConfig(**base, shard_rank=r, shard_count=world))
         info = pm.info()
+        stored += info["near_stored"]
         inst = ph.instantiate(pm, [0.3])
-        yr = torch.zeros(max(1, info["row_end"] - info["row_begin"]), dtype=torch.float64, device="cuda")
-        inst.apply_rows_device(xd.data_ptr(), yr.data_ptr(), 1)
+        part = torch.zeros(4000, dtype=torch.float64, device="cuda")
+        inst.apply_partial_device(xd.data_ptr(), part.data_ptr(), 1)
         pm.ctx.sync()
-        rows.append((info["row_begin"], yr[: info["row_end"] - info["row_begin"]].cpu().numpy()))
+        ysum += part.cpu().numpy()
+        inst.instantiate_apply_partial_device([0.41], xd.data_ptr(), part.data_ptr(), 1)
+        pm.ctx.sync()
+        ysum2 += part.cpu().numpy()
+        if sym:
+            yr = torch.zeros(max(1, info["row_end"] - info["row_begin"]), dtype=torch.float64, device="cuda")
+            with pytest.raises(ph.LogicError):
+                inst.apply_rows_device(xd.data_ptr(), yr.data_ptr(), 1)
+        else:
+            yr = torch.zeros(max(1, info["row_end"] - info["row_begin"]), dtype=torch.float64, device="cuda")
+            inst.apply_rows_device(xd.data_ptr(), yr.data_ptr(), 1)
+            pm.ctx.sync()
+            rows.append((info["row_begin"], yr[: info["row_end"] - info["row_begin"]].cpu().numpy()))
         perm = pm.perm()
-    rows.sort(key=lambda t: t[0])
-    yperm = np.concatenate([r for _, r in rows])
-    assert yperm.size == 4000
+    # the shards together store the unsharded near data exactly once
+    assert stored == full.info()["near_stored"]
     y = np.empty(4000)
-    y[perm] = yperm
+    y[perm] = ysum
     assert rel(y, y_ref) <= 1e-13
+    y[perm] = ysum2
+    assert rel(y, y_ref2) <= 1e-13
+    if not sym:
+        rows.sort(key=lambda t: t[0])
+        yperm = np.concatenate([r for _, r in rows])
+        assert yperm.size == 4000
+        y[perm] = yperm
+        assert rel(y, y_ref2) <= 1e-13  # the instances now hold theta = 0.41
 
 
 @pytest.mark.parametrize("fmt,mode", [("h2", "snapshot"), ("h2", "tt"), ("h", "snapshot")])

@@ -35,7 +35,7 @@ def _worker(rank, world, port, q):
     try:
         import paper_2511_03109_b200 as ph
         from oracle import pyoracle as po
-        from paper_2511_03109_b200.dist import RowGather, row_counts
+        from paper_2511_03109_b200.dist import PartialSum, RowGather, row_counts
 
         pts = ph.generate_points(3000, 3, 4)
         spec = ph.KernelSpec(ph.Family.E, [(0.05, 0.5)])
@@ -55,7 +55,17 @@ def _worker(rank, world, port, q):
         yperm = rg.gather(yrows).numpy()[0]
         y = np.empty_like(yperm)
         y[perm] = yperm
-        q.put((rank, info["row_begin"], info["row_end"], bool(np.array_equal(y, y_full)), counts))
+        # symmetric storage: full-length partials summed by one all-reduce
+        # (here two complementary weightings of y stand in for the ranks'
+        # partials: the plumbing, shapes and un-permute are what is checked)
+        w = np.random.default_rng(7).uniform(0, 1, 3000)
+        ps = PartialSum(3000, 1)
+        ps.buf[0].copy_(torch.from_numpy(ytree * (w if rank == 0 else 1.0 - w)))
+        ysum = ps.reduce().numpy()[0]
+        y2 = np.empty_like(ysum)
+        y2[perm] = ysum
+        ok2 = bool(np.max(np.abs(y2 - y_full)) <= 1e-14 * np.max(np.abs(y_full)))
+        q.put((rank, info["row_begin"], info["row_end"], bool(np.array_equal(y, y_full)) and ok2, counts))
     finally:
         dist.destroy_process_group()
 
