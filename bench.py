@@ -41,7 +41,7 @@ CONFIGS = {
     # BASELINE.json configs[4] (C5): the C3 matrix, 4096 thetas sharded over
     # GPUs with no communication, each instantiated and applied to 10 vectors
     "c5": dict(n=262144, d=3, family="e", box=(0.05, 0.5), l_max=4, p_s=4, p_theta=8, eta=1.0, fmt="h2",
-               points="uniform", sweep=True, rhs=10, n_theta=4096),
+               points="uniform", sweep=True, rhs=10, n_theta=4096, theta_batch=8),
 }
 
 
@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=16, help="1/f of near/far blocks timed on the CPU")
     ap.add_argument("--rhs", type=int, default=0, help="right-hand sides per MVM (default: the config's)")
+    ap.add_argument("--theta-batch", type=int, default=0,
+                    help="sweeps: thetas instantiated per snapshot pass (default: the config's; 1 = one at a time)")
     return ap.parse_args()
 
 
@@ -264,11 +266,19 @@ def run_ours(args):
 
         psum = PartialSum(n, 1, device="cuda")
     inst = ph.instantiate(pm, [thetas[0]])
+    # sweeps: tb thetas per step, instantiated by one snapshot pass (K1 batch)
+    tb = (args.theta_batch or c.get("theta_batch", 1)) if sweep else 1
+    binsts = ph.instantiate_batch(pm, [[thetas[b]] for b in range(tb)]) if tb > 1 else None
 
     def theta_of(s):
         return thetas[(s * world + rank) % len(thetas)] if sweep else thetas[s % len(thetas)]
 
     def step(s):
+        if binsts is not None:
+            ph.reinstantiate_batch(binsts, [[theta_of(s * tb + b)] for b in range(tb)])
+            for b in range(tb):
+                binsts[b].apply_device(x_dev.data_ptr(), y_dev.data_ptr(), m)
+            return
         if not row_shard:
             # instantiate(theta_s) + MVM as one overlapped schedule
             inst.instantiate_apply_device([theta_of(s)], x_dev.data_ptr(), y_dev.data_ptr(), m)
@@ -356,6 +366,12 @@ def run_ours(args):
         from ctypes import POINTER, c_double
 
         def e2e_step(s):
+            if binsts is not None:
+                ph.reinstantiate_batch(binsts, [[theta_of(s * tb + b)] for b in range(tb)])
+                for b in range(tb):
+                    ph._check(ph.lib().phm_apply(binsts[b]._h, xh.ctypes.data_as(POINTER(c_double)), n,
+                                                 yh.ctypes.data_as(POINTER(c_double)), m))
+                return
             if row_shard:
                 # host x -> every rank, sharded step + all-reduce, y -> host
                 x_dev.copy_(x_host, non_blocking=True)
@@ -382,8 +398,8 @@ def run_ours(args):
             t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        e2e = {"value": (world if sweep else 1) * args.steps * 1000.0 / e_ms, "unit": "theta/s",
-               "h2d_bytes_per_step": 8 * n * m + 8, "d2h_bytes_per_step": 8 * n * m}
+        e2e = {"value": (world if sweep else 1) * tb * args.steps * 1000.0 / e_ms, "unit": "theta/s",
+               "h2d_bytes_per_step": tb * (8 * n * m + 8), "d2h_bytes_per_step": tb * 8 * n * m}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and c["fmt"] == "h2" and m == 1:
@@ -403,6 +419,10 @@ def run_ours(args):
         k1_avg = k1_ms / max(1, k1_n)
         traffic = measured_traffic(k1_desc.split()[0], args.config, world)
         k1_bytes = 8 * info["near_stream_elems"]  # R slab reads + 1 write per stored near entry
+        if binsts is not None:  # batched K1: R slab reads + one write per theta of the batch
+            k1_desc = "k_inst_flat_batch (K1 for %d thetas per snapshot pass)" % min(tb, 16)
+            r_snap = round(info["near_stream_elems"] / max(1, info["near_stored"])) - 1
+            k1_bytes = 8 * info["near_stored"] * (r_snap + min(tb, 16))
         achieved = k1_bytes / (k1_avg * 1e-3) / 1e9
         mvm_ms = apply_ms
         # the near-field GEMV kernel of apply alone: reads every stored entry once
@@ -429,12 +449,13 @@ def run_ours(args):
                 "theta/s (instantiate + %d-RHS %s MVM per theta) at %s" % (m, fmt_name, where))
         line = {
             "metric": what,
-            "value": (world if sweep else 1) * args.steps * 1000.0 / ms,
+            "value": (world if sweep else 1) * tb * args.steps * 1000.0 / ms,
             "unit": "theta/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": ms / args.steps,
+            "thetas_per_step": tb,
             "higher_is_better": True,
             "scaling": "weak" if sweep else "strong",
             "vs_baseline": None,
@@ -442,7 +463,7 @@ def run_ours(args):
             "data": "synthetic (seeded uniform points, harness theta draws, x~N(0,1))",
             "config": {"workload": f"{args.config}: n={n} d={c['d']} {c['fmt']} kernel={c['family']} "
                                    f"l_max={c['l_max']} p_s={c['p_s']} p_theta={c['p_theta']} eta={c['eta']} "
-                                   f"near=snapshot rhs={m}",
+                                   f"near=snapshot rhs={m}" + (f" theta_batch={tb}" if tb > 1 else ""),
                        "parallelism": ("theta-sharded replicas" if sweep else f"rows sharded over {world}"),
                        "l2": "inputs (near snapshots) larger than L2; no flush needed"},
             "roofline": {"bound": "hbm", "kernel": k1_desc, "achieved": achieved,

@@ -174,6 +174,15 @@ int phm_parametric_vectors(phm_matrix m, const double* theta, int n_theta, doubl
 /* Online stage. */
 int phm_instantiate(phm_matrix m, const double* theta, int n_theta, phm_instance* out);
 int phm_reinstantiate(phm_instance inst, const double* theta, int n_theta);
+/* theta-batched instantiate for sweeps: count thetas
+ * (count x n_theta, row-major) -> count instances in out[]. Snapshot mode
+ * reads the snapshots once for the whole batch (K1 batch kernel); every D is
+ * bit-identical to phm_instantiate's. Each instance is destroyed with
+ * phm_instance_destroy. Replaces a loop of instantiate(pm, theta) calls
+ * (harness.cpp:293-312 per theta). */
+int phm_instantiate_batch(phm_matrix m, const double* thetas, int n_theta, int count, phm_instance* out);
+/* In place: instances of one matrix re-instantiated at count thetas. */
+int phm_reinstantiate_batch(phm_instance* insts, int count, const double* thetas, int n_theta);
 int phm_instance_destroy(phm_instance inst);
 int phm_instance_sync(phm_instance inst);
 int phm_instance_far_h(phm_instance inst, int64_t far_index, double* out, int64_t* rows, int64_t* cols);

@@ -26,7 +26,7 @@ __all__ = [
     "PHConfig", "KernelSpec", "Family", "Format", "NearMode",
     "Context", "ParametricMatrix", "InstantiatedMatrix",
     "offline_h", "offline_h2", "offline_structure", "instantiate", "metrics",
-    "generate_points", "generate_mixture_points", "generate_normal",
+    "generate_points", "generate_mixture_points", "generate_normal", "instantiate_batch", "reinstantiate_batch",
     "PhmatError", "DomainError", "InvalidArgument", "LogicError", "CudaError",
     "library_path", "lib",
 ]
@@ -126,6 +126,8 @@ SIGNATURES = {
     "phm_parametric_vectors": ([_P, _DP, C.c_int, _DP], C.c_int),
     "phm_instantiate": ([_P, _DP, C.c_int, C.POINTER(_P)], C.c_int),
     "phm_reinstantiate": ([_P, _DP, C.c_int], C.c_int),
+    "phm_instantiate_batch": ([_P, _DP, C.c_int, C.c_int, _P], C.c_int),
+    "phm_reinstantiate_batch": ([_P, C.c_int, _DP, C.c_int], C.c_int),
     "phm_instance_destroy": ([_P], C.c_int),
     "phm_instance_sync": ([_P], C.c_int),
     "phm_instance_far_h": ([_P, C.c_int64, _DP, _I64P, _I64P], C.c_int),
@@ -640,6 +642,26 @@ def instantiate(pm: ParametricMatrix, theta) -> InstantiatedMatrix:
     h = _P()
     _check(lib().phm_instantiate(pm._h, _dp(th), th.size, C.byref(h)))
     return InstantiatedMatrix(pm, h, th)
+
+
+def instantiate_batch(pm: ParametricMatrix, thetas) -> List[InstantiatedMatrix]:
+    """theta-batched instantiate for sweeps: thetas (count, d_theta) -> count
+    instances; in snapshot mode the snapshots are read once for the batch.
+    Equal, bit for bit, to [instantiate(pm, t) for t in thetas]."""
+    th = np.ascontiguousarray(_f64(thetas).reshape(len(thetas), -1))
+    count, dt = th.shape
+    hs = (_P * count)()
+    _check(lib().phm_instantiate_batch(pm._h, _dp(th), dt, count, C.cast(hs, _P)))
+    return [InstantiatedMatrix(pm, _P(hs[b]), th[b]) for b in range(count)]
+
+
+def reinstantiate_batch(insts: Sequence[InstantiatedMatrix], thetas) -> None:
+    """In place: insts[b] re-instantiated at thetas[b], one snapshot pass."""
+    th = np.ascontiguousarray(_f64(thetas).reshape(len(insts), -1))
+    hs = (_P * len(insts))(*[i._h for i in insts])
+    _check(lib().phm_reinstantiate_batch(C.cast(hs, _P), len(insts), _dp(th), th.shape[1]))
+    for b, i in enumerate(insts):
+        i.theta = list(th[b])
 
 
 def metrics(pm: ParametricMatrix) -> dict:

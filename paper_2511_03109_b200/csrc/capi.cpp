@@ -562,6 +562,36 @@ int phm_instantiate(phm_matrix m, const double* theta, int n_theta, phm_instance
     *out = I.release();
   });
 }
+int phm_instantiate_batch(phm_matrix m, const double* thetas, int n_theta, int count, phm_instance* out) {
+  return guarded([&] {
+    need(m, "matrix");
+    need(thetas, "thetas");
+    need(out, "out");
+    auto& H = const_cast<phm::HostMatrix&>(phm::matrix_host(*m->m));
+    auto insts = phm::instantiate_batch(m->m, thetas, n_theta, count, &H.counters);
+    for (int b = 0; b < count; ++b) {
+      auto I = std::make_unique<phm_instance_s>();
+      I->m = m->m;
+      I->inst = insts[b];
+      out[b] = I.release();
+    }
+  });
+}
+int phm_reinstantiate_batch(phm_instance* insts, int count, const double* thetas, int n_theta) {
+  return guarded([&] {
+    need(insts, "instances");
+    need(thetas, "thetas");
+    PHM_CHECK(count >= 1, "reinstantiate_batch: count must be >= 1");
+    std::vector<phm::DevInstance*> raw;
+    for (int b = 0; b < count; ++b) {
+      need(insts[b], "instance");
+      PHM_CHECK(insts[b]->m == insts[0]->m, "reinstantiate_batch: instances of different matrices");
+      raw.push_back(insts[b]->inst.get());
+    }
+    auto& H = const_cast<phm::HostMatrix&>(phm::matrix_host(*insts[0]->m));
+    phm::reinstantiate_batch(raw, thetas, n_theta, &H.counters);
+  });
+}
 int phm_reinstantiate(phm_instance inst, const double* theta, int n_theta) {
   return guarded([&] {
     need(inst, "instance");

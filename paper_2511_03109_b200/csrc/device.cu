@@ -29,6 +29,7 @@ namespace dev {
 void launch_snapshot(cudaStream_t, const SnapTile*, std::int64_t, const BlockGeom*, const double*, std::int64_t, int,
                      int, int, const double*, double, double*);
 void launch_inst_flat(cudaStream_t, const double*, std::int64_t, int, const double*, double*);
+bool launch_inst_flat_batch(cudaStream_t, const double*, std::int64_t, int, int, const double* const*, double* const*);
 void launch_inst_tiles(cudaStream_t, const InstTile*, std::int64_t, const double*, const double*, double*);
 void launch_near_w(cudaStream_t, const NearW*, std::int64_t, const double*, const std::int32_t*, const ThetaV&,
                    double*);
@@ -289,6 +290,7 @@ struct DevMatrix {
   DBuf sym_items, sym_blocks, g_row0, g_rows, g_sbeg, g_segs, sym_part;
   int n_sym_items = 0, n_gather_leaves = 0;
   bool near_tma = false;  // every item spans its whole leaf: TMA near pass
+  DBuf batch_tab;         // K1 batch: w and D pointer tables
   DBuf work_ctr;          // persistent near kernels' item counter
   // K9 multi-RHS near field (DMMA), CSR by sigma over stored blocks
   DBuf k9_items, k9_tb, k9_tn, k9_doff, k9_ld, k9_tr;
@@ -1162,12 +1164,8 @@ void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCoun
 
 }  // namespace
 
-std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const double* theta, int n_theta,
-                                         StageCounters* counters) {
-  if (!m->ctx) throw std::logic_error("instantiate: host-only matrix (built without a device)");
-  CK(cudaSetDevice(m->ctx->device));
-  // validate theta first so nothing is allocated for a bad call
-  (void)parametric_vectors(m->hm->grids, theta, n_theta);
+namespace {
+std::shared_ptr<DevInstance> alloc_instance(const std::shared_ptr<DevMatrix>& m) {
   auto I = std::make_shared<DevInstance>();
   I->M = m;
   {
@@ -1185,8 +1183,88 @@ std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const dou
   if (m->C_len) I->C.alloc(static_cast<size_t>(m->C_len) * sizeof(double));
   const std::int64_t wl = m->mode == NearMode::Snapshot ? m->R_snap : m->w_len;
   if (wl) I->w.alloc(static_cast<size_t>(wl) * sizeof(double));
+  return I;
+}
+
+// instantiate for B thetas at once: the class stage per theta, then (snapshot
+// mode) one K1 pass that reads the snapshots once and writes all B D's.
+void run_instantiate_batch(const std::vector<DevInstance*>& insts, const double* thetas, int n_theta,
+                           StageCounters* counters) {
+  DevMatrix& M = *insts[0]->M;
+  const HostMatrix& H = *M.hm;
+  CK(cudaSetDevice(M.ctx->device));
+  const int B = static_cast<int>(insts.size());
+  std::vector<std::vector<std::vector<double>>> vs(B);
+  for (int b = 0; b < B; ++b) vs[b] = parametric_vectors(H.grids, thetas + b * n_theta, n_theta);  // all checked first
+  cudaStream_t st = M.ctx->stream;
+  std::vector<dev::ThetaV> tvs(B);
+  for (int b = 0; b < B; ++b) {
+    insts[b]->theta.assign(thetas + b * n_theta, thetas + (b + 1) * n_theta);
+    tvs[b] = make_theta_v(vs[b]);
+    inst_classes(*insts[b], tvs[b], st);
+  }
+  if (M.mode != NearMode::Snapshot) {
+    for (int b = 0; b < B; ++b) inst_near(*insts[b], thetas + b * n_theta, vs[b], tvs[b], st, counters);
+    return;
+  }
+  for (int b = 0; b < B; ++b) inst_snapshot_w(*insts[b], vs[b], tvs[b], st);
+  constexpr int kMax = 16;  // dev::kInstBatchMax
+  if (!M.batch_tab.p) M.batch_tab.alloc(2 * kMax * sizeof(void*));
+  for (int b0 = 0; b0 < B; b0 += kMax) {
+    const int nb = std::min(kMax, B - b0);
+    std::vector<const void*> tab(2 * kMax, nullptr);
+    for (int b = 0; b < nb; ++b) {
+      tab[b] = insts[b0 + b]->w.p;
+      tab[kMax + b] = insts[b0 + b]->D.p;
+    }
+    CK(cudaMemcpyAsync(M.batch_tab.p, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice, st));
+    bool ok = false;
+    M.ctx->run_on(st, "near_inst", [&] {
+      ok = dev::launch_inst_flat_batch(st, M.G.as<double>(), M.E, M.R_snap, nb, M.batch_tab.as<const double*>(),
+                                       M.batch_tab.as<double*>() + kMax);
+    });
+    if (!ok)
+      for (int b = 0; b < nb; ++b)
+        M.ctx->run_on(st, "near_inst", [&] {
+          dev::launch_inst_flat(st, M.G.as<double>(), M.E, M.R_snap, insts[b0 + b]->w.as<double>(),
+                                insts[b0 + b]->D.as<double>());
+        });
+  }
+}
+}  // namespace
+
+std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const double* theta, int n_theta,
+                                         StageCounters* counters) {
+  if (!m->ctx) throw std::logic_error("instantiate: host-only matrix (built without a device)");
+  CK(cudaSetDevice(m->ctx->device));
+  // validate theta first so nothing is allocated for a bad call
+  (void)parametric_vectors(m->hm->grids, theta, n_theta);
+  auto I = alloc_instance(m);
   run_instantiate(*I, theta, n_theta, counters);
   return I;
+}
+
+std::vector<std::shared_ptr<DevInstance>> instantiate_batch(std::shared_ptr<DevMatrix> m, const double* thetas,
+                                                            int n_theta, int count, StageCounters* counters) {
+  if (!m->ctx) throw std::logic_error("instantiate: host-only matrix (built without a device)");
+  PHM_CHECK(count >= 1, "instantiate_batch: count must be >= 1");
+  CK(cudaSetDevice(m->ctx->device));
+  for (int b = 0; b < count; ++b) (void)parametric_vectors(m->hm->grids, thetas + b * n_theta, n_theta);
+  std::vector<std::shared_ptr<DevInstance>> out;
+  std::vector<DevInstance*> raw;
+  for (int b = 0; b < count; ++b) {
+    out.push_back(alloc_instance(m));
+    raw.push_back(out.back().get());
+  }
+  run_instantiate_batch(raw, thetas, n_theta, counters);
+  return out;
+}
+
+void reinstantiate_batch(const std::vector<DevInstance*>& insts, const double* thetas, int n_theta,
+                         StageCounters* counters) {
+  PHM_CHECK(!insts.empty(), "reinstantiate_batch: no instances");
+  for (DevInstance* I : insts) PHM_CHECK(I->M == insts[0]->M, "reinstantiate_batch: instances of different matrices");
+  run_instantiate_batch(insts, thetas, n_theta, counters);
 }
 
 void reinstantiate(DevInstance& inst, const double* theta, int n_theta, StageCounters* counters) {

@@ -55,6 +55,13 @@ std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const dou
                                          StageCounters* counters);
 // Re-instantiate in place at a new theta (reuses the device buffers).
 void reinstantiate(DevInstance& inst, const double* theta, int n_theta, StageCounters* counters);
+// theta-batched instantiate (sweeps): count thetas (count x n_theta,
+// row-major); in snapshot mode one K1 pass reads the snapshots once and
+// writes every instance's D (bit-identical to single instantiates).
+std::vector<std::shared_ptr<DevInstance>> instantiate_batch(std::shared_ptr<DevMatrix> m, const double* thetas,
+                                                            int n_theta, int count, StageCounters* counters);
+void reinstantiate_batch(const std::vector<DevInstance*>& insts, const double* thetas, int n_theta,
+                         StageCounters* counters);
 const std::vector<double>& instance_theta(const DevInstance& inst);
 void instance_sync(DevInstance& inst);
 

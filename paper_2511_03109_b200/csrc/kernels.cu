@@ -149,6 +149,41 @@ __global__ void __launch_bounds__(256, 1) k_inst_flat(const double* __restrict__
   }
 }
 
+// K1 for a batch of B thetas (sweeps): the R snapshot slabs are read once
+// and B instances are written, D_b[e] = sum_k w_b,k S[k E + e] with the same
+// FMA order as k_inst_flat (each D_b is bit-identical to a single
+// instantiate). Bytes per stored entry: 8 (R + B) instead of 8 B (R + 1).
+constexpr int kInstBatchMax = 16;
+template <int R>
+__global__ void __launch_bounds__(256, 1) k_inst_flat_batch(const double* __restrict__ G, std::int64_t E, int B,
+                                                         const double* const* __restrict__ wptr,
+                                                         double* const* __restrict__ dptr) {
+  __shared__ double W[kInstBatchMax][R];
+  __shared__ double* Dp[kInstBatchMax];
+  for (int i = threadIdx.x; i < B * R; i += blockDim.x) W[i / R][i % R] = wptr[i / R][i % R];
+  if (threadIdx.x < B) Dp[threadIdx.x] = dptr[threadIdx.x];
+  __syncthreads();
+  const std::int64_t E4 = E >> 2;
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t q = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < E4; q += stride) {
+    dbl4 v[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) v[k] = ld_stream4(G + 4 * (E4 * k + q));
+    for (int b = 0; b < B; ++b) {
+      dbl4 acc = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const double wk = W[b][k];
+        acc.x += v[k].x * wk;
+        acc.y += v[k].y * wk;
+        acc.z += v[k].z * wk;
+        acc.w += v[k].w * wk;
+      }
+      st4(Dp[b] + 4 * q, acc);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_inst_flat_any(const double* __restrict__ G, std::int64_t E, int R,
                                                        const double* __restrict__ w, double* __restrict__ D) {
   const std::int64_t E4 = E >> 2;
@@ -1675,6 +1710,30 @@ void launch_snapshot(cudaStream_t st, const SnapTile* tiles, std::int64_t ntiles
   if (grid > 0) k_snapshot<<<grid, 256, 0, st>>>(tiles, ntiles, geo, pts, n, d, fam, R, theta_nodes, amp, out);
 }
 
+bool launch_inst_flat_batch(cudaStream_t st, const double* G, std::int64_t E, int R, int B, const double* const* wptr,
+                            double* const* dptr) {
+  if (B < 1 || B > kInstBatchMax) return false;
+  static const int per_sm = [] {
+    const char* e = std::getenv("PHM_K1_CTAS");
+    const int k = e ? std::atoi(e) : 4;
+    return k >= 1 && k <= 8 ? k : 4;
+  }();
+  const std::int64_t E4 = E >> 2;
+  const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((E4 + 255) / 256, 148 * per_sm)));
+  switch (R) {
+    case 1: k_inst_flat_batch<1><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
+    case 2: k_inst_flat_batch<2><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
+    case 3: k_inst_flat_batch<3><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
+    case 4: k_inst_flat_batch<4><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
+    case 5: k_inst_flat_batch<5><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
+    case 6: k_inst_flat_batch<6><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
+    case 8: k_inst_flat_batch<8><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
+    case 10: k_inst_flat_batch<10><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
+    case 12: k_inst_flat_batch<12><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
+    case 16: k_inst_flat_batch<16><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
+    default: return false;
+  }
+}
 void launch_inst_flat(cudaStream_t st, const double* G, std::int64_t E, int R, const double* w, double* D) {
   const std::int64_t E4 = E / 4;
   if (E4 == 0) return;

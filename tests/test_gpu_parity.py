@@ -425,3 +425,31 @@ def test_fused_near_pass_across_snapshot_ranks(ph, po, p_theta):
         for k in range(0, len(near), 11):
             sh = (sizes[near[k][0]], sizes[near[k][1]])
             assert np.array_equal(inst.near_d(k, sh), ref.near_d(k, sh))
+
+
+@pytest.mark.parametrize("mode", ["snapshot", "tt"])
+def test_theta_batched_instantiate(ph, po, mode):
+    """instantiate_batch (one snapshot pass for the whole batch) equals a loop
+    of single instantiates bit for bit; batches above 16 thetas are split;
+    a theta outside the box fails the whole call before any launch."""
+    pts = ph.generate_points(2000, 3, 27)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT if mode == "snapshot" else ph.NearMode.TT)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    thetas = np.linspace(0.05, 0.5, 18).reshape(-1, 1)
+    insts = ph.instantiate_batch(pm, thetas)
+    assert len(insts) == 18
+    near, _, _ = pm.blocks()
+    sizes = _node_sizes(pm)
+    x = ph.generate_normal(2000, 3)
+    for b in (0, 7, 15, 16, 17):
+        ref = ph.instantiate(pm, thetas[b])
+        for k in range(0, len(near), 13):
+            sh = (sizes[near[k][0]], sizes[near[k][1]])
+            assert np.array_equal(insts[b].near_d(k, sh), ref.near_d(k, sh))
+        assert np.array_equal(insts[b].apply(x), ref.apply(x))
+    assert rel(insts[5].apply(x), om.instantiate(thetas[5]).apply(x)) <= TOL_Y
+    ph.reinstantiate_batch(insts[:3], [[0.3], [0.2], [0.1]])
+    assert np.array_equal(insts[1].apply(x), ph.instantiate(pm, [0.2]).apply(x))
+    with pytest.raises(ph.DomainError):
+        ph.instantiate_batch(pm, [[0.2], [0.9]])
