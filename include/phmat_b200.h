@@ -174,6 +174,36 @@ int phm_parametric_vectors(phm_matrix m, const double* theta, int n_theta, doubl
 /* Online stage. */
 int phm_instantiate(phm_matrix m, const double* theta, int n_theta, phm_instance* out);
 int phm_reinstantiate(phm_instance inst, const double* theta, int n_theta);
+/* Non-parametric baselines at one fixed theta (proj/include/phmat/baselines.hpp):
+ * PHM_BASELINE_H_ACA = HAcaMatrix (baselines.hpp:27-50: ACA far blocks,
+ * dense near blocks), PHM_BASELINE_H2_HCA = H2HcaMatrix (:52-82: ACA of the
+ * Chebyshev node-interaction matrices per translation class, nested basis
+ * shared with the parametric build). Factorisation on the host (the
+ * reference's aca_engine, aca_impl.hpp:34-173), near blocks evaluated on the
+ * GPU; the returned instance applies through phm_apply / phm_to_dense like a
+ * parametric one (LinearOperator, harness.cpp:314-336). The config supplies
+ * the kernel, tree depth, eta and p_s (H^2-HCA); eps and r_max are the ACA's.
+ * phm_instantiate / phm_reinstantiate reject baseline instances. */
+enum { PHM_BASELINE_H_ACA = 1, PHM_BASELINE_H2_HCA = 2 };
+typedef struct phm_baseline_info {
+  int32_t method;
+  int32_t any_capped;      /* some ACA hit r_max */
+  double mean_far_rank;    /* HAcaMatrix::mean_far_rank / H2HcaMatrix::mean_far_rank */
+  double coupling_ratio;   /* H2HcaMatrix::coupling_ratio, (2/n^2) sum_b p_s^d t_b; 0 for H-ACA */
+  double far_build_s;      /* host ACA time (far_build_seconds) */
+  double near_build_s;     /* device near evaluation time (near_build_seconds) */
+  uint64_t far_evals;      /* kernel evaluations of the ACAs */
+  uint64_t near_evals;     /* dense near entries evaluated */
+  int64_t n_far, n_near, n_classes;
+} phm_baseline_info;
+int phm_baseline_build(phm_context ctx, const double* points, int64_t n, int d, const phm_config* cfg, int method,
+                       const double* theta, int n_theta, double eps, int64_t r_max, phm_instance* out);
+int phm_baseline_info_get(phm_instance inst, phm_baseline_info* out);
+/* aca_partial (baselines.hpp:22-24) on a dense m x n column-major matrix:
+ * A ~ V Y^T, V m x rank, Y n x rank (buffers of min(m, n, r_max) columns). */
+int phm_aca_partial_dense(const double* a, int64_t m, int64_t n, double eps, int64_t r_max, uint64_t seed,
+                          int64_t* rank, int32_t* capped, double* v, double* y);
+
 /* theta-batched instantiate for sweeps: count thetas
  * (count x n_theta, row-major) -> count instances in out[]. Snapshot mode
  * reads the snapshots once for the whole batch (K1 batch kernel); every D is

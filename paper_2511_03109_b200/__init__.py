@@ -27,6 +27,7 @@ __all__ = [
     "Context", "ParametricMatrix", "InstantiatedMatrix",
     "offline_h", "offline_h2", "offline_structure", "instantiate", "metrics",
     "generate_points", "generate_mixture_points", "generate_normal", "instantiate_batch", "reinstantiate_batch",
+    "h_aca", "h2_hca", "aca_partial", "Baseline", "BaselineMatrix",
     "PhmatError", "DomainError", "InvalidArgument", "LogicError", "CudaError",
     "library_path", "lib",
 ]
@@ -83,6 +84,13 @@ class _Info(C.Structure):
         ("any_rank_capped", C.c_int32), ("pad", C.c_int32)]
 
 
+class _BaselineInfo(C.Structure):
+    _fields_ = [("method", C.c_int32), ("any_capped", C.c_int32)] + [
+        (k, C.c_double) for k in ("mean_far_rank", "coupling_ratio", "far_build_s", "near_build_s")] + [
+        ("far_evals", C.c_uint64), ("near_evals", C.c_uint64)] + [
+        (k, C.c_int64) for k in ("n_far", "n_near", "n_classes")]
+
+
 _P = C.c_void_p
 _DP = C.POINTER(C.c_double)
 _I32P = C.POINTER(C.c_int32)
@@ -127,6 +135,11 @@ SIGNATURES = {
     "phm_instantiate": ([_P, _DP, C.c_int, C.POINTER(_P)], C.c_int),
     "phm_reinstantiate": ([_P, _DP, C.c_int], C.c_int),
     "phm_instantiate_batch": ([_P, _DP, C.c_int, C.c_int, _P], C.c_int),
+    "phm_baseline_build": ([_P, _DP, C.c_int64, C.c_int, _P, C.c_int, _DP, C.c_int, C.c_double, C.c_int64, _P],
+                           C.c_int),
+    "phm_baseline_info_get": ([_P, _P], C.c_int),
+    "phm_aca_partial_dense": ([_DP, C.c_int64, C.c_int64, C.c_double, C.c_int64, C.c_uint64, _I64P,
+                               C.POINTER(C.c_int32), _DP, _DP], C.c_int),
     "phm_reinstantiate_batch": ([_P, C.c_int, _DP, C.c_int], C.c_int),
     "phm_instance_destroy": ([_P], C.c_int),
     "phm_instance_sync": ([_P], C.c_int),
@@ -642,6 +655,84 @@ def instantiate(pm: ParametricMatrix, theta) -> InstantiatedMatrix:
     h = _P()
     _check(lib().phm_instantiate(pm._h, _dp(th), th.size, C.byref(h)))
     return InstantiatedMatrix(pm, h, th)
+
+
+class Baseline:
+    H_ACA, H2_HCA = 1, 2
+
+
+class _BaselineParent:
+    """What an instance needs from its parent for a baseline (no parametric data)."""
+
+    def __init__(self, n: int, d: int, p_s: int, ctx):
+        self._n, self.ctx = n, ctx
+        self._P = p_s ** d
+
+    def n(self) -> int:
+        return self._n
+
+    def info(self) -> dict:
+        return {"P": self._P, "n": self._n}
+
+
+class BaselineMatrix(InstantiatedMatrix):
+    """HAcaMatrix / H2HcaMatrix (baselines.hpp:27-82) at one fixed theta:
+    apply, to_dense, mean_far_rank, coupling_ratio, build times and kernel
+    evaluation counts. Built by h_aca / h2_hca."""
+
+    def info(self) -> dict:
+        b = _BaselineInfo()
+        _check(lib().phm_baseline_info_get(self._h, C.byref(b)))
+        return {k: getattr(b, k) for k, _ in _BaselineInfo._fields_}
+
+    def mean_far_rank(self) -> float:
+        return self.info()["mean_far_rank"]
+
+    def coupling_ratio(self) -> float:
+        return self.info()["coupling_ratio"]
+
+    def reinstantiate(self, theta) -> None:
+        raise LogicError("a baseline matrix is built at a fixed theta")
+
+
+def _baseline(points, config: PHConfig, method: int, theta, eps, r_max, ctx) -> BaselineMatrix:
+    p = _points(points)
+    ctx = ctx or Context.default()
+    th = _f64(theta).ravel()
+    cfg = config.to_c(Format.H if method == Baseline.H_ACA else Format.H2)
+    h = _P()
+    _check(lib().phm_baseline_build(ctx._h, _dp(p), p.shape[0], p.shape[1], C.byref(cfg), method, _dp(th), th.size,
+                                    float(config.eps if eps is None else eps),
+                                    int(config.r_max_far if r_max is None else r_max), C.byref(h)))
+    return BaselineMatrix(_BaselineParent(p.shape[0], p.shape[1], config.p_s, ctx), h, th)
+
+
+def h_aca(points, config: PHConfig, theta, eps: Optional[float] = None, r_max: Optional[int] = None,
+          ctx: Optional[Context] = None) -> BaselineMatrix:
+    """HAcaMatrix(tree, blocks, spec, theta, eps, r_max) (baselines.cpp:52-89):
+    tree / blocks / kernel from the config; ACA far blocks, dense near blocks."""
+    return _baseline(points, config, Baseline.H_ACA, theta, eps, r_max, ctx)
+
+
+def h2_hca(points, config: PHConfig, theta, eps: Optional[float] = None, r_max: Optional[int] = None,
+           ctx: Optional[Context] = None) -> BaselineMatrix:
+    """H2HcaMatrix(tree, blocks, spec, theta, p_s, eps, r_max) (baselines.cpp:133-219)."""
+    return _baseline(points, config, Baseline.H2_HCA, theta, eps, r_max, ctx)
+
+
+def aca_partial(a, eps: float, r_max: int, seed: int):
+    """aca_partial (baselines.hpp:22-24) on a dense matrix: (V, Y, capped)."""
+    A = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    m, n = A.shape
+    cap = max(1, min(m, n, r_max))
+    V = np.zeros((m, cap), order="F")
+    Y = np.zeros((n, cap), order="F")
+    rank = C.c_int64()
+    capped = C.c_int32()
+    _check(lib().phm_aca_partial_dense(A.ctypes.data_as(_DP), m, n, eps, r_max, seed, C.byref(rank), C.byref(capped),
+                                       V.ctypes.data_as(_DP), Y.ctypes.data_as(_DP)))
+    t = rank.value
+    return V[:, :t].copy(order="F"), Y[:, :t].copy(order="F"), bool(capped.value)
 
 
 def instantiate_batch(pm: ParametricMatrix, thetas) -> List[InstantiatedMatrix]:

@@ -2,6 +2,7 @@
 // boundary; they become status codes that map back to the reference's
 // exception types, with the message in phm_last_error().
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -272,6 +273,66 @@ int phm_matrix_build(phm_context ctx, const double* points, int64_t n, int d, co
     m->ctx = ctx->ctx;
     m->m = phm::matrix_build(ctx->ctx, points, n, d, to_config(*cfg));
     *out = m.release();
+  });
+}
+int phm_baseline_build(phm_context ctx, const double* points, int64_t n, int d, const phm_config* cfg, int method,
+                       const double* theta, int n_theta, double eps, int64_t r_max, phm_instance* out) {
+  return guarded([&] {
+    need(ctx, "context");
+    need(points, "points");
+    need(cfg, "config");
+    need(theta, "theta");
+    need(out, "out");
+    if (n < 1) throw std::invalid_argument("n must be >= 1");
+    if (d < 1 || d > 3) throw std::invalid_argument("d must be 1..3");
+    if (method != PHM_BASELINE_H_ACA && method != PHM_BASELINE_H2_HCA) throw std::invalid_argument("unknown baseline");
+    if (r_max < 1) throw std::invalid_argument("r_max must be >= 1");
+    auto m = phm::baseline_build(ctx->ctx, points, n, d, to_config(*cfg),
+                                 method == PHM_BASELINE_H_ACA ? phm::Baseline::HAca : phm::Baseline::H2Hca, theta,
+                                 n_theta, eps, r_max);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto inst = phm::baseline_instance(m);
+    phm::instance_sync(*inst);
+    auto& H = const_cast<phm::HostMatrix&>(phm::matrix_host(*m));
+    H.stats.nf_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    auto I = std::make_unique<phm_instance_s>();
+    I->m = m;
+    I->inst = inst;
+    *out = I.release();
+  });
+}
+int phm_baseline_info_get(phm_instance inst, phm_baseline_info* out) {
+  return guarded([&] {
+    need(inst, "instance");
+    need(out, "out");
+    const auto& H = phm::matrix_host(*inst->m);
+    const phm::BaselineData& B = H.baseline;
+    if (B.method == phm::Baseline::None) throw std::logic_error("not a baseline instance");
+    *out = phm_baseline_info{};
+    out->method = B.method == phm::Baseline::HAca ? PHM_BASELINE_H_ACA : PHM_BASELINE_H2_HCA;
+    out->mean_far_rank = B.mean_far_rank;
+    out->coupling_ratio = B.coupling_ratio;
+    out->far_build_s = B.far_s;
+    out->near_build_s = H.stats.nf_s;
+    out->far_evals = B.far_evals;
+    out->near_evals = B.near_evals;
+    out->any_capped = B.any_capped ? 1 : 0;
+    out->n_far = static_cast<int64_t>(H.blocks.far.size());
+    out->n_near = static_cast<int64_t>(H.blocks.near.size());
+    out->n_classes = static_cast<int64_t>(B.rank.size());
+  });
+}
+int phm_aca_partial_dense(const double* a, int64_t m, int64_t n, double eps, int64_t r_max, uint64_t seed,
+                          int64_t* rank, int32_t* capped, double* v, double* y) {
+  return guarded([&] {
+    need(a, "a");
+    need(rank, "rank");
+    if (m < 1 || n < 1) throw std::invalid_argument("aca_partial: empty matrix");
+    auto f = phm::aca_partial([&](phm::Index i, phm::Index j) { return a[i + j * m]; }, m, n, eps, r_max, seed);
+    *rank = f.rank();
+    if (capped) *capped = f.capped ? 1 : 0;
+    if (v) std::memcpy(v, f.v.a.data(), f.v.a.size() * sizeof(double));
+    if (y) std::memcpy(y, f.y.a.data(), f.y.a.size() * sizeof(double));
   });
 }
 int phm_matrix_build_host(const double* points, int64_t n, int d, const phm_config* cfg, phm_matrix* out) {

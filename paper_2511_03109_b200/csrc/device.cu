@@ -299,6 +299,8 @@ struct DevMatrix {
   int ncls = 0;
   std::vector<dev::ClassMeta> cmeta_h;
   DBuf cmeta, class_mid, class_mid_dims, class_L, class_R;
+  bool baseline = false;  // fixed far field (H-ACA / H^2-HCA at one theta)
+  DBuf fixed_H, fixed_C;
   std::int64_t H_len = 0, C_len = 0;
   int capA = 0, capB = 0, capT = 0;
   // H^2 coupling CSR by sigma node
@@ -840,7 +842,26 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
   }
 
   // --- far field: classes
-  {
+  if (H.baseline.method != Baseline::None) {
+    // fixed far field (baselines): per class H = I_t and, for H^2, C_k; the
+    // instance copies them (no theta-core contraction)
+    const BaselineData& B = H.baseline;
+    M.baseline = true;
+    M.ncls = static_cast<int>(B.rank.size());
+    for (int k = 0; k < M.ncls; ++k) {
+      dev::ClassMeta cm{};
+      cm.rl = cm.rr = B.rank[k];
+      PHM_CHECK(cm.rl <= 128, "baseline far rank above 128 unsupported on device");
+      cm.h_off = B.h_off[k];
+      if (M.h2) cm.c_off = static_cast<std::int64_t>(k) * M.P * M.P;
+      M.cmeta_h.push_back(cm);
+    }
+    M.H_len = static_cast<std::int64_t>(B.fixed_h.size());
+    M.C_len = M.h2 ? static_cast<std::int64_t>(M.ncls) * M.P * M.P : 0;
+    upload(M.cmeta, M.cmeta_h, st);
+    upload(M.fixed_H, B.fixed_h, st);
+    if (M.h2) upload(M.fixed_C, B.fixed_c, st);
+  } else {
     M.ncls = static_cast<int>(H.couplings.size());
     std::vector<double> mid, L, R;
     std::vector<std::int32_t> mdims;
@@ -1152,6 +1173,17 @@ void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCoun
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   CK(cudaSetDevice(M.ctx->device));
+  if (M.baseline) {
+    // baselines: the far field was factorised at the build theta; the dense
+    // near blocks are evaluated now (charged to the build's near_evals)
+    const BaselineData& B = H.baseline;
+    cudaStream_t st = M.ctx->stream;
+    I.theta = B.theta;
+    if (M.H_len) CK(cudaMemcpyAsync(I.H.p, M.fixed_H.p, sizeof(double) * M.H_len, cudaMemcpyDeviceToDevice, st));
+    if (M.C_len) CK(cudaMemcpyAsync(I.C.p, M.fixed_C.p, sizeof(double) * M.C_len, cudaMemcpyDeviceToDevice, st));
+    inst_near(I, B.theta.data(), {}, dev::ThetaV{}, st, nullptr);
+    return;
+  }
   // theta box check before any launch (farfield.cpp:23-24)
   const auto v = parametric_vectors(H.grids, theta, n_theta);
   I.theta.assign(theta, theta + n_theta);
@@ -1233,9 +1265,24 @@ void run_instantiate_batch(const std::vector<DevInstance*>& insts, const double*
 }
 }  // namespace
 
+std::shared_ptr<DevInstance> baseline_instance(std::shared_ptr<DevMatrix> m) {
+  PHM_CHECK(m->baseline, "baseline_instance: not a baseline matrix");
+  CK(cudaSetDevice(m->ctx->device));
+  auto I = alloc_instance(m);
+  run_instantiate(*I, nullptr, 0, nullptr);
+  return I;
+}
+
+std::shared_ptr<DevMatrix> baseline_build(std::shared_ptr<Context> ctx, const double* points, Index n, int d,
+                                          const Config& cfg, Baseline method, const double* theta, int n_theta,
+                                          double eps, Index r_max) {
+  return matrix_upload(ctx, build_baseline_host(points, n, d, cfg, method, theta, n_theta, eps, r_max));
+}
+
 std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const double* theta, int n_theta,
                                          StageCounters* counters) {
   if (!m->ctx) throw std::logic_error("instantiate: host-only matrix (built without a device)");
+  if (m->baseline) throw std::logic_error("instantiate: a baseline matrix is built at a fixed theta");
   CK(cudaSetDevice(m->ctx->device));
   // validate theta first so nothing is allocated for a bad call
   (void)parametric_vectors(m->hm->grids, theta, n_theta);
@@ -1247,6 +1294,7 @@ std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const dou
 std::vector<std::shared_ptr<DevInstance>> instantiate_batch(std::shared_ptr<DevMatrix> m, const double* thetas,
                                                             int n_theta, int count, StageCounters* counters) {
   if (!m->ctx) throw std::logic_error("instantiate: host-only matrix (built without a device)");
+  if (m->baseline) throw std::logic_error("instantiate: a baseline matrix is built at a fixed theta");
   PHM_CHECK(count >= 1, "instantiate_batch: count must be >= 1");
   CK(cudaSetDevice(m->ctx->device));
   for (int b = 0; b < count; ++b) (void)parametric_vectors(m->hm->grids, thetas + b * n_theta, n_theta);
@@ -1263,11 +1311,13 @@ std::vector<std::shared_ptr<DevInstance>> instantiate_batch(std::shared_ptr<DevM
 void reinstantiate_batch(const std::vector<DevInstance*>& insts, const double* thetas, int n_theta,
                          StageCounters* counters) {
   PHM_CHECK(!insts.empty(), "reinstantiate_batch: no instances");
+  if (insts[0]->M->baseline) throw std::logic_error("reinstantiate: a baseline matrix is built at a fixed theta");
   for (DevInstance* I : insts) PHM_CHECK(I->M == insts[0]->M, "reinstantiate_batch: instances of different matrices");
   run_instantiate_batch(insts, thetas, n_theta, counters);
 }
 
 void reinstantiate(DevInstance& inst, const double* theta, int n_theta, StageCounters* counters) {
+  if (inst.M->baseline) throw std::logic_error("reinstantiate: a baseline matrix is built at a fixed theta");
   run_instantiate(inst, theta, n_theta, counters);
 }
 const std::vector<double>& instance_theta(const DevInstance& inst) { return inst.theta; }
@@ -1519,6 +1569,7 @@ void instantiate_apply_tree(DevInstance& I, const double* theta, int n_theta, co
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   PHM_CHECK(m >= 1, "apply: m must be >= 1");
+  if (M.baseline) throw std::logic_error("instantiate: a baseline matrix is built at a fixed theta");
   CK(cudaSetDevice(M.ctx->device));
   const auto v = parametric_vectors(H.grids, theta, n_theta);
   const dev::ThetaV tv = make_theta_v(v);

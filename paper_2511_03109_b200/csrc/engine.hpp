@@ -53,6 +53,13 @@ std::int64_t matrix_near_elems(const DevMatrix& m, int kind);
 
 std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const double* theta, int n_theta,
                                          StageCounters* counters);
+// Baselines (baselines.hpp): H-ACA / H^2-HCA built at one theta; the
+// instance holds the dense near blocks (evaluated on the device) and the
+// fixed far field, and applies through the same kernels.
+std::shared_ptr<DevMatrix> baseline_build(std::shared_ptr<Context> ctx, const double* points, Index n, int d,
+                                          const Config& cfg, Baseline method, const double* theta, int n_theta,
+                                          double eps, Index r_max);
+std::shared_ptr<DevInstance> baseline_instance(std::shared_ptr<DevMatrix> m);
 // Re-instantiate in place at a new theta (reuses the device buffers).
 void reinstantiate(DevInstance& inst, const double* theta, int n_theta, StageCounters* counters);
 // theta-batched instantiate (sweeps): count thetas (count x n_theta,

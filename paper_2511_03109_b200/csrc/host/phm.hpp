@@ -282,6 +282,19 @@ struct BuildStats {
   int svd_fallbacks = 0;  // non-converged crosses redone by full TT-SVD
 };
 
+enum class Baseline : int { None = 0, HAca = 1, H2Hca = 2 };
+struct BaselineData {
+  Baseline method = Baseline::None;
+  std::vector<double> theta;
+  std::vector<int> rank;           // per class (H-ACA: per far block): ACA rank t
+  std::vector<std::int64_t> h_off; // per class: offset of its t x t identity in fixed_h
+  std::vector<double> fixed_h;     // H_b = I_t per class, column-major
+  std::vector<double> fixed_c;     // H^2-HCA: C_k = V_k Y_k^T, P x P per class
+  double far_s = 0.0, mean_far_rank = 0.0, coupling_ratio = 0.0;
+  std::uint64_t far_evals = 0, near_evals = 0;
+  bool any_capped = false;
+};
+
 // Everything the offline stage produces on the host, in the reference's
 // representation. The device layer flattens it (device.cu).
 struct HostMatrix {
@@ -304,15 +317,37 @@ struct HostMatrix {
   std::vector<char> near_local, far_local, node_local;
   BuildStats stats;
   StageCounters counters;
+  // Non-parametric baselines (baselines.hpp): the far field is fixed at one
+  // theta, so instantiate copies it instead of contracting theta-cores.
+  BaselineData baseline;
   int d() const { return tree->d; }
   Index n() const { return tree->n; }
   Index P() const;  // p_s^d
 };
 
+// Partially pivoted ACA (aca_impl.hpp:34-173) as the baselines use it:
+// A ~ V Y^T with V m x t, Y n x t (baselines.cpp:30-50).
+struct LowRank {
+  Mat v, y;
+  bool capped = false;
+  Index rank() const { return v.cols; }
+};
+LowRank aca_partial(const std::function<double(Index, Index)>& entry, Index m, Index n, double eps, Index r_max,
+                    std::uint64_t seed);
+LowRank aca_partial_rng(const std::function<double(Index, Index)>& entry, Index m, Index n, double eps, Index r_max,
+                        Rng& rng);
+
 // Offline build on the host (everything except GPU snapshot generation).
 std::unique_ptr<HostMatrix> build_host(const double* points, Index n, int d, const Config& cfg);
 // Explicit L (P x r_d) and R (P x r_{d+dt}) of a coupling (farfield.cpp:157-184).
 void assemble_lr_public(const Coupling& cp, Mat& L, Mat& R);
+
+// Baselines at a fixed theta (baselines.cpp:52-100 H-ACA, :133-219 H^2-HCA):
+// tree and blocks as the parametric build, ACA factors on the host, dense
+// near blocks evaluated on the device at instantiate (Direct near mode).
+std::unique_ptr<HostMatrix> build_baseline_host(const double* points, Index n, int d, const Config& cfg,
+                                                Baseline method, const double* theta, int n_theta, double eps,
+                                                Index r_max);
 
 // HMAT v1 artifacts, byte-compatible with proj/src/serialize.cpp.
 bool artifact_is_h2(const std::string& path);

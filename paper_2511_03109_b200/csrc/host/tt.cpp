@@ -845,4 +845,27 @@ CrossResult tt_cross(const EntryFn& f, const CrossOptions& opt) {
   return res;
 }
 
+// aca_partial (baselines.cpp:45-50): Rng(seed), the ACA engine, and the
+// rank-1 terms as the columns of V (m x t) and Y (n x t).
+LowRank aca_partial_rng(const std::function<double(Index, Index)>& entry, Index m, Index n, double eps, Index r_max,
+                        Rng& rng) {
+  PHM_CHECK(eps > 0.0, "aca_partial: eps must be positive");
+  AcaOut a = aca(entry, m, n, eps, r_max, rng, nullptr);
+  LowRank f;
+  f.capped = a.capped;
+  const Index t = a.rank();
+  f.v = Mat(m, t);
+  f.y = Mat(n, t);
+  for (Index l = 0; l < t; ++l) {
+    std::copy(a.us[l].begin(), a.us[l].end(), f.v.a.begin() + l * m);
+    std::copy(a.vs[l].begin(), a.vs[l].end(), f.y.a.begin() + l * n);
+  }
+  return f;
+}
+LowRank aca_partial(const std::function<double(Index, Index)>& entry, Index m, Index n, double eps, Index r_max,
+                    std::uint64_t seed) {
+  Rng rng(seed);
+  return aca_partial_rng(entry, m, n, eps, r_max, rng);
+}
+
 }  // namespace phm
