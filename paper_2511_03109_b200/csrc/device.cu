@@ -49,9 +49,6 @@ void launch_coupling_mma(cudaStream_t, const CouplingItem*, int, const std::int3
                          const double*, int, const double*, int, double*);
 void launch_coupling_reduce(cudaStream_t, const std::int32_t*, const std::int32_t*, int, const double*, int, int,
                             double*);
-void launch_near_mvm(cudaStream_t, const RowItem*, int, const std::int64_t*, const std::int32_t*,
-                     const std::int64_t*, const double*, const double*, double*);
-void launch_near_mvm_sym(cudaStream_t, const SymItem*, int, const double*, const double*, double*);
 void launch_near_tma_apply(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
                            double*, int*);
 void launch_near_mvm_symcsr(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
@@ -280,8 +277,6 @@ struct DevMatrix {
   std::int64_t n_snap_tiles = 0;
   DBuf inst_tiles, near_w_meta, near_cores, near_core_dims;
   std::int64_t n_inst_tiles = 0, n_near_local = 0, w_len = 0;
-  DBuf row_items, nb_tb, nb_tn, nb_doff;
-  int n_row_items = 0;
   // symmetric near storage (sigma <= tau blocks only)
   bool sym = false;
   bool sharded = false;          // a row shard (rows [row_begin, row_end) of y)
@@ -812,35 +807,6 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     upload(M.k9_ld, ld, st);
     upload(M.k9_tr, tr, st);
   }
-  // K6 work: CSR by sigma leaf, row chunks of 128
-  if (!M.sym) {
-    std::vector<std::vector<Index>> by_sigma(M.nnodes);
-    for (Index b = 0; b < nnear; ++b)
-      if (M.near_doff[b] >= 0) by_sigma[H.blocks.near[b].sigma].push_back(b);
-    std::vector<dev::RowItem> items;
-    std::vector<std::int64_t> tb, dof;
-    std::vector<std::int32_t> tn;
-    for (int s = 0; s < M.nnodes; ++s) {
-      if (by_sigma[s].empty()) continue;
-      const int bbeg = static_cast<int>(tb.size());
-      for (Index b : by_sigma[s]) {
-        const Block blk = H.blocks.near[b];
-        tb.push_back(T.nodes[blk.tau].begin);
-        tn.push_back(static_cast<std::int32_t>(T.nodes[blk.tau].count));
-        dof.push_back(M.near_doff[b]);
-      }
-      const int bend = static_cast<int>(tb.size());
-      const int ns = static_cast<int>(T.nodes[s].count);
-      for (int i0 = 0; i0 < ns; i0 += 128)
-        items.push_back({T.nodes[s].begin + i0, std::min(128, ns - i0), ns, i0, bbeg, bend, 0});
-    }
-    M.n_row_items = static_cast<int>(items.size());
-    upload(M.row_items, items, st);
-    upload(M.nb_tb, tb, st);
-    upload(M.nb_tn, tn, st);
-    upload(M.nb_doff, dof, st);
-  }
-
   // --- far field: classes
   if (H.baseline.method != Baseline::None) {
     // fixed far field (baselines): per class H = I_t and, for H^2, C_k; the

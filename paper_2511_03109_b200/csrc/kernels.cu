@@ -438,53 +438,6 @@ __global__ void k_leaf_fwd(const std::int32_t* __restrict__ leaves, const std::i
   }
 }
 
-// ----------------------------------------------------------------- K4
-// xhat_p[a] = sum_children sum_b prod_k E_{c,k}(b_k, a_k) xhat_c[b]
-// (fast_kron_transposed, chebyshev.cpp:253-260). One CTA per parent.
-__global__ void k_up(const std::int32_t* __restrict__ nodes, const std::int32_t* __restrict__ first_child,
-                     const std::int32_t* __restrict__ count, const double* __restrict__ E, int d, int ps, int P,
-                     int nc, int m, double* __restrict__ xhat) {
-  extern __shared__ double sm[];
-  const int p = nodes[blockIdx.x];
-  const int fc = first_child[p];
-  const int fsz = d * ps * ps;
-  double* se = sm;             // nc x d x ps x ps
-  double* sx = se + nc * fsz;  // nc x P
-  for (int e = threadIdx.x; e < nc * fsz; e += blockDim.x) se[e] = E[static_cast<std::int64_t>(fc) * fsz + e];
-  for (int c = 0; c < m; ++c) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < nc * P; e += blockDim.x) {
-      const int ch = e / P, b = e % P;
-      sx[e] = count[fc + ch] > 0 ? xhat[(static_cast<std::int64_t>(fc + ch) * m + c) * P + b] : 0.0;
-    }
-    __syncthreads();
-    for (int a = threadIdx.x; a < P; a += blockDim.x) {
-      int da[3];
-      int rem = a;
-      for (int k = 0; k < d; ++k) {
-        da[k] = rem % ps;
-        rem /= ps;
-      }
-      double s = 0.0;
-      for (int ch = 0; ch < nc; ++ch) {
-        if (count[fc + ch] == 0) continue;
-        const double* ef = se + ch * fsz;
-        const double* xc = sx + ch * P;
-        for (int b = 0; b < P; ++b) {
-          int r2 = b;
-          double f = xc[b];
-          for (int k = 0; k < d; ++k) {
-            f *= ef[(k * ps + (r2 % ps)) * ps + da[k]];
-            r2 /= ps;
-          }
-          s += f;
-        }
-      }
-      xhat[(static_cast<std::int64_t>(p) * m + c) * P + a] = s;
-    }
-  }
-}
-
 // ----------------------------------------------------------------- K5
 // yhat_sigma = sum over the far blocks of sigma of C_k xhat_tau (CSR by
 // sigma, deterministic order, no atomics). One CTA per sigma node.
@@ -750,57 +703,6 @@ __global__ void __launch_bounds__(128) k_near_mrhs(const MrhsItem* __restrict__ 
       }
 }
 
-// ----------------------------------------------------------------- K6
-// y[rows] = sum over the near blocks of sigma of D_b x_tau. 8 warps split the
-// columns of each block; each lane owns rows lane + 32q (q < 4), so every
-// warp load reads 32 consecutive doubles of one column. Fixed reduction
-// order over warps: deterministic.
-__global__ void __launch_bounds__(256) k_near_mvm(const RowItem* __restrict__ items, const std::int64_t* __restrict__ tb,
-                                                  const std::int32_t* __restrict__ tn,
-                                                  const std::int64_t* __restrict__ doff, const double* __restrict__ D,
-                                                  const double* __restrict__ xp, double* __restrict__ yp) {
-  __shared__ double red[8][128];
-  const RowItem it = items[blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  bool live[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) live[q] = lane + 32 * q < it.rows;
-  for (int b = it.bbeg; b < it.bend; ++b) {
-    const double* Db = D + doff[b] + it.i0 + lane;
-    const double* xb = xp + tb[b];
-    const int ncol = tn[b];
-    const std::int64_t ld = it.ld;
-    int j = warp;
-    for (; j + 8 < ncol; j += 16) {
-      const double x0 = xb[j], x1 = xb[j + 8];
-      double v0[4], v1[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        v0[q] = live[q] ? ld_stream(Db + j * ld + 32 * q) : 0.0;
-        v1[q] = live[q] ? ld_stream(Db + (j + 8) * ld + 32 * q) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] += v0[q] * x0 + v1[q] * x1;
-    }
-    for (; j < ncol; j += 8) {
-      const double x0 = xb[j];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (live[q]) acc[q] += ld_stream(Db + j * ld + 32 * q) * x0;
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) red[warp][lane + 32 * q] = acc[q];
-  __syncthreads();
-  if (threadIdx.x < it.rows) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
-    yp[it.row0 + threadIdx.x] = s;
-  }
-}
-
 // K6, symmetric storage: every stored block is streamed once and used twice
 // (y_sigma += D x_tau and y_tau += D^T x_sigma), halving the near-field
 // bytes of both instantiate and MVM for the (symmetric) radial kernels.
@@ -808,142 +710,6 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
-}
-
-__global__ void __launch_bounds__(256) k_near_mvm_sym(const SymItem* __restrict__ items, const double* __restrict__ D,
-                                                      const double* __restrict__ xp, double* __restrict__ part) {
-  __shared__ double red[8][128];
-  const SymItem it = items[blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double racc[4] = {0.0, 0.0, 0.0, 0.0};
-  double xs[4];
-  bool live[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    live[q] = lane + 32 * q < it.rows;
-    xs[q] = live[q] ? xp[it.x_row0 + it.i0 + lane + 32 * q] : 0.0;
-  }
-  const double* Db = D + it.d_off + it.i0 + lane;
-  const double* xt = xp + it.x_col0;
-  const std::int64_t ld = it.ld;
-  int j = warp;
-  for (; j + 8 < it.ncol; j += 16) {
-    const double x0 = xt[j], x1 = xt[j + 8];
-    double v0[4], v1[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      v0[q] = live[q] ? ld_stream(Db + j * ld + 32 * q) : 0.0;
-      v1[q] = live[q] ? ld_stream(Db + (j + 8) * ld + 32 * q) : 0.0;
-    }
-    double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      racc[q] += v0[q] * x0 + v1[q] * x1;
-      c0 += v0[q] * xs[q];
-      c1 += v1[q] * xs[q];
-    }
-    if (!it.diag) {
-      c0 = warp_sum(c0);
-      c1 = warp_sum(c1);
-      if (lane == 0) {
-        part[it.p_col + j] = c0;
-        part[it.p_col + j + 8] = c1;
-      }
-    }
-  }
-  for (; j < it.ncol; j += 8) {
-    const double x0 = xt[j];
-    double c0 = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double v = live[q] ? ld_stream(Db + j * ld + 32 * q) : 0.0;
-      racc[q] += v * x0;
-      c0 += v * xs[q];
-    }
-    if (!it.diag) {
-      c0 = warp_sum(c0);
-      if (lane == 0) part[it.p_col + j] = c0;
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) red[warp][lane + 32 * q] = racc[q];
-  __syncthreads();
-  if (threadIdx.x < it.rows) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
-    part[it.p_row + threadIdx.x] = s;
-  }
-}
-
-// Warp-per-item version: one warp streams a whole stored block (<= 128
-// rows per item), lane l owning rows l + 32q. Column partials of 32
-// consecutive columns are kept per lane and reduced across the warp with one
-// transpose-reduce (16 + 8 + 4 + 2 + 1 = 31 shuffles for 32 columns) instead
-// of a 5-shuffle reduction per column; lane l ends with column j0 + l.
-template <int NQ>
-__device__ __forceinline__ void sym_block(const SymItem& it, const double* __restrict__ D,
-                                          const double* __restrict__ xp, double* __restrict__ part, int lane) {
-  double racc[NQ], xs[NQ];
-  bool live[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    live[q] = lane + 32 * q < it.rows;
-    xs[q] = live[q] ? xp[it.x_row0 + it.i0 + lane + 32 * q] : 0.0;
-    racc[q] = 0.0;
-  }
-  const double* Db = D + it.d_off + it.i0 + lane;
-  const double* xt = xp + it.x_col0;
-  const std::int64_t ld = it.ld;
-  for (int j0 = 0; j0 < it.ncol; j0 += 32) {
-    double c[32];
-#pragma unroll
-    for (int jj = 0; jj < 32; ++jj) {
-      const int j = j0 + jj;
-      double cj = 0.0;
-      if (j < it.ncol) {
-        const double x0 = xt[j];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const double v = live[q] ? ld_stream(Db + j * ld + 32 * q) : 0.0;
-          racc[q] += v * x0;
-          cj += v * xs[q];
-        }
-      }
-      c[jj] = cj;
-    }
-    if (!it.diag) {
-      // transpose-reduce: after the round with offset o each lane keeps the
-      // half of its columns whose bit o matches its own lane bit
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        const bool upper = lane & o;
-#pragma unroll
-        for (int k = 0; k < o; ++k) {
-          const double send = upper ? c[k] : c[k + o];
-          const double keep = upper ? c[k + o] : c[k];
-          c[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-      }
-      if (j0 + lane < it.ncol) part[it.p_col + j0 + lane] = c[0];
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < NQ; ++q)
-    if (live[q]) part[it.p_row + lane + 32 * q] = racc[q];
-}
-
-__global__ void __launch_bounds__(128) k_near_mvm_sym2(const SymItem* __restrict__ items, int nitems,
-                                                       const double* __restrict__ D, const double* __restrict__ xp,
-                                                       double* __restrict__ part) {
-  const int w = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (w >= nitems) return;
-  const int lane = threadIdx.x & 31;
-  const SymItem it = items[w];
-  if (it.rows <= 64)
-    sym_block<2>(it, D, xp, part, lane);
-  else
-    sym_block<4>(it, D, xp, part, lane);
 }
 
 // CSR-by-sigma version: a CTA streams every stored block owned by its leaf
@@ -1387,78 +1153,6 @@ __global__ void k_near_gather(const std::int64_t* __restrict__ leaf_row0, const 
   }
 }
 
-// ----------------------------------------------------------------- K7
-// yhat_child[b] += sum_a prod_k E_k(b_k, a_k) yhat_parent[a] (fast_kron,
-// chebyshev.cpp:286-295). One CTA per child node of the level.
-__global__ void k_down(const std::int32_t* __restrict__ nodes, const std::int32_t* __restrict__ parent,
-                       const double* __restrict__ E, int d, int ps, int P, int m, double* __restrict__ yhat) {
-  extern __shared__ double sm[];
-  const int ch = nodes[blockIdx.x];
-  const int p = parent[ch];
-  const int fsz = d * ps * ps;
-  double* se = sm;
-  double* sy = se + fsz;
-  for (int e = threadIdx.x; e < fsz; e += blockDim.x) se[e] = E[static_cast<std::int64_t>(ch) * fsz + e];
-  for (int c = 0; c < m; ++c) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < P; e += blockDim.x) sy[e] = yhat[(static_cast<std::int64_t>(p) * m + c) * P + e];
-    __syncthreads();
-    for (int b = threadIdx.x; b < P; b += blockDim.x) {
-      int db[3];
-      int rem = b;
-      for (int k = 0; k < d; ++k) {
-        db[k] = rem % ps;
-        rem /= ps;
-      }
-      double s = 0.0;
-      for (int a = 0; a < P; ++a) {
-        int r2 = a;
-        double f = sy[a];
-        for (int k = 0; k < d; ++k) {
-          f *= se[(k * ps + db[k]) * ps + (r2 % ps)];
-          r2 /= ps;
-        }
-        s += f;
-      }
-      yhat[(static_cast<std::int64_t>(ch) * m + c) * P + b] += s;
-    }
-  }
-}
-
-// y_i += sum_a prod_k U_k(i, a_k) yhat_sigma[a] (chebyshev.cpp:270-282).
-__global__ void k_leaf_bwd(const std::int32_t* __restrict__ leaves, const std::int64_t* __restrict__ begin,
-                           const std::int32_t* __restrict__ count, const double* __restrict__ U, std::int64_t n,
-                           int d, int ps, int P, const double* __restrict__ yhat, int m, std::int64_t row_lo,
-                           std::int64_t row_hi, double* __restrict__ yp) {
-  extern __shared__ double sm[];
-  const int leaf = leaves[blockIdx.x];
-  const std::int64_t b0 = begin[leaf];
-  const int cnt = count[leaf];
-  for (int c = 0; c < m; ++c) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < P; e += blockDim.x) sm[e] = yhat[(static_cast<std::int64_t>(leaf) * m + c) * P + e];
-    __syncthreads();
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      const std::int64_t pos = b0 + i;
-      if (pos < row_lo || pos >= row_hi) continue;
-      // fold dimension by dimension: last dim first, like the reference
-      double f[3][16];
-      for (int k = 0; k < d; ++k)
-        for (int j = 0; j < ps; ++j) f[k][j] = U[(static_cast<std::int64_t>(k) * n + pos) * ps + j];
-      double s = 0.0;
-      for (int a = 0; a < P; ++a) {
-        int rem = a;
-        double g = sm[a];
-        for (int k = 0; k < d; ++k) {
-          g *= f[k][rem % ps];
-          rem /= ps;
-        }
-        s += g;
-      }
-      yp[static_cast<std::int64_t>(c) * n + pos] += s;
-    }
-  }
-}
 
 // ----------------------------------------------------------------- K8
 // H form: y_sigma += S_b (H_k (T_b^T x_tau)) for the far blocks of sigma at
@@ -1824,13 +1518,6 @@ void launch_coupling(cudaStream_t st, const std::int32_t* sig, int nsig, const s
   if (nsig == 0) return;
   k_coupling<<<nsig, threads_for(P), P * sizeof(double), st>>>(sig, fbeg, ftau, fcls, C, P, m, xhat, yhat);
 }
-void launch_near_mvm_sym(cudaStream_t st, const SymItem* items, int nitems, const double* D, const double* xp,
-                         double* part) {
-  if (nitems == 0) return;
-  // k_near_mvm_sym2 (warp per block, transpose-reduce) measured 3.3x slower
-  // than this CTA-per-block version at C3 (242 registers, low occupancy).
-  k_near_mvm_sym<<<nitems, 256, 0, st>>>(items, D, xp, part);
-}
 void launch_near_tma_apply(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks,
                            const double* D, const double* xp, double* part, int* counter) {
   if (nitems == 0) return;
@@ -1977,11 +1664,6 @@ void launch_coupling_reduce(cudaStream_t st, const std::int32_t* grp_sigma, cons
       grp_sigma, grp_items, partial, P, m, yhat);
 }
 
-void launch_near_mvm(cudaStream_t st, const RowItem* items, int nitems, const std::int64_t* tb, const std::int32_t* tn,
-                     const std::int64_t* doff, const double* D, const double* xp, double* yp) {
-  if (nitems == 0) return;
-  k_near_mvm<<<nitems, 256, 0, st>>>(items, tb, tn, doff, D, xp, yp);
-}
 void launch_down(cudaStream_t st, const std::int32_t* nodes, int cnt, const std::int32_t* parent, const double* E,
                  int d, int ps, int P, int m, double* yhat) {
   if (cnt == 0) return;

@@ -1,17 +1,23 @@
 // sm_100a kernels of the online stage (instantiate + MVM) and the offline
 // snapshot generator. Numbering follows SURVEY.md §2.1:
-//   K11 k_snapshot        near-field kernel snapshots at theta nodes (offline)
-//   K1  k_inst_flat       D = sum_k w_k S_k  (snapshot mode, flat HBM stream)
-//   K1  k_inst_tiles      D_b = G1_b w_b     (TT near mode, per-block tiles)
-//   --  k_near_w          w_b = prod_i contract(G_{b,i+1}, v_i) (TT mode)
-//   K2  k_class_inst      H_k(theta) and C_k = L_k H_k R_k^T per class
-//   K10 k_gather/k_scatter tree-order permutation of x / y
-//   K3  k_leaf_fwd        xhat_sigma = U_sigma^T x_sigma
-//   K4  k_up              xhat_parent += E^T xhat_child (one launch per level)
-//   K5  k_coupling        yhat_sigma += C_k xhat_tau (CSR by sigma)
-//   K6  k_near_mvm        y_sigma = sum_tau D_b x_tau (CSR by sigma, no atomics)
-//   K7  k_down/k_leaf_bwd yhat_child += E yhat_parent; y += U yhat
-//   K8  k_far_h           y_sigma += S_b H_k T_b^T x_tau (H form, per level)
+//   K11   k_snapshot          near-field kernel snapshots at theta nodes (offline)
+//   K1+K6 k_near_tma          snapshot instantiate fused with the near GEMV (TMA ring)
+//   K1    k_inst_flat         D = sum_k w_k S_k  (snapshot mode, flat HBM stream)
+//   K1    k_inst_flat_batch   the same for B thetas per snapshot pass (sweeps)
+//   K1    k_inst_tiles        D_b = G1_b w_b     (TT near mode, per-block tiles)
+//   --    k_near_w            w_b = prod_i contract(G_{b,i+1}, v_i) (TT mode)
+//   K2    k_class_inst        H_k(theta) and C_k = L_k H_k R_k^T per class
+//   K10   k_gather/k_scatter  tree-order permutation of x / y
+//   K3    k_leaf_fwd          xhat_sigma = U_sigma^T x_sigma
+//   K4    k_up2               xhat_parent += E^T xhat_child (one launch per level)
+//   K5    k_coupling_mma      yhat_sigma += C_k xhat_tau (grouped fp64 DMMA) + reduce
+//   K6    k_near_tma_apply    two-sided near GEMV over TMA (apply alone)
+//   K6    k_near_mvm_symcsr   the same with plain loads (leaves > 128 rows)
+//   --    k_near_gather       fixed-order sum of the near partial segments
+//   K7    k_down2/k_leaf_bwd2 yhat_child += E yhat_parent; y += U yhat
+//   K8    k_far_h             y_sigma += S_b H_k T_b^T x_tau (H form, per level)
+//   K9    k_near_mrhs         Y_sigma += D_b X_tau on fp64 DMMA (m >= 4 RHS)
+//   --    k_exact_rows        exact probe rows for estimate_error
 #pragma once
 
 #include <cstdint>
@@ -58,11 +64,6 @@ struct ClassMeta {
   std::int32_t rl, rr, dims_off, pad;  // dims_off into class_mid_dims (3 per theta core)
 };
 
-struct RowItem {  // K6 work item: up to 128 rows of one leaf sigma
-  std::int64_t row0;
-  std::int32_t rows, ld, i0, bbeg, bend, pad;
-};
-
 // K5 (grouped DMMA): a group is up to 32 sigma nodes of one level with the
 // same child parity (so their far partners share translation classes); an
 // item is a contiguous range of that group's classes. cls_tau[e*32 + slot] is
@@ -72,14 +73,6 @@ struct CouplingItem {
   std::int32_t group, e_begin, e_end, pad;
 };
 
-// K6 with symmetric near storage: one item per (stored block, 128-row
-// chunk). The item writes its row partial D x_tau (rows doubles at p_row)
-// and, for off-diagonal blocks, its column partial D^T x_sigma (ncol doubles
-// at p_col); k_near_gather sums the partials of each leaf in a fixed order.
-struct SymItem {
-  std::int64_t d_off, x_row0, x_col0, p_row, p_col;
-  std::int32_t ld, i0, rows, ncol, diag, pad;
-};
 // CSR form of the symmetric near GEMV: one item per (leaf sigma, 128-row
 // chunk) streaming all stored blocks owned by sigma; row sums accumulate
 // across those blocks, column sums are written per block.
