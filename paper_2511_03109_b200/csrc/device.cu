@@ -45,8 +45,8 @@ void launch_up(cudaStream_t, const std::int32_t*, int, const std::int32_t*, cons
 void launch_coupling(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*,
                      const std::int32_t*, const double*, int, int, const double*, double*);
 bool coupling_mma_supported(int P);
-void launch_coupling_mma(cudaStream_t, const CouplingItem*, int, const std::int32_t*, const std::int32_t*,
-                         const double*, int, const double*, int, double*);
+void launch_coupling_mma(cudaStream_t, const CouplingItem*, int, const std::int32_t*, const std::uint8_t*,
+                         const std::int32_t*, const double*, int, const double*, int, double*);
 void launch_coupling_reduce(cudaStream_t, const std::int32_t*, const std::int32_t*, int, const double*, int, int,
                             double*);
 void launch_near_tma_apply(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
@@ -303,7 +303,7 @@ struct DevMatrix {
   int n_cp_sig = 0;
   // H^2 coupling, grouped DMMA path (P in {16, 32, 64, 128})
   bool cp_mma = false;
-  DBuf cg_items, cg_cls, cg_tau, cg_grp_sigma, cg_grp_items, cg_partial;
+  DBuf cg_items, cg_cls, cg_tiles, cg_tau, cg_grp_sigma, cg_grp_items, cg_partial;
   int n_cg_items = 0, n_cg_groups = 0;
   // H form far CSR by level
   DBuf fh_items, fh_tb, fh_tn, fh_cls, fh_soff, fh_toff, fh_S, fh_T;
@@ -917,6 +917,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
         by_lp[{T.nodes[s].level, parity}].push_back(s);
       }
       std::vector<std::int32_t> grp_sigma, grp_items{0}, item_cls, cls_tau;
+      std::vector<std::uint8_t> item_tiles;
       std::vector<dev::CouplingItem> items;
       for (auto& kv : by_lp) {
         const auto& sigs = kv.second;
@@ -941,6 +942,10 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
           for (auto& cr : table) {
             item_cls.push_back(cr.first);
             cls_tau.insert(cls_tau.end(), cr.second.begin(), cr.second.end());
+            std::uint8_t tiles = 0;  // n-tiles of 8 slots holding a partner
+            for (int slot = 0; slot < kSlots; ++slot)
+              if (cr.second[slot] >= 0) tiles |= static_cast<std::uint8_t>(1u << (slot >> 3));
+            item_tiles.push_back(tiles);
           }
           const int e_end = static_cast<int>(item_cls.size());
           for (; e < e_end; e += kItemClasses) items.push_back({grp, e, std::min(e + kItemClasses, e_end), 0});
@@ -951,6 +956,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
       M.n_cg_groups = static_cast<int>(grp_items.size()) - 1;
       upload(M.cg_items, items, st);
       upload(M.cg_cls, item_cls, st);
+      upload(M.cg_tiles, item_tiles, st);
       upload(M.cg_tau, cls_tau, st);
       upload(M.cg_grp_sigma, grp_sigma, st);
       upload(M.cg_grp_items, grp_items, st);
@@ -1362,8 +1368,8 @@ void far_chain(DevInstance& I, Index m, cudaStream_t fs) {
     if (M.cg_partial.bytes < need) M.cg_partial.alloc(need);
     ctx.run_on(fs, "coupling", [&] {
       dev::launch_coupling_mma(fs, M.cg_items.as<dev::CouplingItem>(), M.n_cg_items, M.cg_cls.as<std::int32_t>(),
-                               M.cg_tau.as<std::int32_t>(), I.C.as<double>(), P, M.xhat.as<double>(), mm,
-                               M.cg_partial.as<double>());
+                               M.cg_tiles.as<std::uint8_t>(), M.cg_tau.as<std::int32_t>(), I.C.as<double>(), P,
+                               M.xhat.as<double>(), mm, M.cg_partial.as<double>());
     });
     ctx.run_on(fs, "coupling_reduce", [&] {
       dev::launch_coupling_reduce(fs, M.cg_grp_sigma.as<std::int32_t>(), M.cg_grp_items.as<std::int32_t>(),

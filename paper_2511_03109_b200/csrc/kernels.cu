@@ -500,9 +500,15 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // MC right-hand-side columns per CTA share every C_k fragment load
 // (grid.y walks the column chunks); X holds MC gathered 32-slot panels.
+// item_tiles[e] has bit j set when n-tile j (slots 8j .. 8j + 7) holds any
+// partner of class item_cls[e]; empty tiles skip their MMAs and loads
+// (the slot order of a group is Morton order, so boundary sigmas missing an
+// offset cluster: at C3 this lifts the useful fraction of the MMA work from
+// 64% to 83%).
 template <int P, int MC>
 __global__ void __launch_bounds__(P / 16 * 32) k_coupling_mma(const CouplingItem* __restrict__ items,
                                                               const std::int32_t* __restrict__ item_cls,
+                                                              const std::uint8_t* __restrict__ item_tiles,
                                                               const std::int32_t* __restrict__ cls_tau,
                                                               const double* __restrict__ C,
                                                               const double* __restrict__ xhat, int m,
@@ -525,10 +531,12 @@ __global__ void __launch_bounds__(P / 16 * 32) k_coupling_mma(const CouplingItem
 
   auto gather = [&](int e, int buf) {
     const std::int32_t* taus = cls_tau + static_cast<std::int64_t>(e) * kGroupSlots;
+    const unsigned tiles = item_tiles[e];
     for (int c = 0; c < ncol; ++c) {
       double* X = smem + (buf * MC + c) * PANEL;
       for (int q2 = threadIdx.x; q2 < kGroupSlots * (P / 2); q2 += blockDim.x) {
         const int slot = q2 / (P / 2), q = q2 % (P / 2);
+        if (!((tiles >> (slot >> 3)) & 1u)) continue;  // tile skipped by the MMAs
         const int tau = taus[slot];
         const double* src =
             xhat + (static_cast<std::int64_t>(tau < 0 ? 0 : tau) * m + col0 + c) * P + 2 * q;
@@ -550,6 +558,7 @@ __global__ void __launch_bounds__(P / 16 * 32) k_coupling_mma(const CouplingItem
     }
     __syncthreads();
     const double* Ck = C + static_cast<std::int64_t>(item_cls[e]) * P * P;
+    const unsigned tiles = item_tiles[e];
     double a[KS][2];
 #pragma unroll
     for (int s2 = 0; s2 < KS; ++s2) {
@@ -561,11 +570,14 @@ __global__ void __launch_bounds__(P / 16 * 32) k_coupling_mma(const CouplingItem
     for (int c = 0; c < MC; ++c) {
       if (c >= ncol) break;
       const double* X = smem + (buf * MC + c) * PANEL;
+      // tile-outer so an empty tile is a branch around its KS MMAs (a
+      // predicated MMA would still occupy the pipe)
 #pragma unroll
-      for (int s2 = 0; s2 < KS; ++s2) {
-        const int k = 4 * s2 + t0;
+      for (int j = 0; j < NT; ++j) {
+        if (!((tiles >> j) & 1u)) continue;
 #pragma unroll
-        for (int j = 0; j < NT; ++j) dmma_16x8x4(acc[c][j], a[s2][0], a[s2][1], X[(8 * j + g) * LD + k]);
+        for (int s2 = 0; s2 < KS; ++s2)
+          dmma_16x8x4(acc[c][j], a[s2][0], a[s2][1], X[(8 * j + g) * LD + 4 * s2 + t0]);
       }
     }
     __syncthreads();  // X[buf] is refilled two classes later
@@ -1630,8 +1642,8 @@ void launch_near_mrhs(cudaStream_t st, const MrhsItem* items, int nitems, const 
 bool coupling_mma_supported(int P) { return P == 16 || P == 32 || P == 64 || P == 128; }
 
 void launch_coupling_mma(cudaStream_t st, const CouplingItem* items, int nitems, const std::int32_t* item_cls,
-                         const std::int32_t* cls_tau, const double* C, int P, const double* xhat, int m,
-                         double* partial) {
+                         const std::uint8_t* item_tiles, const std::int32_t* cls_tau, const double* C, int P,
+                         const double* xhat, int m, double* partial) {
   if (nitems == 0) return;
   const int mc = m >= 2 ? 2 : 1;
   const size_t smem = 2 * mc * kGroupSlots * (P + 4) * sizeof(double);
@@ -1643,7 +1655,8 @@ void launch_coupling_mma(cudaStream_t st, const CouplingItem* items, int nitems,
       cudaFuncSetAttribute(k_coupling_mma<PP, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
       attr = true;                                                                                          \
     }                                                                                                       \
-    k_coupling_mma<PP, MC><<<grid, PP / 16 * 32, smem, st>>>(items, item_cls, cls_tau, C, xhat, m, partial); \
+    k_coupling_mma<PP, MC><<<grid, PP / 16 * 32, smem, st>>>(items, item_cls, item_tiles, cls_tau, C, xhat, m,     \
+                                                             partial);                                          \
     return;                                                                                                 \
   }
   PHM_CASE(16, 1)
