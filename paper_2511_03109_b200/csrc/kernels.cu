@@ -691,12 +691,17 @@ __global__ void __launch_bounds__(128) k_near_mrhs(const MrhsItem* __restrict__ 
     __syncthreads();
     const double* A = As[buf];
     const double* B = Bs[buf];
+    // only the k-steps this chunk holds, and only warps with rows: the
+    // zero-padded remainder of a block (n_tau mod 32) and of a short row
+    // slice costs no MMAs
+    const int ksteps = (min(kK9Kc, tn[b] - k0) + 3) >> 2;
+    if (16 * warp < it.rows) {
+      for (int s = 0; s < ksteps; ++s) {
+        const double a0 = A[(16 * warp + g) * LDA + 4 * s + t0];
+        const double a1 = A[(16 * warp + g + 8) * LDA + 4 * s + t0];
 #pragma unroll
-    for (int s = 0; s < kK9Kc / 4; ++s) {
-      const double a0 = A[(16 * warp + g) * LDA + 4 * s + t0];
-      const double a1 = A[(16 * warp + g + 8) * LDA + 4 * s + t0];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) dmma_16x8x4(acc[j], a0, a1, B[(4 * s + t0) * LDB + 8 * j + g]);
+        for (int j = 0; j < NT; ++j) dmma_16x8x4(acc[j], a0, a1, B[(4 * s + t0) * LDB + 8 * j + g]);
+      }
     }
     __syncthreads();
     b = nb;
