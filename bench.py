@@ -173,10 +173,12 @@ def measured_peak():
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_baseline(ph, c, pts, pm_host, steps, sample, seed):
+def cpu_baseline(ph, c, pts, pm_host, steps, sample, seed, m=1):
     """The oracle port of the reference's online path on this host's cores,
     on a bounded sample: every class, 1/sample of the near blocks and 1/sample
-    of the far blocks; per-theta time extrapolated to the full block lists."""
+    of the far blocks; per-theta time extrapolated to the full block lists.
+    m right-hand sides cost m applies (the reference's apply takes one
+    vector, phmatrix.hpp:95-100)."""
     from oracle import pyoracle as po
 
     cores = os.cpu_count() or 1
@@ -204,13 +206,13 @@ def cpu_baseline(ph, c, pts, pm_host, steps, sample, seed):
     for s in range(steps):
         inst, secs = om.instantiate_timed([thetas[s % len(thetas)]], near_mask)
         _, asecs = inst.apply_sample(x, near_mask, far_mask)
-        t = secs[0] + secs[1] / f_near + asecs[0] + asecs[1] / f_far + asecs[2] / f_near
+        t = secs[0] + secs[1] / f_near + m * (asecs[0] + asecs[1] / f_far + asecs[2] / f_near)
         per.append(t)
         del inst
     t = float(np.median(per))
     return {"value": 1.0 / t, "unit": "theta/s", "cores": cores, "kind": "port",
             "sample": f"instantiate over all {cnt['n_classes']} classes and 1/{sample} of the near blocks "
-                      f"({f_near:.4f} of near entries, {cores} threads); one MVM (single-threaded, as the reference) "
+                      f"({f_near:.4f} of near entries, {cores} threads); {m} MVM(s) (single-threaded, as the reference) "
                       f"over 1/{sample} of the far and near blocks + full basis passes; extrapolated per theta, "
                       f"median of {steps} thetas"}
 
@@ -402,9 +404,9 @@ def run_ours(args):
                "h2d_bytes_per_step": tb * (8 * n * m + 8), "d2h_bytes_per_step": tb * 8 * n * m}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and c["fmt"] == "h2" and m == 1:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and c["fmt"] == "h2":
         host_pm = ph.offline_structure(pts, make_cfg(ph, c))
-        cpu = cpu_baseline(ph, c, pts, host_pm, 3, args.cpu_sample, args.seed)
+        cpu = cpu_baseline(ph, c, pts, host_pm, 3, args.cpu_sample, args.seed, m)
 
     if rank == 0:
         peak, peak_kind = measured_peak()
@@ -441,12 +443,7 @@ def run_ours(args):
             if cp else None,
             "near_mrhs_tflops": (2.0 * info["near_entries"] * m / (k9["ms_per_launch"] * 1e-3) / 1e12) if k9 else None,
         }
-        where = "n=2^%d, %dD" % (n.bit_length() - 1, c["d"]) if n & (n - 1) == 0 else "n=%d, %dD" % (n, c["d"])
-        fmt_name = "H2" if c["fmt"] == "h2" else "H"
-        what = ("theta/s (instantiate + %d-RHS %s MVM per theta) at %s, theta sweep sharded over GPUs"
-                % (m, fmt_name, where) if sweep else
-                "theta-instantiations/s (instantiate + %s MVM per theta) at %s" % (fmt_name, where) if m == 1 else
-                "theta/s (instantiate + %d-RHS %s MVM per theta) at %s" % (m, fmt_name, where))
+        what, config = describe(args, c, m, tb, world)
         line = {
             "metric": what,
             "value": (world if sweep else 1) * tb * args.steps * 1000.0 / ms,
@@ -461,11 +458,7 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded uniform points, harness theta draws, x~N(0,1))",
-            "config": {"workload": f"{args.config}: n={n} d={c['d']} {c['fmt']} kernel={c['family']} "
-                                   f"l_max={c['l_max']} p_s={c['p_s']} p_theta={c['p_theta']} eta={c['eta']} "
-                                   f"near=snapshot rhs={m}" + (f" theta_batch={tb}" if tb > 1 else ""),
-                       "parallelism": ("theta-sharded replicas" if sweep else f"rows sharded over {world}"),
-                       "l2": "inputs (near snapshots) larger than L2; no flush needed"},
+            "config": config,
             "roofline": {"bound": "hbm", "kernel": k1_desc, "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg},
@@ -493,6 +486,24 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def describe(args, c, m, tb, world):
+    """The metric name and config dict both arms print (same workload)."""
+    n = c["n"]
+    sweep = c.get("sweep", False)
+    where = "n=2^%d, %dD" % (n.bit_length() - 1, c["d"]) if n & (n - 1) == 0 else "n=%d, %dD" % (n, c["d"])
+    fmt_name = "H2" if c["fmt"] == "h2" else "H"
+    what = ("theta/s (instantiate + %d-RHS %s MVM per theta) at %s, theta sweep sharded over GPUs"
+            % (m, fmt_name, where) if sweep else
+            "theta-instantiations/s (instantiate + %s MVM per theta) at %s" % (fmt_name, where) if m == 1 else
+            "theta/s (instantiate + %d-RHS %s MVM per theta) at %s" % (m, fmt_name, where))
+    config = {"workload": f"{args.config}: n={n} d={c['d']} {c['fmt']} kernel={c['family']} "
+                          f"l_max={c['l_max']} p_s={c['p_s']} p_theta={c['p_theta']} eta={c['eta']} "
+                          f"near=snapshot rhs={m}" + (f" theta_batch={tb}" if tb > 1 else ""),
+              "parallelism": ("theta-sharded replicas" if sweep else f"rows sharded over {world}"),
+              "l2": "inputs (near snapshots) larger than L2; no flush needed"}
+    return what, config
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -504,13 +515,19 @@ def run_reference(args):
     pts = make_points(ph, c, args.seed)
     host_pm = ph.offline_structure(pts, make_cfg(ph, c))
     steps = max(1, args.steps)
-    cpu = cpu_baseline(ph, c, pts, host_pm, steps, args.cpu_sample, args.seed)
+    m = args.rhs or c.get("rhs", 1)
+    cpu = cpu_baseline(ph, c, pts, host_pm, steps, args.cpu_sample, args.seed, m)
+    tb = (args.theta_batch or c.get("theta_batch", 1)) if c.get("sweep", False) else 1
+    what, config = describe(args, c, m, tb, world)
+    config["parallelism"] = "reference CPU path on the host cores of rank 0"
     line = {
         "impl": "reference",
-        "metric": "theta-instantiations/s (instantiate + H2 MVM per theta) at n=2^18, 3D",
+        "metric": what,
         "value": cpu["value"], "unit": "theta/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 / cpu["value"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": {"workload": args.config},
+        "ms_per_step": 1000.0 / cpu["value"], "higher_is_better": True,
+        "scaling": "weak" if c.get("sweep", False) else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded uniform points, harness theta draws, x~N(0,1))",
+        "config": config,
         "cpu_baseline": cpu,
         "e2e": {"value": cpu["value"], "unit": "theta/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
