@@ -35,7 +35,7 @@ void launch_near_w(cudaStream_t, const NearW*, std::int64_t, const double*, cons
                    double*);
 void launch_set_vec(cudaStream_t, double*, int, const ThetaV&, double);
 void launch_class_inst(cudaStream_t, const ClassMeta*, int, const double*, const std::int32_t*, const double*,
-                       const double*, const ThetaV&, int, bool, int, int, int, double*, double*);
+                       const double*, const ThetaV&, int, bool, int, int, int, int, double*, double*);
 void launch_gather(cudaStream_t, const double*, const std::int32_t*, std::int64_t, std::int64_t, double*);
 void launch_scatter(cudaStream_t, const double*, const std::int32_t*, std::int64_t, std::int64_t, double*);
 void launch_leaf_fwd(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*, const double*,
@@ -297,7 +297,7 @@ struct DevMatrix {
   bool baseline = false;  // fixed far field (H-ACA / H^2-HCA at one theta)
   DBuf fixed_H, fixed_C;
   std::int64_t H_len = 0, C_len = 0;
-  int capA = 0, capB = 0, capT = 0;
+  int capA = 0, capB = 0, capT = 0, capL = 0;
   // H^2 coupling CSR by sigma node
   DBuf cp_sig, cp_beg, cp_tau, cp_cls;
   int n_cp_sig = 0;
@@ -713,12 +713,22 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     std::vector<dev::SymBlock> blocks;
     std::vector<std::vector<dev::GatherSeg>> segs_of(M.nnodes);
     std::int64_t poff = 0;
+    // Enough items for ~8 waves of two CTAs per SM: a row shard (few leaves)
+    // splits each leaf's blocks over several items, so the near pass does
+    // not end on a partial wave of long CTAs; the unsharded C3 keeps one
+    // item per leaf.
+    std::size_t kItemBlocks = 128;
+    {
+      std::size_t total = 0;
+      for (const auto& o : owned) total += o.size();
+      const std::size_t target = 8 * 2 * 148;
+      kItemBlocks = std::min<std::size_t>(128, std::max<std::size_t>(8, (total + target - 1) / target));
+    }
     for (int s = 0; s < M.nnodes; ++s) {
       if (owned[s].empty()) continue;
       const int ns = static_cast<int>(T.nodes[s].count);
       // items: 128-row slices of the leaf x runs of at most kItemBlocks owned
       // blocks (the TMA pass caches an item's block list in shared memory)
-      constexpr std::size_t kItemBlocks = 128;
       for (int i0 = 0; i0 < ns; i0 += 128)
       for (std::size_t q0 = 0; q0 < owned[s].size(); q0 += kItemBlocks) {
         dev::SymRowItem it{};
@@ -873,7 +883,11 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     M.capA = std::max(maxA, maxrl * maxs1);
     M.capB = maxB;
     M.capT = std::max(maxrl * 32, maxrl * maxs1);
-    PHM_CHECK((M.capA + M.capB + M.capT) * 8 <= 227 * 1024, "class instantiate shared memory over 227 KB");
+    if (M.h2 && M.P == 64) {  // register-tiled C = L (H R^T): T (rl x 64) and L (64 x rl) staged
+      M.capT = std::max(M.capT, maxrl * 64);
+      M.capL = 64 * maxrl;
+    }
+    PHM_CHECK((M.capA + M.capB + M.capT + M.capL) * 8 <= 227 * 1024, "class instantiate shared memory over 227 KB");
     M.H_len = hoff;
     M.C_len = M.h2 ? static_cast<std::int64_t>(M.ncls) * M.P * M.P : 0;
     upload(M.cmeta, M.cmeta_h, st);
@@ -1084,7 +1098,7 @@ void inst_classes(DevInstance& I, const dev::ThetaV& tv, cudaStream_t s) {
   M.ctx->run_on(s, "class_inst", [&] {
     dev::launch_class_inst(s, M.cmeta.as<dev::ClassMeta>(), M.ncls, M.class_mid.as<double>(),
                            M.class_mid_dims.as<std::int32_t>(), M.class_L.as<double>(), M.class_R.as<double>(), tv, M.P,
-                           M.h2, M.capA, M.capB, M.capT, I.H.as<double>(), I.C.as<double>());
+                           M.h2, M.capA, M.capB, M.capT, M.capL, I.H.as<double>(), I.C.as<double>());
   });
 }
 

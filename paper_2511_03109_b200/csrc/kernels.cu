@@ -303,7 +303,7 @@ __global__ void k_scale(double* x, std::int64_t n, double a) {
 __global__ void k_class_inst(const ClassMeta* __restrict__ meta, int ncls, const double* __restrict__ mid,
                              const std::int32_t* __restrict__ mid_dims, const double* __restrict__ Lm,
                              const double* __restrict__ Rm, ThetaV tv, int P, int want_c, int capA, int capB,
-                             double* __restrict__ H, double* __restrict__ C) {
+                             int capT, double* __restrict__ H, double* __restrict__ C) {
   extern __shared__ double sm[];
   const ClassMeta M = meta[blockIdx.x];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -352,6 +352,46 @@ __global__ void k_class_inst(const ClassMeta* __restrict__ meta, int ncls, const
   __syncthreads();
   for (int e = tid; e < rl * rr; e += nt) H[M.h_off + e] = A[e];
   if (!want_c) return;
+  if (P == 64 && nt == 256) {
+    // C = L (H R^T) register-tiled: T = H R^T (rl x 64) into shared memory,
+    // L staged (64 x rl), then thread (a4, b4) accumulates the 4 x 4 tile
+    // rows a4 + 16 q, columns b4 + 16 q' over i < rl (conflict-free reads:
+    // consecutive a4 hit consecutive banks, b4 is a broadcast per half-warp).
+    double* Ts = Tt;             // rl x 64, column-major (ld rl)
+    double* Ls = Tt + capT;      // 64 x rl, column-major (ld 64)
+    for (int e = tid; e < rl * 64; e += nt) {
+      const int i = e % rl, b = e / rl;
+      double t = 0.0;
+      for (int c = 0; c < rr; ++c) t += A[i + c * rl] * Rm[M.r_off + b + static_cast<std::int64_t>(c) * 64];
+      Ts[e] = t;
+    }
+    for (int e = tid; e < 64 * rl; e += nt) Ls[e] = Lm[M.l_off + e];
+    __syncthreads();
+    const int a4 = tid & 15, b4 = tid >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int r2 = 0; r2 < 4; ++r2) acc[q][r2] = 0.0;
+    for (int i = 0; i < rl; ++i) {
+      double l[4], t[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        l[q] = Ls[a4 + 16 * q + i * 64];
+        t[q] = Ts[i + (b4 + 16 * q) * rl];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r2 = 0; r2 < 4; ++r2) acc[q][r2] += l[q] * t[r2];
+    }
+#pragma unroll
+    for (int r2 = 0; r2 < 4; ++r2)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        C[M.c_off + (a4 + 16 * q) + static_cast<std::int64_t>(b4 + 16 * r2) * 64] = acc[q][r2];
+    return;
+  }
   for (int b0 = 0; b0 < P; b0 += 32) {
     const int bw = min(32, P - b0);
     __syncthreads();
@@ -1491,15 +1531,15 @@ void launch_set_vec(cudaStream_t st, double* dst, int n, const ThetaV& tv, doubl
 
 void launch_class_inst(cudaStream_t st, const ClassMeta* meta, int ncls, const double* mid, const std::int32_t* dims,
                        const double* L, const double* R, const ThetaV& tv, int P, bool want_c, int capA, int capB,
-                       int capT, double* H, double* C) {
+                       int capT, int capL, double* H, double* C) {
   if (ncls == 0) return;
-  const size_t smem = static_cast<size_t>(capA + capB + capT) * sizeof(double);
+  const size_t smem = static_cast<size_t>(capA + capB + capT + capL) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_class_inst, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  k_class_inst<<<ncls, 256, smem, st>>>(meta, ncls, mid, dims, L, R, tv, P, want_c ? 1 : 0, capA, capB, H, C);
+  k_class_inst<<<ncls, 256, smem, st>>>(meta, ncls, mid, dims, L, R, tv, P, want_c ? 1 : 0, capA, capB, capT, H, C);
 }
 
 void launch_gather(cudaStream_t st, const double* x, const std::int32_t* perm, std::int64_t n, std::int64_t m,
