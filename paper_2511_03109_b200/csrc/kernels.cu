@@ -6,6 +6,9 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "kernels.cuh"
 
@@ -1516,6 +1519,22 @@ void launch_inst_tiles(cudaStream_t st, const InstTile* tiles, std::int64_t nt, 
   if (grid > 0) k_inst_tiles<<<grid, 256, 0, st>>>(tiles, nt, G, w, D);
 }
 
+namespace {
+// cudaFuncSetAttribute once per (kernel, device, size): the attributes live
+// in each device's context, and launches may come from several host threads.
+void smem_attr(const void* fn, int bytes, bool max_carveout) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!done.insert(std::make_tuple(fn, dev, bytes)).second) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (max_carveout)
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+}  // namespace
+
 void launch_near_w(cudaStream_t st, const NearW* meta, std::int64_t nb, const double* cores, const std::int32_t* dims,
                    const ThetaV& tv, double* w) {
   if (nb == 0) return;
@@ -1529,16 +1548,13 @@ void launch_set_vec(cudaStream_t st, double* dst, int n, const ThetaV& tv, doubl
   if (amp != 1.0) k_scale<<<(n + 127) / 128, 128, 0, st>>>(dst, n, amp);
 }
 
+
 void launch_class_inst(cudaStream_t st, const ClassMeta* meta, int ncls, const double* mid, const std::int32_t* dims,
                        const double* L, const double* R, const ThetaV& tv, int P, bool want_c, int capA, int capB,
                        int capT, int capL, double* H, double* C) {
   if (ncls == 0) return;
   const size_t smem = static_cast<size_t>(capA + capB + capT + capL) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_class_inst, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  smem_attr(reinterpret_cast<const void*>(k_class_inst), 227 * 1024, false);
   k_class_inst<<<ncls, 256, smem, st>>>(meta, ncls, mid, dims, L, R, tv, P, want_c ? 1 : 0, capA, capB, capT, H, C);
 }
 
@@ -1560,6 +1576,7 @@ void launch_leaf_fwd(cudaStream_t st, const std::int32_t* leaves, int nleaves, c
                      int m, double* xhat) {
   if (nleaves == 0) return;
   const size_t smem = (64 * d * ps + 64) * sizeof(double);
+  if (smem > 48 * 1024) smem_attr(reinterpret_cast<const void*>(k_leaf_fwd), static_cast<int>(smem), false);
   k_leaf_fwd<<<dim3(nleaves, m), threads_for(P), smem, st>>>(leaves, begin, count, U, n, d, ps, P, xp, m, xhat);
 }
 void launch_up(cudaStream_t st, const std::int32_t* nodes, int cnt, const std::int32_t* first_child,
@@ -1567,6 +1584,7 @@ void launch_up(cudaStream_t st, const std::int32_t* nodes, int cnt, const std::i
   if (cnt == 0) return;
   const int nc = 1 << d;
   const size_t smem = (d * ps * ps + 3 * P) * sizeof(double);
+  if (smem > 48 * 1024) smem_attr(reinterpret_cast<const void*>(k_up2), static_cast<int>(smem), false);
   k_up2<<<dim3(cnt, m), threads_for(P), smem, st>>>(nodes, first_child, count, E, d, ps, P, nc, m, xhat);
 }
 void launch_coupling(cudaStream_t st, const std::int32_t* sig, int nsig, const std::int64_t* fbeg,
@@ -1581,14 +1599,7 @@ void launch_near_tma_apply(cudaStream_t st, const SymRowItem* items, int nitems,
   // 3 stages of 24 KB (48 columns of a 64-row leaf): two CTAs per SM
   constexpr int CH = 3072, NST = 3;
   const size_t smem = static_cast<size_t>(NST * (CH + 2 + 66) + 8 * 128) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_near_tma_apply<CH, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    cudaFuncSetAttribute(k_near_tma_apply<CH, NST>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    attr = true;
-  }
+  smem_attr(reinterpret_cast<const void*>(k_near_tma_apply<CH, NST>), static_cast<int>(smem), true);
   static const int per_sm = [] {
     const char* e = std::getenv("PHM_NEAR_CTAS_PER_SM");
     const int k = e ? std::atoi(e) : 2;
@@ -1616,14 +1627,7 @@ bool launch_near_inst_tma(cudaStream_t st, const SymRowItem* items, int nitems, 
   {                                                                                                           \
     constexpr int CHc = CHv;                                                                                  \
     const size_t smem = static_cast<size_t>(tma_smem_doubles(RR, CHc, NST)) * sizeof(double);                \
-    static bool attr = false;                                                                                 \
-    if (!attr) {                                                                                              \
-      cudaFuncSetAttribute(k_near_tma<RR, CHc, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
-                           static_cast<int>(smem));                                                          \
-      cudaFuncSetAttribute(k_near_tma<RR, CHc, NST>, cudaFuncAttributePreferredSharedMemoryCarveout,          \
-                           cudaSharedmemCarveoutMaxShared);                                                  \
-      attr = true;                                                                                            \
-    }                                                                                                         \
+    smem_attr(reinterpret_cast<const void*>(k_near_tma<RR, CHc, NST>), static_cast<int>(smem), true);       \
     k_near_tma<RR, CHc, NST><<<nitems, kTmaThreads, smem, st>>>(items, blocks, G, E, w, D, xp, part);                 \
     return true;                                                                                              \
   }
@@ -1668,11 +1672,7 @@ void launch_near_mrhs(cudaStream_t st, const MrhsItem* items, int nitems, const 
 #define PHM_K9(NC)                                                                                          \
   {                                                                                                         \
     const size_t smem = 2 * (kK9Rows * (kK9Kc + 4) + kK9Kc * (NC + 4)) * sizeof(double);                   \
-    static bool attr = false;                                                                               \
-    if (!attr) {                                                                                            \
-      cudaFuncSetAttribute(k_near_mrhs<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);        \
-      attr = true;                                                                                          \
-    }                                                                                                       \
+    smem_attr(reinterpret_cast<const void*>(k_near_mrhs<NC>), 96 * 1024, false);                           \
     const dim3 grid(static_cast<unsigned>(nitems), static_cast<unsigned>((m + NC - 1) / NC));               \
     k_near_mrhs<NC><<<grid, 128, smem, st>>>(items, tb, tn, doff, ld, tr, D, X, n, m, Y);                   \
     return;                                                                                                 \
@@ -1695,11 +1695,7 @@ void launch_coupling_mma(cudaStream_t st, const CouplingItem* items, int nitems,
   const dim3 grid(static_cast<unsigned>(nitems), static_cast<unsigned>((m + mc - 1) / mc));
 #define PHM_CASE(PP, MC)                                                                                    \
   if (P == PP && mc == MC) {                                                                                \
-    static bool attr = false;                                                                               \
-    if (!attr) {                                                                                            \
-      cudaFuncSetAttribute(k_coupling_mma<PP, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-      attr = true;                                                                                          \
-    }                                                                                                       \
+    smem_attr(reinterpret_cast<const void*>(k_coupling_mma<PP, MC>), 200 * 1024, false);                   \
     k_coupling_mma<PP, MC><<<grid, PP / 16 * 32, smem, st>>>(items, item_cls, item_tiles, cls_tau, C, xhat, m,     \
                                                              partial);                                          \
     return;                                                                                                 \
@@ -1726,6 +1722,7 @@ void launch_down(cudaStream_t st, const std::int32_t* nodes, int cnt, const std:
                  int d, int ps, int P, int m, double* yhat) {
   if (cnt == 0) return;
   const size_t smem = (d * ps * ps + 3 * P) * sizeof(double);
+  if (smem > 48 * 1024) smem_attr(reinterpret_cast<const void*>(k_down2), static_cast<int>(smem), false);
   k_down2<<<dim3(cnt, m), threads_for(P), smem, st>>>(nodes, parent, E, d, ps, P, m, yhat);
 }
 void launch_leaf_bwd(cudaStream_t st, const std::int32_t* leaves, int nleaves, const std::int64_t* begin,
@@ -1733,6 +1730,7 @@ void launch_leaf_bwd(cudaStream_t st, const std::int32_t* leaves, int nleaves, c
                      const double* yhat, int m, std::int64_t row_lo, std::int64_t row_hi, double* yp) {
   if (nleaves == 0) return;
   const size_t smem = (P + 2 * 32 * (P / ps)) * sizeof(double);
+  if (smem > 48 * 1024) smem_attr(reinterpret_cast<const void*>(k_leaf_bwd2), static_cast<int>(smem), false);
   k_leaf_bwd2<<<dim3(nleaves, m), 128, smem, st>>>(leaves, begin, count, U, n, d, ps, P, yhat, m, row_lo, row_hi, yp);
 }
 void launch_far_h(cudaStream_t st, const FarHItem* items, int nitems, int max_rows, const std::int64_t* tbeg,
@@ -1741,6 +1739,7 @@ void launch_far_h(cudaStream_t st, const FarHItem* items, int nitems, int max_ro
                   const double* xp, std::int64_t row_lo, std::int64_t row_hi, double* yp) {
   if (nitems == 0) return;
   const size_t smem = (max_rows + 256) * sizeof(double);
+  if (smem > 48 * 1024) smem_attr(reinterpret_cast<const void*>(k_far_h), static_cast<int>(smem), false);
   k_far_h<<<nitems, 128, smem, st>>>(items, tbeg, tcnt, cls, s_off, t_off, meta, S, T, H, xp, row_lo, row_hi, yp);
 }
 

@@ -453,3 +453,17 @@ def test_theta_batched_instantiate(ph, po, mode):
     assert np.array_equal(insts[1].apply(x), ph.instantiate(pm, [0.2]).apply(x))
     with pytest.raises(ph.DomainError):
         ph.instantiate_batch(pm, [[0.2], [0.9]])
+
+
+def test_h_form_far_blocks_beyond_48kb_shared(ph, po):
+    """H form whose coarsest far blocks have > 6,000 rows: k_far_h stages the
+    sigma rows in more than 48 KB of shared memory (opt-in attribute)."""
+    pts = ph.generate_points(24000, 1, 5)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=5, p_s=8, p_theta=6, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H)
+    ints, _ = pm.nodes()
+    _, far, _ = pm.blocks()
+    assert max(int(ints[s, 3]) for s, _ in far) > 6000
+    x = ph.generate_normal(24000, 9)
+    assert rel(ph.instantiate(pm, [0.2]).apply(x), om.instantiate([0.2]).apply(x)) <= TOL_Y
