@@ -1605,8 +1605,9 @@ void launch_near_tma_apply(cudaStream_t st, const SymRowItem* items, int nitems,
     const int k = e ? std::atoi(e) : 2;
     return k >= 1 && k <= 2 ? k : 2;
   }();
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaMemsetAsync(counter, 0, sizeof(int), st);
   const int grid = std::min(nitems, sms * per_sm);
   k_near_tma_apply<CH, NST><<<grid, kTmaThreads, smem, st>>>(items, nitems, blocks, D, xp, part, counter);
