@@ -66,9 +66,10 @@ void launch_down(cudaStream_t, const std::int32_t*, int, const std::int32_t*, co
                  double*);
 void launch_leaf_bwd(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*, const double*,
                      std::int64_t, int, int, int, const double*, int, std::int64_t, std::int64_t, double*);
-void launch_far_h(cudaStream_t, const FarHItem*, int, int, const std::int64_t*, const std::int32_t*,
-                  const std::int32_t*, const std::int64_t*, const std::int64_t*, const ClassMeta*, const double*,
-                  const double*, const double*, const double*, std::int64_t, std::int64_t, double*);
+void launch_far_h(cudaStream_t, const FarHItem*, int, int, const std::int32_t*, int, int, const std::int64_t*,
+                  const std::int32_t*, const std::int32_t*, const std::int64_t*, const std::int64_t*,
+                  const std::int64_t*, const ClassMeta*, const double*, const double*, const double*, const double*,
+                  double*, std::int64_t, std::int64_t, double*);
 }  // namespace dev
 
 // ---------------------------------------------------------------- buffers
@@ -306,9 +307,9 @@ struct DevMatrix {
   DBuf cg_items, cg_cls, cg_tiles, cg_tau, cg_grp_sigma, cg_grp_items, cg_partial;
   int n_cg_items = 0, n_cg_groups = 0;
   // H form far CSR by level
-  DBuf fh_items, fh_tb, fh_tn, fh_cls, fh_soff, fh_toff, fh_S, fh_T;
+  DBuf fh_items, fh_tb, fh_tn, fh_cls, fh_soff, fh_toff, fh_S, fh_T, fh_bitem, fh_poff, fh_part;
+  std::vector<dev::FarHItem> fh_items_h;
   std::vector<std::pair<int, int>> fh_level_range;  // [item begin, item end) per level
-  std::vector<int> fh_level_maxrows;
   // basis
   DBuf U, Etr;
   DBuf leaves_all, leaves_local;
@@ -1035,11 +1036,11 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
   } else {
     // H form: far blocks grouped per level, CSR by sigma, S/T payloads
     std::vector<dev::FarHItem> items;
-    std::vector<std::int64_t> tb, soff, toff;
-    std::vector<std::int32_t> tn, cls;
+    std::vector<std::int64_t> tb, soff, toff, poff;
+    std::vector<std::int32_t> tn, cls, bitem;
     std::vector<double> S, Tm;
+    std::int64_t pnext = 0;  // per-block partial segments (n_sigma each)
     M.fh_level_range.assign(T.l_max + 1, {0, 0});
-    M.fh_level_maxrows.assign(T.l_max + 1, 0);
     for (int l = 0; l <= T.l_max; ++l) {
       std::map<int, std::vector<Index>> by_sigma;
       for (Index i = 0; i < static_cast<Index>(H.blocks.far.size()); ++i)
@@ -1062,13 +1063,20 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
           Tm.insert(Tm.end(), H.far_t[i].a.begin(), H.far_t[i].a.end());
         }
         it.bend = static_cast<std::int32_t>(tb.size());
-        M.fh_level_maxrows[l] = std::max<int>(M.fh_level_maxrows[l], it.rows);
+        for (int q = it.bbeg; q < it.bend; ++q) {
+          bitem.push_back(static_cast<std::int32_t>(items.size()));
+          poff.push_back(pnext);
+          pnext += it.rows;
+        }
         items.push_back(it);
       }
       M.fh_level_range[l].second = static_cast<int>(items.size());
-      PHM_CHECK((M.fh_level_maxrows[l] + 256) * 8 <= 200 * 1024, "H-form far block rows exceed shared memory");
     }
+    upload(M.fh_bitem, bitem, st);
+    upload(M.fh_poff, poff, st);
+    M.fh_part.alloc(sizeof(double) * std::max<std::int64_t>(pnext, 1));
     upload(M.fh_items, items, st);
+    M.fh_items_h = items;
     upload(M.fh_tb, tb, st);
     upload(M.fh_tn, tn, st);
     upload(M.fh_cls, cls, st);
@@ -1473,13 +1481,15 @@ void far_finish(DevInstance& I, Index m, cudaStream_t st) {
   for (int l = 0; l <= H.tree->l_max; ++l) {
     const auto r = M.fh_level_range[l];
     if (r.second == r.first) continue;
+    const int b0 = M.fh_items_h[r.first].bbeg, b1 = M.fh_items_h[r.second - 1].bend;
     for (Index c = 0; c < m; ++c)
       ctx.run_on(st, "far_h", [&] {
-        dev::launch_far_h(st, M.fh_items.as<dev::FarHItem>() + r.first, r.second - r.first, M.fh_level_maxrows[l],
-                          M.fh_tb.as<std::int64_t>(), M.fh_tn.as<std::int32_t>(), M.fh_cls.as<std::int32_t>(),
-                          M.fh_soff.as<std::int64_t>(), M.fh_toff.as<std::int64_t>(), M.cmeta.as<dev::ClassMeta>(),
+        dev::launch_far_h(st, M.fh_items.as<dev::FarHItem>(), r.first, r.second - r.first,
+                          M.fh_bitem.as<std::int32_t>(), b0, b1 - b0, M.fh_tb.as<std::int64_t>(),
+                          M.fh_tn.as<std::int32_t>(), M.fh_cls.as<std::int32_t>(), M.fh_soff.as<std::int64_t>(),
+                          M.fh_toff.as<std::int64_t>(), M.fh_poff.as<std::int64_t>(), M.cmeta.as<dev::ClassMeta>(),
                           M.fh_S.as<double>(), M.fh_T.as<double>(), I.H.as<double>(), M.xp.as<double>() + c * M.n,
-                          H.row_begin, H.row_end, M.yp.as<double>() + c * M.n);
+                          M.fh_part.as<double>(), H.row_begin, H.row_end, M.yp.as<double>() + c * M.n);
       });
   }
 }

@@ -1214,51 +1214,62 @@ __global__ void k_near_gather(const std::int64_t* __restrict__ leaf_row0, const 
 }
 
 
-// ----------------------------------------------------------------- K8
-// H form: y_sigma += S_b (H_k (T_b^T x_tau)) for the far blocks of sigma at
-// one level (phmatrix.cpp:231-237). One CTA per sigma; rows clipped to the
-// local shard.
-__global__ void k_far_h(const FarHItem* __restrict__ items, const std::int64_t* __restrict__ tbeg,
-                        const std::int32_t* __restrict__ tcnt, const std::int32_t* __restrict__ cls,
-                        const std::int64_t* __restrict__ s_off, const std::int64_t* __restrict__ t_off,
-                        const ClassMeta* __restrict__ meta, const double* __restrict__ S, const double* __restrict__ T,
-                        const double* __restrict__ H, const double* __restrict__ xp, std::int64_t row_lo,
-                        std::int64_t row_hi, double* __restrict__ yp) {
-  extern __shared__ double sm[];
-  const FarHItem it = items[blockIdx.x];
-  double* acc = sm;               // rows
-  double* tv = acc + it.rows;     // <= 128
-  double* uv = tv + 128;          // <= 128
-  for (int i = threadIdx.x; i < it.rows; i += blockDim.x) acc[i] = 0.0;
-  for (int b = it.bbeg; b < it.bend; ++b) {
-    const ClassMeta M = meta[cls[b]];
-    const int rl = M.rl, rr = M.rr, nt = tcnt[b];
-    const double* Tb = T + t_off[b];
-    const double* Sb = S + s_off[b];
-    const double* xb = xp + tbeg[b];
-    __syncthreads();
-    for (int c = threadIdx.x; c < rr; c += blockDim.x) {
-      double s = 0.0;
-      for (int j = 0; j < nt; ++j) s += Tb[j + static_cast<std::int64_t>(c) * nt] * xb[j];
-      tv[c] = s;
-    }
-    __syncthreads();
-    for (int a = threadIdx.x; a < rl; a += blockDim.x) {
-      double s = 0.0;
-      for (int c = 0; c < rr; ++c) s += H[M.h_off + a + static_cast<std::int64_t>(c) * rl] * tv[c];
-      uv[a] = s;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < it.rows; i += blockDim.x) {
-      double s = 0.0;
-      for (int a = 0; a < rl; ++a) s += Sb[i + static_cast<std::int64_t>(a) * it.rows] * uv[a];
-      acc[i] += s;
-    }
+// K8, H form: y_sigma += S_b (H_k (T_b^T x_tau)) per far block (one CTA per
+// block: the T^T x reduction is split over the warps, H and S products over
+// the threads), written to the block's partial segment; k_far_h_reduce then
+// sums each sigma's segments in block order (deterministic, no atomics).
+__global__ void __launch_bounds__(128) k_far_h_blocks(const FarHItem* __restrict__ items,
+                                                      const std::int32_t* __restrict__ bitem,
+                                                      const std::int64_t* __restrict__ tbeg,
+                                                      const std::int32_t* __restrict__ tcnt,
+                                                      const std::int32_t* __restrict__ cls,
+                                                      const std::int64_t* __restrict__ s_off,
+                                                      const std::int64_t* __restrict__ t_off,
+                                                      const std::int64_t* __restrict__ p_off,
+                                                      const ClassMeta* __restrict__ meta, const double* __restrict__ S,
+                                                      const double* __restrict__ T, const double* __restrict__ H,
+                                                      const double* __restrict__ xp, int b0,
+                                                      double* __restrict__ part) {
+  __shared__ double tv[128], uv[128];
+  const int b = b0 + blockIdx.x;
+  const FarHItem it = items[bitem[b]];
+  const ClassMeta M = meta[cls[b]];
+  const int rl = M.rl, rr = M.rr, nt = tcnt[b];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* Tb = T + t_off[b];
+  const double* Sb = S + s_off[b];
+  const double* xb = xp + tbeg[b];
+  for (int c = warp; c < rr; c += 4) {  // tv = T^T x_tau
+    double s = 0.0;
+    for (int j = lane; j < nt; j += 32) s += Tb[j + static_cast<std::int64_t>(c) * nt] * xb[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) tv[c] = s;
   }
   __syncthreads();
+  for (int a = threadIdx.x; a < rl; a += blockDim.x) {  // uv = H tv
+    double s = 0.0;
+    for (int c = 0; c < rr; ++c) s += H[M.h_off + a + static_cast<std::int64_t>(c) * rl] * tv[c];
+    uv[a] = s;
+  }
+  __syncthreads();
+  double* out = part + p_off[b];
+  for (int i = threadIdx.x; i < it.rows; i += blockDim.x) {  // S uv
+    double s = 0.0;
+    for (int a = 0; a < rl; ++a) s += Sb[i + static_cast<std::int64_t>(a) * it.rows] * uv[a];
+    out[i] = s;
+  }
+}
+
+__global__ void k_far_h_reduce(const FarHItem* __restrict__ items, const std::int64_t* __restrict__ p_off,
+                               const double* __restrict__ part, std::int64_t row_lo, std::int64_t row_hi,
+                               double* __restrict__ yp) {
+  const FarHItem it = items[blockIdx.x];
   for (int i = threadIdx.x; i < it.rows; i += blockDim.x) {
+    double s = 0.0;
+    for (int b = it.bbeg; b < it.bend; ++b) s += part[p_off[b] + i];
     const std::int64_t pos = it.row0 + i;
-    if (pos >= row_lo && pos < row_hi) yp[pos] += acc[i];
+    if (pos >= row_lo && pos < row_hi) yp[pos] += s;
   }
 }
 
@@ -1734,14 +1745,15 @@ void launch_leaf_bwd(cudaStream_t st, const std::int32_t* leaves, int nleaves, c
   if (smem > 48 * 1024) smem_attr(reinterpret_cast<const void*>(k_leaf_bwd2), static_cast<int>(smem), false);
   k_leaf_bwd2<<<dim3(nleaves, m), 128, smem, st>>>(leaves, begin, count, U, n, d, ps, P, yhat, m, row_lo, row_hi, yp);
 }
-void launch_far_h(cudaStream_t st, const FarHItem* items, int nitems, int max_rows, const std::int64_t* tbeg,
-                  const std::int32_t* tcnt, const std::int32_t* cls, const std::int64_t* s_off,
-                  const std::int64_t* t_off, const ClassMeta* meta, const double* S, const double* T, const double* H,
-                  const double* xp, std::int64_t row_lo, std::int64_t row_hi, double* yp) {
-  if (nitems == 0) return;
-  const size_t smem = (max_rows + 256) * sizeof(double);
-  if (smem > 48 * 1024) smem_attr(reinterpret_cast<const void*>(k_far_h), static_cast<int>(smem), false);
-  k_far_h<<<nitems, 128, smem, st>>>(items, tbeg, tcnt, cls, s_off, t_off, meta, S, T, H, xp, row_lo, row_hi, yp);
+void launch_far_h(cudaStream_t st, const FarHItem* items, int item0, int nitems, const std::int32_t* bitem, int b0,
+                  int nblocks, const std::int64_t* tbeg, const std::int32_t* tcnt, const std::int32_t* cls,
+                  const std::int64_t* s_off, const std::int64_t* t_off, const std::int64_t* p_off,
+                  const ClassMeta* meta, const double* S, const double* T, const double* H, const double* xp,
+                  double* part, std::int64_t row_lo, std::int64_t row_hi, double* yp) {
+  if (nitems == 0 || nblocks == 0) return;
+  k_far_h_blocks<<<nblocks, 128, 0, st>>>(items, bitem, tbeg, tcnt, cls, s_off, t_off, p_off, meta, S, T, H, xp, b0,
+                                          part);
+  k_far_h_reduce<<<nitems, 128, 0, st>>>(items + item0, p_off, part, row_lo, row_hi, yp);
 }
 
 }  // namespace dev
