@@ -94,7 +94,11 @@ def algorithmic_bytes(info, c, n_classes_bytes):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clock / throttle-reason sampling during the timed region
+    (B200_PROFILING.md clocks line): NVML polled every 5 ms from a thread
+    (the device found by PCI bus id), nvidia-smi -lms as the fallback. The
+    sampler is running before the warm-up starts, so short timed regions
+    still get samples."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -104,20 +108,60 @@ class Clocks:
         self.device = device
         self.rows = []
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
         self.window = (0.0, float("inf"))
 
     def mark(self, t0, t1):
         self.window = (t0, t1)
 
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        try:
+            p = torch.cuda.get_device_properties(self.device)
+            bus = "%08x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.device)
+
+    def _poll(self):
+        nv, h = self.nvml
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                row = [str(sm), str(mx), "%.1f" % pw, hex(rs)] + ["Active" if rs & b else "Not Active" for b in bits]
+                self.rows.append((time.time(), row))
+            except Exception:
+                pass
+            self.stop.wait(0.005)
+
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.nvml = self._nvml_handle()
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+        except Exception:
+            self.nvml = None
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                              "--format=csv,noheader,nounits", "-lms", "50"],
+                                             stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+            except FileNotFoundError:
+                self.proc = None
+        # wait (bounded) for the first sample so the timed region is covered
+        t_end = time.time() + 3.0
+        while (self.nvml or self.proc) and not self.rows and time.time() < t_end:
+            time.sleep(0.01)
         return self
 
     def _read(self):
@@ -127,12 +171,14 @@ class Clocks:
                 self.rows.append((time.time(), parts))
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if self.nvml or self.proc:
             self.t.join(timeout=5)
 
     def summary(self):
@@ -150,7 +196,8 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows), "in_timed_window": in_window}
+                "reasons": reasons, "samples": len(self.rows), "in_timed_window": in_window,
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def measured_traffic(kernel, config, world):
@@ -309,8 +356,7 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
         tw1 = time.time()
-        if tw1 - tw0 < 1.0:
-            time.sleep(0.5)  # let the sampler land at least one row
+        time.sleep(0.05)  # the sampler's last row of the window
         clk.mark(tw0, tw1)
     launches = ctx.launches - launches0
     ms = ev0.elapsed_time(ev1)
