@@ -51,6 +51,8 @@ void launch_coupling_reduce(cudaStream_t, const std::int32_t*, const std::int32_
                             double*);
 void launch_near_tma_apply(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
                            double*, int*);
+void launch_near_mrhs2(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
+                       std::int64_t, int, std::int64_t, double*);
 void launch_near_mvm_symcsr(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
                             double*);
 bool launch_near_inst_tma(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, std::int64_t, int,
@@ -284,6 +286,8 @@ struct DevMatrix {
   std::vector<char> near_trans;  // block stored as the transpose of its partner
   std::int64_t E_logical = 0;    // sum of n_sigma n_tau over local near blocks
   DBuf sym_items, sym_blocks, g_row0, g_rows, g_sbeg, g_segs, sym_part;
+  std::int64_t sym_pstride = 0;  // partial segments per right-hand side
+  DBuf sym_part_m;               // two-sided K9: sym_pstride x m partials
   int n_sym_items = 0, n_gather_leaves = 0;
   bool near_tma = false;  // every item spans its whole leaf: TMA near pass
   DBuf batch_tab;         // K1 batch: w and D pointer tables
@@ -784,6 +788,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     upload(M.g_sbeg, sbeg, st);
     upload(M.g_segs, segs, st);
     M.sym_part.alloc(sizeof(double) * std::max<std::int64_t>(poff, 1));
+    M.sym_pstride = std::max<std::int64_t>(poff, 1);
   }
   {
     // K9 work (multi-RHS): CSR by sigma over every local near block; blocks
@@ -1436,6 +1441,29 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
   // runs on fp64 tensor cores (K9); single vectors stay on the HBM GEMV.
   // K9 computes rows sigma only, so a symmetric shard (whose transposed
   // products belong to other ranks' rows) keeps the two-sided GEMV.
+  static const bool two_sided = [] {
+    const char* e = std::getenv("PHM_K9_TWO_SIDED");
+    return !(e && std::atoi(e) == 0);
+  }();
+  // up to 32 RHS: each stored block read once, both products on DMMA
+  // (k_near_mrhs2; C3 at 10 RHS 6.4 -> 5.0 ms). At 64 RHS its 172 KB of
+  // shared memory leaves one CTA per SM and the one-sided K9 is faster
+  // (13.8 vs 15.1 ms), except on a symmetric shard, which needs both sides.
+  if (m >= kMrhsMin && M.near_tma && two_sided && (m <= 32 || (M.sym && M.sharded))) {
+    const size_t need = sizeof(double) * M.sym_pstride * m;
+    if (M.sym_part_m.bytes < need) M.sym_part_m.alloc(need);
+    ctx.run_on(st, "near_mrhs", [&] {
+      dev::launch_near_mrhs2(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items, M.sym_blocks.as<dev::SymBlock>(),
+                             I.D.as<double>(), M.xp.as<double>(), M.n, mm, M.sym_pstride, M.sym_part_m.as<double>());
+    });
+    for (Index c = 0; c < m; ++c)
+      ctx.run_on(st, "near_gather", [&] {
+        dev::launch_near_gather(st, M.n_gather_leaves, M.g_row0.as<std::int64_t>(), M.g_rows.as<std::int32_t>(),
+                                M.g_sbeg.as<std::int32_t>(), M.g_segs.as<dev::GatherSeg>(),
+                                M.sym_part_m.as<double>() + c * M.sym_pstride, M.yp.as<double>() + c * M.n);
+      });
+    return;
+  }
   const bool block_rhs = m >= kMrhsMin && !(M.sym && M.sharded);
   if (block_rhs)
     ctx.run_on(st, "near_mrhs", [&] {

@@ -763,6 +763,148 @@ __global__ void __launch_bounds__(128) k_near_mrhs(const MrhsItem* __restrict__ 
       }
 }
 
+// Copies the double pair src[0..1] into dst[0..1] (16 bytes when both are
+// 16-byte aligned, else two 8-byte copies); n_valid < 2 zero-fills the rest
+// (a zero-fill names the valid global address `safe` and reads nothing).
+__device__ __forceinline__ void cp_pair(double* dst, const double* src, int n_valid, const double* safe) {
+  if (n_valid == 2 && ((reinterpret_cast<std::uintptr_t>(src) | reinterpret_cast<std::uintptr_t>(dst)) & 15) == 0) {
+    cp_async16(dst, src, true);
+    return;
+  }
+  cp_async8(dst, n_valid > 0 ? src : safe, n_valid > 0);
+  cp_async8(dst + 1, n_valid > 1 ? src + 1 : safe, n_valid > 1);
+}
+
+// K9, two-sided (symmetric storage, whole-leaf items): every stored block is
+// read once and used twice on DMMA, Y_sigma += D X_tau (accumulated in
+// registers over the item's blocks) and Z_tau = D^T X_sigma (per 32-column
+// chunk, written to the block's column segment), so the near field of m
+// right-hand sides costs one pass over the stored D instead of two. One CTA
+// (8 warps) per (owner-leaf item, NC-column tile of the RHS). The D chunk is
+// staged column-major with leading dimension 132 and the X panels with 36 /
+// 132, which makes the four fragment reads (D, D^T, X_tau, X_sigma)
+// conflict-free per half-warp. Outputs go to the partial buffer (column c at
+// c * pstride) and k_near_gather sums them per leaf in a fixed order.
+constexpr int kK9bKc = 32, kK9bLd = 132, kK9bLx = 36;
+template <int NC>
+__global__ void __launch_bounds__(256) k_near_mrhs2(const SymRowItem* __restrict__ items,
+                                                    const SymBlock* __restrict__ blocks, const double* __restrict__ D,
+                                                    const double* __restrict__ X, std::int64_t n, int m,
+                                                    std::int64_t pstride, double* __restrict__ part) {
+  constexpr int NTN = NC / 8;
+  constexpr int STAGE = kK9bKc * kK9bLd + NC * kK9bLx;
+  extern __shared__ __align__(16) double sm[];
+  double* Xs = sm;                      // X_sigma: [c][r], ld 132
+  double* St = sm + NC * kK9bLd;        // two stages: D chunk [k][r] then X_tau [c][k]
+  const SymRowItem it = items[blockIdx.x];
+  const int c0 = blockIdx.y * NC;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t0 = lane & 3;
+  const int R = it.ld;                  // == rows (whole-leaf items)
+  const int R4 = (R + 3) & ~3;          // rows staged (zero beyond R)
+  const int hp = R4 >> 1;               // pairs per staged column
+  const int mtiles = (R + 15) >> 4;
+  const int ypairs = mtiles * NTN;
+  // X_sigma once per item
+  for (int q = tid; q < NC * hp; q += 256) {
+    const int c = q / hp, r = 2 * (q - c * hp);
+    const int nv = c0 + c < m ? max(0, min(2, R - r)) : 0;
+    cp_pair(Xs + c * kK9bLd + r, X + it.x_row0 + r + static_cast<std::int64_t>(c0 + c) * n, nv, X);
+  }
+  auto stage = [&](const SymBlock& blk, int j0, int buf) {
+    double* Dc = St + buf * STAGE;
+    double* Xt = Dc + kK9bKc * kK9bLd;
+    const int kc = min(kK9bKc, blk.ncol - j0);
+    const double* Db = D + blk.d_off + static_cast<std::int64_t>(j0) * R;
+    for (int q = tid; q < kK9bKc * hp; q += 256) {
+      const int k = q / hp, r = 2 * (q - k * hp);
+      const int nv = k < kc ? max(0, min(2, R - r)) : 0;
+      cp_pair(Dc + k * kK9bLd + r, Db + r + static_cast<std::int64_t>(k) * R, nv, D);
+    }
+    for (int q = tid; q < NC * (kK9bKc / 2); q += 256) {
+      const int c = q >> 4, k = 2 * (q & 15);
+      const int nv = c0 + c < m ? max(0, min(2, kc - k)) : 0;
+      cp_pair(Xt + c * kK9bLx + k, X + blk.x_col0 + j0 + k + static_cast<std::int64_t>(c0 + c) * n, nv, X);
+    }
+    cp_async_commit();
+  };
+  double yacc[8][4];  // up to 8 (m-tile, n-tile) pairs of Y per warp
+#pragma unroll
+  for (int p = 0; p < 8; ++p) yacc[p][0] = yacc[p][1] = yacc[p][2] = yacc[p][3] = 0.0;
+
+  int b = it.bbeg, j0 = 0, buf = 0;
+  if (b < it.bend) stage(blocks[b], 0, 0);
+  while (b < it.bend) {
+    const SymBlock blk = blocks[b];
+    int nb = b, nj = j0 + kK9bKc;
+    if (nj >= blk.ncol) {
+      nb = b + 1;
+      nj = 0;
+    }
+    if (nb < it.bend) {
+      stage(blocks[nb], nj, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* Dc = St + buf * STAGE;
+    const double* Xt = Dc + kK9bKc * kK9bLd;
+    const int kc = min(kK9bKc, blk.ncol - j0);
+    const int ksy = (kc + 3) >> 2;
+    // Y_sigma += D(:, chunk) X_tau(chunk, :)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int p = warp + 8 * q;
+      if (p < ypairs) {
+        const int mt = p / NTN, nt = p - mt * NTN;
+        for (int s2 = 0; s2 < ksy; ++s2) {
+          const int k = 4 * s2 + t0;
+          dmma_16x8x4(yacc[q], Dc[k * kK9bLd + 16 * mt + g], Dc[k * kK9bLd + 16 * mt + g + 8],
+                      Xt[(8 * nt + g) * kK9bLx + k]);
+        }
+      }
+    }
+    // Z_tau(chunk, :) = D(:, chunk)^T X_sigma (off-diagonal blocks)
+    if (blk.p_col >= 0) {
+      const int zpairs = ((kc + 15) >> 4) * NTN;
+      for (int p = warp; p < zpairs; p += 8) {
+        const int mt = p / NTN, nt = p - mt * NTN;
+        double z[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int s2 = 0; s2 < (R4 >> 2); ++s2) {
+          const int k = 4 * s2 + t0;
+          dmma_16x8x4(z, Dc[(16 * mt + g) * kK9bLd + k], Dc[(16 * mt + g + 8) * kK9bLd + k],
+                      Xs[(8 * nt + g) * kK9bLd + k]);
+        }
+#pragma unroll
+        for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int j = 16 * mt + g + 8 * r2, c = c0 + 8 * nt + 2 * t0 + cc;
+            if (j < kc && c < m) part[static_cast<std::int64_t>(c) * pstride + blk.p_col + j0 + j] = z[2 * r2 + cc];
+          }
+      }
+    }
+    __syncthreads();
+    b = nb;
+    j0 = nj;
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int p = warp + 8 * q;
+    if (p < ypairs) {
+      const int mt = p / NTN, nt = p - mt * NTN;
+#pragma unroll
+      for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int r = 16 * mt + g + 8 * r2, c = c0 + 8 * nt + 2 * t0 + cc;
+          if (r < R && c < m) part[static_cast<std::int64_t>(c) * pstride + it.p_row + r] = yacc[q][2 * r2 + cc];
+        }
+    }
+  }
+}
+
 // K6, symmetric storage: every stored block is streamed once and used twice
 // (y_sigma += D x_tau and y_tau += D^T x_sigma), halving the near-field
 // bytes of both instantiate and MVM for the (symmetric) radial kernels.
@@ -1675,6 +1817,24 @@ void launch_near_gather(cudaStream_t st, int nleaves, const std::int64_t* leaf_r
                         const std::int32_t* seg_beg, const GatherSeg* segs, const double* part, double* yp) {
   if (nleaves == 0) return;
   k_near_gather<<<nleaves, 128, 0, st>>>(leaf_row0, leaf_rows, seg_beg, segs, part, yp);
+}
+
+void launch_near_mrhs2(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks, const double* D,
+                       const double* X, std::int64_t n, int m, std::int64_t pstride, double* part) {
+  if (nitems == 0) return;
+#define PHM_K9B(NC)                                                                                         \
+  {                                                                                                         \
+    const size_t smem = (NC * kK9bLd + 2 * (kK9bKc * kK9bLd + NC * kK9bLx)) * sizeof(double);             \
+    smem_attr(reinterpret_cast<const void*>(k_near_mrhs2<NC>), static_cast<int>(smem), true);              \
+    const dim3 grid(static_cast<unsigned>(nitems), static_cast<unsigned>((m + NC - 1) / NC));               \
+    k_near_mrhs2<NC><<<grid, 256, smem, st>>>(items, blocks, D, X, n, m, pstride, part);                    \
+    return;                                                                                                 \
+  }
+  if (m <= 8) PHM_K9B(8)
+  if (m <= 16) PHM_K9B(16)
+  if (m <= 32) PHM_K9B(32)
+  PHM_K9B(64)
+#undef PHM_K9B
 }
 
 void launch_near_mrhs(cudaStream_t st, const MrhsItem* items, int nitems, const std::int64_t* tb, const std::int32_t* tn,
