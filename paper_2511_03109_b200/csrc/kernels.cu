@@ -804,21 +804,27 @@ __global__ void __launch_bounds__(256) k_near_mrhs2(const SymRowItem* __restrict
   const int hp = R4 >> 1;               // pairs per staged column
   const int mtiles = (R + 15) >> 4;
   const int ypairs = mtiles * NTN;
-  // X_sigma once per item
-  for (int q = tid; q < NC * hp; q += 256) {
-    const int c = q / hp, r = 2 * (q - c * hp);
-    const int nv = c0 + c < m ? max(0, min(2, R - r)) : 0;
-    cp_pair(Xs + c * kK9bLd + r, X + it.x_row0 + r + static_cast<std::int64_t>(c0 + c) * n, nv, X);
-  }
+  // X_sigma once per item: warp w stages columns w, w + 8, ..., lane l the
+  // row pairs l, l + 32 (no index division on the staging path)
+  for (int c = warp; c < NC; c += 8)
+    for (int pr = lane; pr < hp; pr += 32) {
+      const int r = 2 * pr;
+      const int nv = c0 + c < m ? max(0, min(2, R - r)) : 0;
+      cp_pair(Xs + c * kK9bLd + r, X + it.x_row0 + r + static_cast<std::int64_t>(c0 + c) * n, nv, X);
+    }
   auto stage = [&](const SymBlock& blk, int j0, int buf) {
     double* Dc = St + buf * STAGE;
     double* Xt = Dc + kK9bKc * kK9bLd;
     const int kc = min(kK9bKc, blk.ncol - j0);
     const double* Db = D + blk.d_off + static_cast<std::int64_t>(j0) * R;
-    for (int q = tid; q < kK9bKc * hp; q += 256) {
-      const int k = q / hp, r = 2 * (q - k * hp);
-      const int nv = k < kc ? max(0, min(2, R - r)) : 0;
-      cp_pair(Dc + k * kK9bLd + r, Db + r + static_cast<std::int64_t>(k) * R, nv, D);
+#pragma unroll
+    for (int kq = 0; kq < kK9bKc / 8; ++kq) {  // warp w: columns 4w .. 4w + 3
+      const int k = 4 * warp + kq;
+      for (int pr = lane; pr < hp; pr += 32) {
+        const int r = 2 * pr;
+        const int nv = k < kc ? max(0, min(2, R - r)) : 0;
+        cp_pair(Dc + k * kK9bLd + r, Db + r + static_cast<std::int64_t>(k) * R, nv, D);
+      }
     }
     for (int q = tid; q < NC * (kK9bKc / 2); q += 256) {
       const int c = q >> 4, k = 2 * (q & 15);
@@ -869,12 +875,23 @@ __global__ void __launch_bounds__(256) k_near_mrhs2(const SymRowItem* __restrict
       const int zpairs = ((kc + 15) >> 4) * NTN;
       for (int p = warp; p < zpairs; p += 8) {
         const int mt = p / NTN, nt = p - mt * NTN;
-        double z[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int s2 = 0; s2 < (R4 >> 2); ++s2) {
+        double z[4] = {0.0, 0.0, 0.0, 0.0}, z1[4] = {0.0, 0.0, 0.0, 0.0};
+        const int ksz = R4 >> 2;
+        int s2 = 0;
+        for (; s2 + 1 < ksz; s2 += 2) {  // two independent chains
+          const int k = 4 * s2 + t0;
+          dmma_16x8x4(z, Dc[(16 * mt + g) * kK9bLd + k], Dc[(16 * mt + g + 8) * kK9bLd + k],
+                      Xs[(8 * nt + g) * kK9bLd + k]);
+          dmma_16x8x4(z1, Dc[(16 * mt + g) * kK9bLd + k + 4], Dc[(16 * mt + g + 8) * kK9bLd + k + 4],
+                      Xs[(8 * nt + g) * kK9bLd + k + 4]);
+        }
+        if (s2 < ksz) {
           const int k = 4 * s2 + t0;
           dmma_16x8x4(z, Dc[(16 * mt + g) * kK9bLd + k], Dc[(16 * mt + g + 8) * kK9bLd + k],
                       Xs[(8 * nt + g) * kK9bLd + k]);
         }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) z[e] += z1[e];
 #pragma unroll
         for (int r2 = 0; r2 < 2; ++r2)
 #pragma unroll
