@@ -326,6 +326,10 @@ struct DevMatrix {
   // pooled instance buffers
   std::vector<DBuf> pool_D;
   std::mutex mu;
+  // Serialises the public entry points on one matrix: they share its
+  // workspace (xp, yp, x-hat, ...) and enqueue on one stream, so two host
+  // threads must not interleave their launch sequences.
+  std::recursive_mutex exec_mu;
   std::int64_t device_bytes = 0;
 
   cudaStream_t st() const { return ctx->stream; }
@@ -1265,6 +1269,7 @@ void run_instantiate_batch(const std::vector<DevInstance*>& insts, const double*
 }  // namespace
 
 std::shared_ptr<DevInstance> baseline_instance(std::shared_ptr<DevMatrix> m) {
+  std::lock_guard<std::recursive_mutex> exec_lock(m->exec_mu);
   PHM_CHECK(m->baseline, "baseline_instance: not a baseline matrix");
   CK(cudaSetDevice(m->ctx->device));
   auto I = alloc_instance(m);
@@ -1280,6 +1285,7 @@ std::shared_ptr<DevMatrix> baseline_build(std::shared_ptr<Context> ctx, const do
 
 std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const double* theta, int n_theta,
                                          StageCounters* counters) {
+  std::lock_guard<std::recursive_mutex> exec_lock(m->exec_mu);
   if (!m->ctx) throw std::logic_error("instantiate: host-only matrix (built without a device)");
   if (m->baseline) throw std::logic_error("instantiate: a baseline matrix is built at a fixed theta");
   CK(cudaSetDevice(m->ctx->device));
@@ -1292,6 +1298,7 @@ std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const dou
 
 std::vector<std::shared_ptr<DevInstance>> instantiate_batch(std::shared_ptr<DevMatrix> m, const double* thetas,
                                                             int n_theta, int count, StageCounters* counters) {
+  std::lock_guard<std::recursive_mutex> exec_lock(m->exec_mu);
   if (!m->ctx) throw std::logic_error("instantiate: host-only matrix (built without a device)");
   if (m->baseline) throw std::logic_error("instantiate: a baseline matrix is built at a fixed theta");
   PHM_CHECK(count >= 1, "instantiate_batch: count must be >= 1");
@@ -1309,6 +1316,7 @@ std::vector<std::shared_ptr<DevInstance>> instantiate_batch(std::shared_ptr<DevM
 
 void reinstantiate_batch(const std::vector<DevInstance*>& insts, const double* thetas, int n_theta,
                          StageCounters* counters) {
+  std::lock_guard<std::recursive_mutex> exec_lock(insts.at(0)->M->exec_mu);
   PHM_CHECK(!insts.empty(), "reinstantiate_batch: no instances");
   if (insts[0]->M->baseline) throw std::logic_error("reinstantiate: a baseline matrix is built at a fixed theta");
   for (DevInstance* I : insts) PHM_CHECK(I->M == insts[0]->M, "reinstantiate_batch: instances of different matrices");
@@ -1316,6 +1324,7 @@ void reinstantiate_batch(const std::vector<DevInstance*>& insts, const double* t
 }
 
 void reinstantiate(DevInstance& inst, const double* theta, int n_theta, StageCounters* counters) {
+  std::lock_guard<std::recursive_mutex> exec_lock(inst.M->exec_mu);
   if (inst.M->baseline) throw std::logic_error("reinstantiate: a baseline matrix is built at a fixed theta");
   run_instantiate(inst, theta, n_theta, counters);
 }
@@ -1323,6 +1332,7 @@ const std::vector<double>& instance_theta(const DevInstance& inst) { return inst
 void instance_sync(DevInstance& inst) { CK(cudaStreamSynchronize(inst.M->st())); }
 
 void instance_far_h(DevInstance& I, Index far_index, std::vector<double>& out, Index& rows, Index& cols) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   const DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   if (far_index < 0 || far_index >= static_cast<Index>(H.blocks.far.size())) throw std::out_of_range("far index");
@@ -1336,6 +1346,7 @@ void instance_far_h(DevInstance& I, Index far_index, std::vector<double>& out, I
 }
 
 void instance_near_d(DevInstance& I, Index b, std::vector<double>& out) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   const DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   if (b < 0 || b >= static_cast<Index>(H.blocks.near.size())) throw std::out_of_range("near index");
@@ -1355,6 +1366,7 @@ void instance_near_d(DevInstance& I, Index b, std::vector<double>& out) {
 }
 
 void instance_class_c(DevInstance& I, Index k, std::vector<double>& out) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   const DevMatrix& M = *I.M;
   if (!M.h2) throw std::invalid_argument("explicit C_k exists only for the H2 format");
   if (k < 0 || k >= M.ncls) throw std::out_of_range("class index");
@@ -1556,6 +1568,7 @@ void apply_tree_order(DevInstance& I, Index m) {
 }  // namespace
 
 void apply_device(DevInstance& I, const double* x_dev, double* y_dev, Index m) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   DevMatrix& M = *I.M;
   PHM_CHECK(m >= 1, "apply: m must be >= 1");
   CK(cudaSetDevice(M.ctx->device));
@@ -1567,6 +1580,7 @@ void apply_device(DevInstance& I, const double* x_dev, double* y_dev, Index m) {
 }
 
 void apply_host(DevInstance& I, const double* x, double* y, Index m) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   if (H.row_begin != 0 || H.row_end != M.n)
@@ -1650,6 +1664,7 @@ void instantiate_apply_tree(DevInstance& I, const double* theta, int n_theta, co
 
 void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, const double* x_dev, double* y_dev,
                               Index m, StageCounters* counters) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   DevMatrix& M = *I.M;
   if (M.sharded)
     throw std::logic_error("fused instantiate+apply on a row shard: use the partial apply and sum across ranks");
@@ -1661,6 +1676,7 @@ void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, 
 
 void instantiate_apply_partial_device(DevInstance& I, const double* theta, int n_theta, const double* x_dev,
                                       double* ypart_dev, Index m, StageCounters* counters) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   DevMatrix& M = *I.M;
   instantiate_apply_tree(I, theta, n_theta, x_dev, m, counters);
   CK(cudaMemcpyAsync(ypart_dev, M.yp.p, sizeof(double) * M.n * m, cudaMemcpyDeviceToDevice, M.st()));
@@ -1674,6 +1690,7 @@ void instantiate_apply_partial_device(DevInstance& I, const double* theta, int n
 double estimate_error(DevInstance& I, Index probe_rows, std::uint64_t seed, StageCounters* counters,
                       std::vector<Index>* rows_out, std::vector<double>* exact_out, std::vector<double>* approx_out,
                       std::vector<double>* x_out) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   const Tree& T = *H.tree;
@@ -1727,6 +1744,7 @@ double estimate_error(DevInstance& I, Index probe_rows, std::uint64_t seed, Stag
 
 void instantiate_apply_host(DevInstance& I, const double* theta, int n_theta, const double* x, double* y, Index m,
                             StageCounters* counters) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   DevMatrix& M = *I.M;
   CK(cudaSetDevice(M.ctx->device));
   ensure_workspace(M, m);
@@ -1738,6 +1756,7 @@ void instantiate_apply_host(DevInstance& I, const double* theta, int n_theta, co
 }
 
 void apply_device_partial(DevInstance& I, const double* x_dev, double* ypart_dev, Index m) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   DevMatrix& M = *I.M;
   PHM_CHECK(m >= 1, "apply: m must be >= 1");
   CK(cudaSetDevice(M.ctx->device));
@@ -1749,6 +1768,7 @@ void apply_device_partial(DevInstance& I, const double* x_dev, double* ypart_dev
 }
 
 void apply_device_rows(DevInstance& I, const double* x_dev, double* yrows_dev, Index m) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   if (M.sym && M.sharded)

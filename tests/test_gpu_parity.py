@@ -467,3 +467,31 @@ def test_h_form_far_blocks_beyond_48kb_shared(ph, po):
     assert max(int(ints[s, 3]) for s, _ in far) > 6000
     x = ph.generate_normal(24000, 9)
     assert rel(ph.instantiate(pm, [0.2]).apply(x), om.instantiate([0.2]).apply(x)) <= TOL_Y
+
+
+def test_concurrent_host_threads_share_one_matrix(ph, po):
+    """Two host threads applying instances of one matrix at the same time (the
+    C ABI releases the GIL): the matrix serialises its launch sequences, so
+    both get their own exact result."""
+    import threading
+
+    pts = ph.generate_points(2000, 3, 41)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    pm = ph.offline_h2(pts, cfg)
+    a, b = ph.instantiate(pm, [0.1]), ph.instantiate(pm, [0.4])
+    xs = [ph.generate_normal(2000, s) for s in (1, 2)]
+    want = [a.apply(xs[0]), b.apply(xs[1])]
+    got = [[], []]
+
+    def run(k, inst):
+        for _ in range(20):
+            got[k].append(inst.apply(xs[k]))
+
+    ts = [threading.Thread(target=run, args=(0, a)), threading.Thread(target=run, args=(1, b))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for k in (0, 1):
+        assert all(np.array_equal(y, want[k]) for y in got[k])
