@@ -1461,7 +1461,7 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
   // (k_near_mrhs2; C3 at 10 RHS 6.4 -> 5.0 ms). At 64 RHS its 172 KB of
   // shared memory leaves one CTA per SM and the one-sided K9 is faster
   // (13.8 vs 15.1 ms), except on a symmetric shard, which needs both sides.
-  if (m >= kMrhsMin && M.near_tma && two_sided && (m <= 32 || (M.sym && M.sharded))) {
+  if (m >= kMrhsMin && M.n_sym_items > 0 && two_sided && (m <= 32 || (M.sym && M.sharded))) {
     const size_t need = sizeof(double) * M.sym_pstride * m;
     if (M.sym_part_m.bytes < need) M.sym_part_m.alloc(need);
     ctx.run_on(st, "near_mrhs", [&] {

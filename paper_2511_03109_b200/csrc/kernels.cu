@@ -775,7 +775,7 @@ __device__ __forceinline__ void cp_pair(double* dst, const double* src, int n_va
   cp_async8(dst + 1, n_valid > 1 ? src + 1 : safe, n_valid > 1);
 }
 
-// K9, two-sided (symmetric storage, whole-leaf items): every stored block is
+// K9, two-sided (symmetric storage; items are <= 128-row slices of a leaf): every stored block is
 // read once and used twice on DMMA, Y_sigma += D X_tau (accumulated in
 // registers over the item's blocks) and Z_tau = D^T X_sigma (per 32-column
 // chunk, written to the block's column segment), so the near field of m
@@ -799,7 +799,8 @@ __global__ void __launch_bounds__(256) k_near_mrhs2(const SymRowItem* __restrict
   const SymRowItem it = items[blockIdx.x];
   const int c0 = blockIdx.y * NC;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t0 = lane & 3;
-  const int R = it.ld;                  // == rows (whole-leaf items)
+  const int R = it.rows;                // rows of this slice (<= 128)
+  const std::int64_t ld = it.ld;        // stored column length (the leaf)
   const int R4 = (R + 3) & ~3;          // rows staged (zero beyond R)
   const int hp = R4 >> 1;               // pairs per staged column
   const int mtiles = (R + 15) >> 4;
@@ -816,14 +817,14 @@ __global__ void __launch_bounds__(256) k_near_mrhs2(const SymRowItem* __restrict
     double* Dc = St + buf * STAGE;
     double* Xt = Dc + kK9bKc * kK9bLd;
     const int kc = min(kK9bKc, blk.ncol - j0);
-    const double* Db = D + blk.d_off + static_cast<std::int64_t>(j0) * R;
+    const double* Db = D + blk.d_off + it.i0 + static_cast<std::int64_t>(j0) * ld;
 #pragma unroll
     for (int kq = 0; kq < kK9bKc / 8; ++kq) {  // warp w: columns 4w .. 4w + 3
       const int k = 4 * warp + kq;
       for (int pr = lane; pr < hp; pr += 32) {
         const int r = 2 * pr;
         const int nv = k < kc ? max(0, min(2, R - r)) : 0;
-        cp_pair(Dc + k * kK9bLd + r, Db + r + static_cast<std::int64_t>(k) * R, nv, D);
+        cp_pair(Dc + k * kK9bLd + r, Db + r + static_cast<std::int64_t>(k) * ld, nv, D);
       }
     }
     for (int q = tid; q < NC * (kK9bKc / 2); q += 256) {

@@ -398,7 +398,7 @@ def test_near_gemv_paths_odd_n_and_large_leaves(ph, po, n, l_max):
     inst = ph.instantiate(pm, [0.19])
     oi = om.instantiate([0.19])
     rng = np.random.default_rng(n)
-    for m in (1, 2, 3):
+    for m in (1, 2, 3, 5, 40):  # 5: two-sided K9 over 128-row slices; 40: one-sided K9
         X = rng.standard_normal((n, m)) if m > 1 else rng.standard_normal(n)
         assert rel(inst.apply(X), oi.apply(X)) <= TOL_Y
     x = rng.standard_normal(n)
