@@ -42,6 +42,13 @@ CONFIGS = {
     # GPUs with no communication, each instantiated and applied to 10 vectors
     "c5": dict(n=262144, d=3, family="e", box=(0.05, 0.5), l_max=4, p_s=4, p_theta=8, eta=1.0, fmt="h2",
                points="uniform", sweep=True, rhs=10, n_theta=4096, theta_batch=8),
+    # BASELINE.json configs[3] (C4, the 8-GPU DMMA case): n = 2^20 points from
+    # a 16-Gaussian mixture, leaf 32, Matern-5/2 with theta = (l, sigma^2) on
+    # an 8 x 6 grid, 64 right-hand sides. Fits 8 x B200 only with symmetric
+    # near storage sharded over the ranks (about 150 GB of snapshots + D per
+    # rank); run under torchrun --nproc-per-node 8.
+    "c4": dict(n=1048576, d=3, family="m52", box=(0.05, 0.5), boxes=[(0.05, 0.5), (0.5, 2.0)], amplitude=True,
+               l_max=5, p_s=4, p_theta=[8, 6], eta=1.0, fmt="h2", points="mixture", rhs=64),
 }
 
 
@@ -74,8 +81,17 @@ def make_points(ph, c, seed):
     return ph.generate_mixture_points(c["n"], c["d"], 16, 0.05, seed)
 
 
+def theta_vectors(c, count, seed):
+    """count theta vectors: harness draws per parameter (harness.cpp:254-260),
+    the k-th parameter from seed + k."""
+    boxes = c.get("boxes", [c["box"]])
+    cols = [theta_draws(lo, hi, count, seed + k) for k, (lo, hi) in enumerate(boxes)]
+    return [[float(col[i]) for col in cols] for i in range(count)]
+
+
 def make_cfg(ph, c, rank=0, world=1, near_mode=None):
-    return ph.PHConfig(spec=ph.KernelSpec(ph.Family.from_id(c["family"]), [c["box"]]), l_max=c["l_max"],
+    spec = ph.KernelSpec(ph.Family.from_id(c["family"]), c.get("boxes", [c["box"]]), amplitude=c.get("amplitude", False))
+    return ph.PHConfig(spec=spec, l_max=c["l_max"],
                        p_s=c["p_s"], p_theta=c["p_theta"], eta=c["eta"], eps=1e-5, seed=0,
                        near_mode=ph.NearMode.SNAPSHOT if near_mode is None else near_mode,
                        shard_rank=rank, shard_count=world)
@@ -247,11 +263,11 @@ def cpu_baseline(ph, c, pts, pm_host, steps, sample, seed, m=1):
     ent = sizes[near[:, 0]] * sizes[near[:, 1]]
     f_near = ent[near_mask == 1].sum() / ent.sum()
     f_far = far_mask.sum() / max(1, len(far_mask))
-    thetas = theta_draws(c["box"][0], c["box"][1], max(steps, 1), seed)
+    thetas = theta_vectors(c, max(steps, 1), seed)
     x = ph.generate_normal(c["n"], seed + 1)
     per = []
     for s in range(steps):
-        inst, secs = om.instantiate_timed([thetas[s % len(thetas)]], near_mask)
+        inst, secs = om.instantiate_timed(thetas[s % len(thetas)], near_mask)
         _, asecs = inst.apply_sample(x, near_mask, far_mask)
         t = secs[0] + secs[1] / f_near + m * (asecs[0] + asecs[1] / f_far + asecs[2] / f_near)
         per.append(t)
@@ -289,8 +305,6 @@ def run_ours(args):
     sweep = c.get("sweep", False)          # C5: thetas sharded over ranks, no communication
     m = args.rhs or c.get("rhs", 1)        # right-hand sides per MVM
     row_shard = world > 1 and not sweep    # C3 at N GPUs: leaf rows sharded, y all-gathered
-    if row_shard and m != 1:
-        raise SystemExit("row-sharded bench supports one right-hand side")
     ctx = ph.Context(local)
     # A real (non-legacy) stream shared by torch (events, NCCL ordering) and
     # every kernel the library launches.
@@ -304,7 +318,7 @@ def run_ours(args):
     build_s = time.time() - t0
     info = pm.info()
     n = c["n"]
-    thetas = theta_draws(c["box"][0], c["box"][1], c.get("n_theta", 32), args.seed)
+    thetas = theta_vectors(c, c.get("n_theta", 32), args.seed)
     xs = np.stack([ph.generate_normal(n, args.seed + 1 + j) for j in range(m)])  # (m, n) = column-major n x m
     x_host = torch.from_numpy(xs).pin_memory()
     x_dev = x_host.cuda()
@@ -313,30 +327,30 @@ def run_ours(args):
     if row_shard:
         from paper_2511_03109_b200.dist import PartialSum
 
-        psum = PartialSum(n, 1, device="cuda")
-    inst = ph.instantiate(pm, [thetas[0]])
+        psum = PartialSum(n, m, device="cuda")
+    inst = ph.instantiate(pm, thetas[0])
     # sweeps: tb thetas per step, instantiated by one snapshot pass (K1 batch)
     tb = (args.theta_batch or c.get("theta_batch", 1)) if sweep else 1
-    binsts = ph.instantiate_batch(pm, [[thetas[b]] for b in range(tb)]) if tb > 1 else None
+    binsts = ph.instantiate_batch(pm, [thetas[b] for b in range(tb)]) if tb > 1 else None
 
     def theta_of(s):
         return thetas[(s * world + rank) % len(thetas)] if sweep else thetas[s % len(thetas)]
 
     def step(s):
         if binsts is not None:
-            ph.reinstantiate_batch(binsts, [[theta_of(s * tb + b)] for b in range(tb)])
+            ph.reinstantiate_batch(binsts, [theta_of(s * tb + b) for b in range(tb)])
             for b in range(tb):
                 binsts[b].apply_device(x_dev.data_ptr(), y_dev.data_ptr(), m)
             return
         if not row_shard:
             # instantiate(theta_s) + MVM as one overlapped schedule
-            inst.instantiate_apply_device([theta_of(s)], x_dev.data_ptr(), y_dev.data_ptr(), m)
+            inst.instantiate_apply_device(theta_of(s), x_dev.data_ptr(), y_dev.data_ptr(), m)
         else:
             # this rank's partial y (its owner leaves' near pairs, both ways,
             # and its rows' far field), summed over ranks by one all-reduce
-            inst.instantiate_apply_partial_device([theta_of(s)], x_dev.data_ptr(), psum.buf.data_ptr(), 1)
+            inst.instantiate_apply_partial_device(theta_of(s), x_dev.data_ptr(), psum.buf.data_ptr(), m)
             psum.reduce()
-            ph.lib().phm_unpermute_device(pm._h, ph._P(psum.buf.data_ptr()), ph._P(y_dev.data_ptr()), 1)
+            ph.lib().phm_unpermute_device(pm._h, ph._P(psum.buf.data_ptr()), ph._P(y_dev.data_ptr()), m)
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -386,7 +400,7 @@ def run_ours(args):
         return a.elapsed_time(b) / args.steps
 
     # phase split of the same step (same stream, CUDA events)
-    inst_ms = time_loop(lambda s: inst.reinstantiate([theta_of(s)]))
+    inst_ms = time_loop(lambda s: inst.reinstantiate(theta_of(s)))
     apply_ms = (time_loop(lambda s: inst.apply_device(x_dev.data_ptr(), y_dev.data_ptr(), m))
                 if not row_shard else None)
     # per-kernel split of the apply phase (separate loop: the timers add events)
@@ -415,7 +429,7 @@ def run_ours(args):
 
         def e2e_step(s):
             if binsts is not None:
-                ph.reinstantiate_batch(binsts, [[theta_of(s * tb + b)] for b in range(tb)])
+                ph.reinstantiate_batch(binsts, [theta_of(s * tb + b) for b in range(tb)])
                 for b in range(tb):
                     ph._check(ph.lib().phm_apply(binsts[b]._h, xh.ctypes.data_as(POINTER(c_double)), n,
                                                  yh.ctypes.data_as(POINTER(c_double)), m))
@@ -427,8 +441,8 @@ def run_ours(args):
                 y_host.copy_(y_dev, non_blocking=True)
                 stream.synchronize()
                 return
-            th = np.array([theta_of(s)])
-            ph._check(ph.lib().phm_instantiate_apply(inst._h, th.ctypes.data_as(POINTER(c_double)), 1,
+            th = np.array(theta_of(s))
+            ph._check(ph.lib().phm_instantiate_apply(inst._h, th.ctypes.data_as(POINTER(c_double)), th.size,
                                                      xh.ctypes.data_as(POINTER(c_double)), n,
                                                      yh.ctypes.data_as(POINTER(c_double)), m))
 

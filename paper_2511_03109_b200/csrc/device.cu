@@ -63,7 +63,7 @@ void launch_near_mrhs(cudaStream_t, const MrhsItem*, int, const std::int64_t*, c
                       const std::int64_t*, const std::int32_t*, const std::int32_t*, const double*, const double*,
                       std::int64_t, int, double*);
 void launch_near_gather(cudaStream_t, int, const std::int64_t*, const std::int32_t*, const std::int32_t*,
-                        const GatherSeg*, const double*, double*);
+                        const GatherSeg*, const double*, std::int64_t, std::int64_t, int, double*);
 void launch_down(cudaStream_t, const std::int32_t*, int, const std::int32_t*, const double*, int, int, int, int,
                  double*);
 void launch_leaf_bwd(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*, const double*,
@@ -1437,8 +1437,8 @@ void near_gather(DevInstance& I, Index c, cudaStream_t st) {
   DevMatrix& M = *I.M;
   M.ctx->run_on(st, "near_gather", [&] {
     dev::launch_near_gather(st, M.n_gather_leaves, M.g_row0.as<std::int64_t>(), M.g_rows.as<std::int32_t>(),
-                            M.g_sbeg.as<std::int32_t>(), M.g_segs.as<dev::GatherSeg>(), M.sym_part.as<double>(),
-                            M.yp.as<double>() + c * M.n);
+                            M.g_sbeg.as<std::int32_t>(), M.g_segs.as<dev::GatherSeg>(), M.sym_part.as<double>(), 0,
+                            M.n, 1, M.yp.as<double>() + c * M.n);
   });
 }
 
@@ -1468,12 +1468,11 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
       dev::launch_near_mrhs2(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items, M.sym_blocks.as<dev::SymBlock>(),
                              I.D.as<double>(), M.xp.as<double>(), M.n, mm, M.sym_pstride, M.sym_part_m.as<double>());
     });
-    for (Index c = 0; c < m; ++c)
-      ctx.run_on(st, "near_gather", [&] {
-        dev::launch_near_gather(st, M.n_gather_leaves, M.g_row0.as<std::int64_t>(), M.g_rows.as<std::int32_t>(),
-                                M.g_sbeg.as<std::int32_t>(), M.g_segs.as<dev::GatherSeg>(),
-                                M.sym_part_m.as<double>() + c * M.sym_pstride, M.yp.as<double>() + c * M.n);
-      });
+    ctx.run_on(st, "near_gather", [&] {
+      dev::launch_near_gather(st, M.n_gather_leaves, M.g_row0.as<std::int64_t>(), M.g_rows.as<std::int32_t>(),
+                              M.g_sbeg.as<std::int32_t>(), M.g_segs.as<dev::GatherSeg>(), M.sym_part_m.as<double>(),
+                              M.sym_pstride, M.n, mm, M.yp.as<double>());
+    });
     return;
   }
   const bool block_rhs = m >= kMrhsMin && !(M.sym && M.sharded);

@@ -433,6 +433,74 @@ __global__ void k_scatter(const double* __restrict__ yp, const std::int32_t* __r
 // ----------------------------------------------------------------- K3
 // xhat_sigma[a] = sum_i x_i prod_k U_k(i, a_k) (chebyshev.cpp:236-252); one
 // CTA per non-empty leaf, factor rows staged in shared memory per 64 points.
+// K3 for blocks of right-hand sides (P == 64, m >= 4): x_hat_sigma (P x m) =
+// F (P x cnt) X_sigma (cnt x m) with F[a][i] = prod_k U_k(i, a_k). One CTA
+// per (leaf, 64-column tile); thread t owns output row a = t mod 64 and the
+// columns cg, cg + 4, ... (cg = t / 64): each point's factor entries are read
+// once for all of them, and the factor rows are staged once per leaf instead
+// of once per column. Products and sums run in k_leaf_fwd's order, so every
+// column equals the single-vector result bit for bit.
+template <int MC>
+__global__ void __launch_bounds__(256) k_leaf_fwd_m(const std::int32_t* __restrict__ leaves,
+                                                    const std::int64_t* __restrict__ begin,
+                                                    const std::int32_t* __restrict__ count,
+                                                    const double* __restrict__ U, std::int64_t n, int d, int ps,
+                                                    const double* __restrict__ xp, int m, double* __restrict__ xhat) {
+  constexpr int P = 64, CH = 32;
+  __shared__ double su[CH * 3 * 16];  // CH points x d x ps (d * ps <= 48)
+  __shared__ double sx[CH * 4 * MC];  // CH points x the tile's columns
+  const int leaf = leaves[blockIdx.x];
+  const std::int64_t b0 = begin[leaf];
+  const int cnt = count[leaf];
+  const int c0 = blockIdx.y * 4 * MC;
+  const int ncol = min(4 * MC, m - c0);
+  const int a = threadIdx.x & 63, cg = threadIdx.x >> 6;
+  int dig[3] = {0, 0, 0};
+  {
+    int rem = a;
+    for (int k = 0; k < d; ++k) {
+      dig[k] = rem % ps;
+      rem /= ps;
+    }
+  }
+  double acc[MC];
+#pragma unroll
+  for (int j = 0; j < MC; ++j) acc[j] = 0.0;
+  const int dps = d * ps;
+  for (int i0 = 0; i0 < cnt; i0 += CH) {
+    const int len = min(CH, cnt - i0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < len * dps; e += blockDim.x) {
+      const int i = e / dps, r = e - i * dps, k = r / ps, j = r - k * ps;
+      su[e] = U[(static_cast<std::int64_t>(k) * n + b0 + i0 + i) * ps + j];
+    }
+    for (int e = threadIdx.x; e < len * ncol; e += blockDim.x) {
+      const int c = e / len, i = e - c * len;  // consecutive threads read consecutive points
+      sx[i * (4 * MC) + c] = xp[static_cast<std::int64_t>(c0 + c) * n + b0 + i0 + i];
+    }
+    __syncthreads();
+    for (int i = 0; i < len; ++i) {
+      double u[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) u[k] = k < d ? su[(i * d + k) * ps + dig[k]] : 1.0;
+#pragma unroll
+      for (int j = 0; j < MC; ++j) {
+        const int c = cg + 4 * j;
+        if (c < ncol) {
+          double f = sx[i * (4 * MC) + c];  // x_i u_1 ... u_d, the order of k_leaf_fwd
+          for (int k = 0; k < d; ++k) f *= u[k];
+          acc[j] += f;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MC; ++j) {
+    const int c = cg + 4 * j;
+    if (c < ncol) xhat[(static_cast<std::int64_t>(leaf) * m + c0 + c) * P + a] = acc[j];
+  }
+}
+
 __global__ void k_leaf_fwd(const std::int32_t* __restrict__ leaves, const std::int64_t* __restrict__ begin,
                            const std::int32_t* __restrict__ count, const double* __restrict__ U, std::int64_t n,
                            int d, int ps, int P, const double* __restrict__ xp, int m, double* __restrict__ xhat) {
@@ -1356,20 +1424,50 @@ __global__ void __maxnreg__(96) k_near_tma_apply(const SymRowItem* __restrict__ 
   }
 }
 
-// y[rows of leaf] = sum of the leaf's partial segments, in list order.
-__global__ void k_near_gather(const std::int64_t* __restrict__ leaf_row0, const std::int32_t* __restrict__ leaf_rows,
-                              const std::int32_t* __restrict__ seg_beg, const GatherSeg* __restrict__ segs,
-                              const double* __restrict__ part, double* __restrict__ yp) {
+// y[rows of leaf] = sum of the leaf's partial segments, in list order. Small
+// leaves: a thread per row walks the segments. Large leaves (clustered
+// points): the rows are accumulated in shared memory (chunks of 4096 rows)
+// while the segments are walked once in order, so the work is the total
+// segment length (not rows x segments); every row sums in the same order
+// either way.
+// blockIdx.y is the right-hand-side column (part stride pstride, yp stride n).
+__global__ void __launch_bounds__(128) k_near_gather(const std::int64_t* __restrict__ leaf_row0,
+                                                     const std::int32_t* __restrict__ leaf_rows,
+                                                     const std::int32_t* __restrict__ seg_beg,
+                                                     const GatherSeg* __restrict__ segs, const double* __restrict__ part,
+                                                     std::int64_t pstride, std::int64_t n, double* __restrict__ yp) {
+  constexpr int kRows = 4096;
+  __shared__ double acc[kRows];
   const int l = blockIdx.x;
+  const double* pc = part + blockIdx.y * pstride;
+  double* yc = yp + blockIdx.y * n;
   const int sb = seg_beg[l], se = seg_beg[l + 1];
-  for (int r = threadIdx.x; r < leaf_rows[l]; r += blockDim.x) {
-    double s = 0.0;
+  const int rows = leaf_rows[l];
+  if (rows <= 2 * static_cast<int>(blockDim.x)) {
+    // small leaf: a thread per row walks the (few) segments itself
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+      double s = 0.0;
+      for (int k = sb; k < se; ++k) {
+        const GatherSeg g = segs[k];
+        const int o = r - g.base;
+        if (o >= 0 && o < g.len) s += pc[g.poff + o];
+      }
+      yc[leaf_row0[l] + r] = s;
+    }
+    return;
+  }
+  for (int r0 = 0; r0 < rows; r0 += kRows) {
+    const int rn = min(kRows, rows - r0);
+    for (int r = threadIdx.x; r < rn; r += blockDim.x) acc[r] = 0.0;
+    __syncthreads();
     for (int k = sb; k < se; ++k) {
       const GatherSeg g = segs[k];
-      const int o = r - g.base;
-      if (o >= 0 && o < g.len) s += part[g.poff + o];
+      const int lo = max(g.base, r0), hi = min(g.base + g.len, r0 + rn);
+      for (int r = lo + threadIdx.x; r < hi; r += blockDim.x) acc[r - r0] += pc[g.poff + (r - g.base)];
+      __syncthreads();  // next segment may overlap these rows
     }
-    yp[leaf_row0[l] + r] = s;
+    for (int r = threadIdx.x; r < rn; r += blockDim.x) yc[leaf_row0[l] + r0 + r] = acc[r];
+    __syncthreads();
   }
 }
 
@@ -1746,6 +1844,14 @@ void launch_leaf_fwd(cudaStream_t st, const std::int32_t* leaves, int nleaves, c
                      const std::int32_t* count, const double* U, std::int64_t n, int d, int ps, int P, const double* xp,
                      int m, double* xhat) {
   if (nleaves == 0) return;
+  if (P == 64 && m >= 4 && d * ps <= 48) {
+    if (m <= 16) {
+      k_leaf_fwd_m<4><<<dim3(nleaves, (m + 15) / 16), 256, 0, st>>>(leaves, begin, count, U, n, d, ps, xp, m, xhat);
+    } else {
+      k_leaf_fwd_m<16><<<dim3(nleaves, (m + 63) / 64), 256, 0, st>>>(leaves, begin, count, U, n, d, ps, xp, m, xhat);
+    }
+    return;
+  }
   const size_t smem = (64 * d * ps + 64) * sizeof(double);
   if (smem > 48 * 1024) smem_attr(reinterpret_cast<const void*>(k_leaf_fwd), static_cast<int>(smem), false);
   k_leaf_fwd<<<dim3(nleaves, m), threads_for(P), smem, st>>>(leaves, begin, count, U, n, d, ps, P, xp, m, xhat);
@@ -1832,9 +1938,10 @@ bool launch_near_inst_tma(cudaStream_t st, const SymRowItem* items, int nitems, 
 }
 
 void launch_near_gather(cudaStream_t st, int nleaves, const std::int64_t* leaf_row0, const std::int32_t* leaf_rows,
-                        const std::int32_t* seg_beg, const GatherSeg* segs, const double* part, double* yp) {
-  if (nleaves == 0) return;
-  k_near_gather<<<nleaves, 128, 0, st>>>(leaf_row0, leaf_rows, seg_beg, segs, part, yp);
+                        const std::int32_t* seg_beg, const GatherSeg* segs, const double* part, std::int64_t pstride,
+                        std::int64_t n, int m, double* yp) {
+  if (nleaves == 0 || m == 0) return;
+  k_near_gather<<<dim3(nleaves, m), 128, 0, st>>>(leaf_row0, leaf_rows, seg_beg, segs, part, pstride, n, yp);
 }
 
 void launch_near_mrhs2(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks, const double* D,

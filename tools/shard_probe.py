@@ -1,4 +1,4 @@
-"""Per-rank cost of the row-sharded C3 step, measured on ONE GPU: builds shard
+"""Per-rank cost of the row-sharded step (C3, or C4 with --config c4), measured on ONE GPU: builds shard
 r of N (the rank's own near pairs, far blocks and replicated class stage) and
 times its instantiate + partial apply with CUDA events. Predicts the N-GPU
 step (max over ranks + the y all-reduce); not a multi-GPU measurement.
@@ -20,17 +20,20 @@ def main():
     ap.add_argument("--n-shards", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--ranks", type=int, nargs="+", default=[0, -1])
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--rhs", type=int, default=0)
     a = ap.parse_args()
     import torch
 
     import bench
     import paper_2511_03109_b200 as ph
 
-    c = bench.CONFIGS["c3"]
+    c = bench.CONFIGS[a.config]
+    m = a.rhs or c.get("rhs", 1)
     pts = bench.make_points(ph, c, 0)
-    thetas = bench.theta_draws(c["box"][0], c["box"][1], 32, 0)
-    x = torch.from_numpy(ph.generate_normal(c["n"], 1)).cuda()
-    part = torch.zeros(c["n"], dtype=torch.float64, device="cuda")
+    thetas = bench.theta_vectors(c, 32, 0)
+    x = torch.from_numpy(np.stack([ph.generate_normal(c["n"], 1 + j) for j in range(m)])).cuda()
+    part = torch.zeros((m, c["n"]), dtype=torch.float64, device="cuda")
     ctx = ph.Context(0)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -38,16 +41,19 @@ def main():
     for N in a.n_shards:
         for r in a.ranks:
             rank = r % N
+            import time
+            t0 = time.time()
             pm = ph.offline_h2(pts, bench.make_cfg(ph, c, rank, N), ctx)
+            build_s = time.time() - t0
             info = pm.info()
-            inst = ph.instantiate(pm, [thetas[0]])
+            inst = ph.instantiate(pm, thetas[0])
             for s in range(3):
-                inst.instantiate_apply_partial_device([thetas[s]], x.data_ptr(), part.data_ptr(), 1)
+                inst.instantiate_apply_partial_device(thetas[s], x.data_ptr(), part.data_ptr(), m)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record(stream)
             for s in range(a.steps):
-                inst.instantiate_apply_partial_device([thetas[s % 32]], x.data_ptr(), part.data_ptr(), 1)
+                inst.instantiate_apply_partial_device(thetas[s % 32], x.data_ptr(), part.data_ptr(), m)
             e1.record(stream)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / a.steps
@@ -55,17 +61,19 @@ def main():
             ctx.enable_timing(True)
             ctx.reset_timers()
             for s in range(a.steps):
-                inst.instantiate_apply_partial_device([thetas[s % 32]], x.data_ptr(), part.data_ptr(), 1)
+                inst.instantiate_apply_partial_device(thetas[s % 32], x.data_ptr(), part.data_ptr(), m)
             torch.cuda.synchronize()
             kern = {}
-            for name in ("near_inst_mvm", "class_inst", "near_w", "near_gather", "coupling", "coupling_reduce",
-                         "leaf_fwd", "up", "down", "leaf_bwd", "gather"):
+            for name in ("near_inst_mvm", "near_inst", "near_mrhs", "class_inst", "near_w", "near_gather", "coupling",
+                         "coupling_reduce", "leaf_fwd", "up", "down", "leaf_bwd", "gather"):
                 t, cnt = ctx.timer(name)
                 if cnt:
                     kern[name] = round(t / a.steps, 4)
             ctx.enable_timing(False)
-            print(json.dumps({"shards": N, "rank": rank, "ms_per_step": ms, "rows": info["row_end"] - info["row_begin"],
-                              "near_stored": info["near_stored"], "kernels_ms_per_step": kern}), flush=True)
+            print(json.dumps({"config": a.config, "rhs": m, "shards": N, "rank": rank, "ms_per_step": ms,
+                              "rows": info["row_end"] - info["row_begin"], "near_stored": info["near_stored"],
+                              "device_bytes": info["device_bytes"], "build_s": build_s,
+                              "kernels_ms_per_step": kern}), flush=True)
             del inst, pm
             torch.cuda.empty_cache()
 
