@@ -495,3 +495,24 @@ def test_concurrent_host_threads_share_one_matrix(ph, po):
         t.join()
     for k in (0, 1):
         assert all(np.array_equal(y, want[k]) for y in got[k])
+
+
+def test_clustered_points_large_leaves(ph, po):
+    """Mixture points (the C4 generator) leave some leaves with hundreds of
+    rows: row-sliced near items, the shared-memory leaf gather, and the
+    two-sided block-RHS kernel over slices, against the oracle."""
+    n = 12000
+    pts = ph.generate_mixture_points(n, 3, 16, 0.05, 3)
+    spec = ph.KernelSpec(ph.Family.MATERN52, [(0.05, 0.5), (0.5, 2.0)], amplitude=True)
+    cfg = ph.PHConfig(spec=spec, l_max=2, p_s=4, p_theta=[6, 4], eta=1.0, near_mode=ph.NearMode.SNAPSHOT)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    ints, _ = pm.nodes()
+    assert ints[ints[:, 0] == 2, 3].max() > 300
+    theta = [0.21, 1.3]
+    inst, oi = ph.instantiate(pm, theta), om.instantiate(theta)
+    rng = np.random.default_rng(12)
+    for m in (1, 5, 40):
+        X = rng.standard_normal((n, m)) if m > 1 else rng.standard_normal(n)
+        assert rel(inst.apply(X), oi.apply(X)) <= TOL_Y
+    x = rng.standard_normal(n)
+    assert rel(inst.instantiate_apply([0.33, 0.7], x), om.instantiate([0.33, 0.7]).apply(x)) <= TOL_Y
