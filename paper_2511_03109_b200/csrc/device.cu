@@ -29,7 +29,8 @@ namespace dev {
 void launch_snapshot(cudaStream_t, const SnapTile*, std::int64_t, const BlockGeom*, const double*, std::int64_t, int,
                      int, int, const double*, double, double*);
 void launch_inst_flat(cudaStream_t, const double*, std::int64_t, int, const double*, double*);
-bool launch_inst_flat_batch(cudaStream_t, const double*, std::int64_t, int, int, const double* const*, double* const*);
+bool launch_inst_flat_batch(cudaStream_t, const double*, std::int64_t, int, int, const InstPtrs&);
+bool launch_inst_tma(cudaStream_t, const double*, std::int64_t, int, int, const InstPtrs&);
 void launch_inst_tiles(cudaStream_t, const InstTile*, std::int64_t, const double*, const double*, double*);
 void launch_near_w(cudaStream_t, const NearW*, std::int64_t, const double*, const std::int32_t*, const ThetaV&,
                    double*);
@@ -290,7 +291,6 @@ struct DevMatrix {
   DBuf sym_part_m;               // two-sided K9: sym_pstride x m partials
   int n_sym_items = 0, n_gather_leaves = 0;
   bool near_tma = false;  // every item spans its whole leaf: TMA near pass
-  DBuf batch_tab;         // K1 batch: w and D pointer tables
   DBuf work_ctr;          // persistent near kernels' item counter
   // K9 multi-RHS near field (DMMA), CSR by sigma over stored blocks
   DBuf k9_items, k9_tb, k9_tn, k9_doff, k9_ld, k9_tr;
@@ -1136,6 +1136,16 @@ void inst_snapshot_w(DevInstance& I, const std::vector<std::vector<double>>& v, 
   M.ctx->run_on(s, "near_w", [&] { dev::launch_set_vec(s, I.w.as<double>(), M.R_snap, shape, amp); });
 }
 
+// K1 moves the snapshot slabs by TMA (k_inst_tma) unless PHM_K1_TMA=0
+// (k_inst_flat: 256-bit loads): 8.5 vs 9.3 ms at C3.
+bool k1_tma() {
+  static const bool on = [] {
+    const char* e = std::getenv("PHM_K1_TMA");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 // Near stage of instantiate: every stored D_b(theta) (K1).
 void inst_near(DevInstance& I, const double* theta, const std::vector<std::vector<double>>& v,
                const dev::ThetaV& tv, cudaStream_t s, StageCounters* counters) {
@@ -1145,7 +1155,11 @@ void inst_near(DevInstance& I, const double* theta, const std::vector<std::vecto
   if (M.mode == NearMode::Snapshot) {
     inst_snapshot_w(I, v, tv, s);
     ctx.run_on(s, "near_inst", [&] {
-      dev::launch_inst_flat(s, M.G.as<double>(), M.E, M.R_snap, I.w.as<double>(), I.D.as<double>());
+      dev::InstPtrs tab{};
+      tab.w[0] = I.w.as<double>();
+      tab.d[0] = I.D.as<double>();
+      if (!k1_tma() || !dev::launch_inst_tma(s, M.G.as<double>(), M.E, M.R_snap, 1, tab))
+        dev::launch_inst_flat(s, M.G.as<double>(), M.E, M.R_snap, I.w.as<double>(), I.D.as<double>());
     });
   } else if (M.mode == NearMode::TT) {
     ctx.run_on(s, "near_w", [&] {
@@ -1244,19 +1258,19 @@ void run_instantiate_batch(const std::vector<DevInstance*>& insts, const double*
   }
   for (int b = 0; b < B; ++b) inst_snapshot_w(*insts[b], vs[b], tvs[b], st);
   constexpr int kMax = 16;  // dev::kInstBatchMax
-  if (!M.batch_tab.p) M.batch_tab.alloc(2 * kMax * sizeof(void*));
   for (int b0 = 0; b0 < B; b0 += kMax) {
     const int nb = std::min(kMax, B - b0);
-    std::vector<const void*> tab(2 * kMax, nullptr);
+    dev::InstPtrs tab{};  // by value: no host staging buffer to race with
     for (int b = 0; b < nb; ++b) {
-      tab[b] = insts[b0 + b]->w.p;
-      tab[kMax + b] = insts[b0 + b]->D.p;
+      tab.w[b] = insts[b0 + b]->w.as<double>();
+      tab.d[b] = insts[b0 + b]->D.as<double>();
     }
-    CK(cudaMemcpyAsync(M.batch_tab.p, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice, st));
     bool ok = false;
     M.ctx->run_on(st, "near_inst", [&] {
-      ok = dev::launch_inst_flat_batch(st, M.G.as<double>(), M.E, M.R_snap, nb, M.batch_tab.as<const double*>(),
-                                       M.batch_tab.as<double*>() + kMax);
+      // larger batches are bound by the formation work, where the plain
+      // 256-bit stream is as fast (8 thetas: 16.7 vs 17.0 ms at C3)
+      ok = (nb <= 2 && k1_tma() && dev::launch_inst_tma(st, M.G.as<double>(), M.E, M.R_snap, nb, tab)) ||
+           dev::launch_inst_flat_batch(st, M.G.as<double>(), M.E, M.R_snap, nb, tab);
     });
     if (!ok)
       for (int b = 0; b < nb; ++b)

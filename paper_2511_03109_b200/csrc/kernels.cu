@@ -159,12 +159,11 @@ __global__ void __launch_bounds__(256, 1) k_inst_flat(const double* __restrict__
 constexpr int kInstBatchMax = 16;
 template <int R>
 __global__ void __launch_bounds__(256, 1) k_inst_flat_batch(const double* __restrict__ G, std::int64_t E, int B,
-                                                         const double* const* __restrict__ wptr,
-                                                         double* const* __restrict__ dptr) {
+                                                         InstPtrs tab) {
   __shared__ double W[kInstBatchMax][R];
   __shared__ double* Dp[kInstBatchMax];
-  for (int i = threadIdx.x; i < B * R; i += blockDim.x) W[i / R][i % R] = wptr[i / R][i % R];
-  if (threadIdx.x < B) Dp[threadIdx.x] = dptr[threadIdx.x];
+  for (int i = threadIdx.x; i < B * R; i += blockDim.x) W[i / R][i % R] = tab.w[i / R][i % R];
+  if (threadIdx.x < B) Dp[threadIdx.x] = tab.d[threadIdx.x];
   __syncthreads();
   const std::int64_t E4 = E >> 2;
   const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
@@ -861,7 +860,7 @@ __global__ void __launch_bounds__(256) k_near_mrhs2(const SymRowItem* __restrict
                                                     std::int64_t pstride, double* __restrict__ part) {
   constexpr int NTN = NC / 8;
   constexpr int STAGE = kK9bKc * kK9bLd + NC * kK9bLx;
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(128) double sm[];
   double* Xs = sm;                      // X_sigma: [c][r], ld 132
   double* St = sm + NC * kK9bLd;        // two stages: D chunk [k][r] then X_tau [c][k]
   const SymRowItem it = items[blockIdx.x];
@@ -1424,6 +1423,77 @@ __global__ void __maxnreg__(96) k_near_tma_apply(const SymRowItem* __restrict__ 
   }
 }
 
+// K1 over TMA (instantiate alone, snapshot mode): the flat stream of
+// k_inst_flat with the slabs moved by cp.async.bulk into an NST-deep ring
+// (one producer lane, 8 consumer warps, full/empty mbarriers), persistent
+// over chunks of CH doubles. Consumers form D_b[e] = sum_k w_b,k S_k[e] in
+// k_inst_flat's FMA order (bit-identical D) for each of the B thetas of the
+// call (B = 1: instantiate; B <= 16: the theta batch, whose weight and output
+// tables are device arrays) and store with 256-bit stores. 96 registers:
+// two CTAs per SM.
+template <int R, int CH, int NST>
+__global__ void __maxnreg__(96) k_inst_tma(const double* __restrict__ G, std::int64_t E, int B, InstPtrs tab) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) std::uint64_t full[NST], empty[NST];
+  __shared__ double W[kInstBatchMax][R];
+  __shared__ double* Dp[kInstBatchMax];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const std::int64_t nchunks = (E + CH - 1) / CH;
+  for (int i = tid; i < B * R; i += blockDim.x) W[i / R][i % R] = tab.w[i / R][i % R];
+  if (tid < B) Dp[tid] = tab.d[tid];
+  if (tid == 0) {
+    for (int q = 0; q < NST; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 8) {
+    if (lane == 0) {
+      int c = 0;
+      for (std::int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, ++c) {
+        const int slot = c % NST;
+        if (c >= NST) mbar_wait(&empty[slot], ((c / NST) - 1) & 1);
+        const std::int64_t e0 = ch * CH;
+        const std::int64_t left = E - e0;
+        const unsigned bytes = static_cast<unsigned>((left < CH ? left : CH) * 8);
+        mbar_expect_tx(&full[slot], bytes * R);
+#pragma unroll
+        for (int k = 0; k < R; ++k) bulk_g2s(sm + (slot * R + k) * CH, G + k * E + e0, bytes, &full[slot]);
+      }
+    }
+    return;
+  }
+  int c = 0;
+  for (std::int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, ++c) {
+    const int slot = c % NST;
+    const std::int64_t e0 = ch * CH;
+    const std::int64_t left = E - e0;
+    const int len = static_cast<int>(left < CH ? left : CH);  // a multiple of 4
+    mbar_wait(&full[slot], (c / NST) & 1);
+    const double* S = sm + slot * R * CH;
+    for (int q = tid; q < (len >> 2); q += 256) {
+      for (int b = 0; b < B; ++b) {
+        dbl4 acc = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          const double* sk = S + k * CH + 4 * q;
+          const double wk = W[b][k];
+          acc.x += sk[0] * wk;
+          acc.y += sk[1] * wk;
+          acc.z += sk[2] * wk;
+          acc.w += sk[3] * wk;
+        }
+        st4(Dp[b] + e0 + 4 * q, acc);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+}
+
+
 // y[rows of leaf] = sum of the leaf's partial segments, in list order. Small
 // leaves: a thread per row walks the segments. Large leaves (clustered
 // points): the rows are accumulated in shared memory (chunks of 4096 rows)
@@ -1721,6 +1791,22 @@ __global__ void __launch_bounds__(256) k_exact_rows(const std::int64_t* __restri
 }
 
 // ------------------------------------------------------------ launchers
+namespace {
+// cudaFuncSetAttribute once per (kernel, device, size): the attributes live
+// in each device's context, and launches may come from several host threads.
+void smem_attr(const void* fn, int bytes, bool max_carveout) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!done.insert(std::make_tuple(fn, dev, bytes)).second) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (max_carveout)
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+}  // namespace
+
 void launch_exact_rows(cudaStream_t st, const std::int64_t* rows, int nrows, const double* pts, std::int64_t n, int d,
                        int fam, const double* theta, double amp, const double* xp, double* out) {
   if (nrows == 0) return;
@@ -1733,8 +1819,7 @@ void launch_snapshot(cudaStream_t st, const SnapTile* tiles, std::int64_t ntiles
   if (grid > 0) k_snapshot<<<grid, 256, 0, st>>>(tiles, ntiles, geo, pts, n, d, fam, R, theta_nodes, amp, out);
 }
 
-bool launch_inst_flat_batch(cudaStream_t st, const double* G, std::int64_t E, int R, int B, const double* const* wptr,
-                            double* const* dptr) {
+bool launch_inst_flat_batch(cudaStream_t st, const double* G, std::int64_t E, int R, int B, const InstPtrs& tab) {
   if (B < 1 || B > kInstBatchMax) return false;
   static const int per_sm = [] {
     const char* e = std::getenv("PHM_K1_CTAS");
@@ -1744,19 +1829,49 @@ bool launch_inst_flat_batch(cudaStream_t st, const double* G, std::int64_t E, in
   const std::int64_t E4 = E >> 2;
   const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((E4 + 255) / 256, 148 * per_sm)));
   switch (R) {
-    case 1: k_inst_flat_batch<1><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
-    case 2: k_inst_flat_batch<2><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
-    case 3: k_inst_flat_batch<3><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
-    case 4: k_inst_flat_batch<4><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
-    case 5: k_inst_flat_batch<5><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
-    case 6: k_inst_flat_batch<6><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
-    case 8: k_inst_flat_batch<8><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
-    case 10: k_inst_flat_batch<10><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
-    case 12: k_inst_flat_batch<12><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
-    case 16: k_inst_flat_batch<16><<<grid, 256, 0, st>>>(G, E, B, wptr, dptr); return true;
+    case 1: k_inst_flat_batch<1><<<grid, 256, 0, st>>>(G, E, B, tab); return true;
+    case 2: k_inst_flat_batch<2><<<grid, 256, 0, st>>>(G, E, B, tab); return true;
+    case 3: k_inst_flat_batch<3><<<grid, 256, 0, st>>>(G, E, B, tab); return true;
+    case 4: k_inst_flat_batch<4><<<grid, 256, 0, st>>>(G, E, B, tab); return true;
+    case 5: k_inst_flat_batch<5><<<grid, 256, 0, st>>>(G, E, B, tab); return true;
+    case 6: k_inst_flat_batch<6><<<grid, 256, 0, st>>>(G, E, B, tab); return true;
+    case 8: k_inst_flat_batch<8><<<grid, 256, 0, st>>>(G, E, B, tab); return true;
+    case 10: k_inst_flat_batch<10><<<grid, 256, 0, st>>>(G, E, B, tab); return true;
+    case 12: k_inst_flat_batch<12><<<grid, 256, 0, st>>>(G, E, B, tab); return true;
+    case 16: k_inst_flat_batch<16><<<grid, 256, 0, st>>>(G, E, B, tab); return true;
     default: return false;
   }
 }
+bool launch_inst_tma(cudaStream_t st, const double* G, std::int64_t E, int R, int B, const InstPtrs& tab) {
+  if (E == 0) return true;
+  if (B < 1 || B > kInstBatchMax) return false;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#define PHM_K1T(RR)                                                                                           \
+  case RR: {                                                                                                  \
+    constexpr int CH = ((5120 / RR) & ~63) < 256 ? 256 : (((5120 / RR) & ~63) > 1024 ? 1024 : ((5120 / RR) & ~63)); \
+    constexpr int NST = 2;                                                                                    \
+    const size_t smem = static_cast<size_t>(NST * RR * CH) * sizeof(double);                                 \
+    smem_attr(reinterpret_cast<const void*>(k_inst_tma<RR, CH, NST>), static_cast<int>(smem), true);          \
+    const int grid = static_cast<int>(std::min<std::int64_t>((E + CH - 1) / CH, 2 * sms));                   \
+    k_inst_tma<RR, CH, NST><<<grid, kTmaThreads, smem, st>>>(G, E, B, tab);                                   \
+    return true;                                                                                              \
+  }
+  switch (R) {
+    PHM_K1T(1)
+    PHM_K1T(2)
+    PHM_K1T(4)
+    PHM_K1T(6)
+    PHM_K1T(8)
+    PHM_K1T(10)
+    PHM_K1T(12)
+    PHM_K1T(16)
+    default: return false;
+  }
+#undef PHM_K1T
+}
+
 void launch_inst_flat(cudaStream_t st, const double* G, std::int64_t E, int R, const double* w, double* D) {
   const std::int64_t E4 = E / 4;
   if (E4 == 0) return;
@@ -1788,21 +1903,6 @@ void launch_inst_tiles(cudaStream_t st, const InstTile* tiles, std::int64_t nt, 
   if (grid > 0) k_inst_tiles<<<grid, 256, 0, st>>>(tiles, nt, G, w, D);
 }
 
-namespace {
-// cudaFuncSetAttribute once per (kernel, device, size): the attributes live
-// in each device's context, and launches may come from several host threads.
-void smem_attr(const void* fn, int bytes, bool max_carveout) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  static std::mutex mu;
-  static std::set<std::tuple<const void*, int, int>> done;
-  std::lock_guard<std::mutex> lk(mu);
-  if (!done.insert(std::make_tuple(fn, dev, bytes)).second) return;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (max_carveout)
-    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-}
-}  // namespace
 
 void launch_near_w(cudaStream_t st, const NearW* meta, std::int64_t nb, const double* cores, const std::int32_t* dims,
                    const ThetaV& tv, double* w) {

@@ -59,6 +59,13 @@ struct NearW {  // theta-core chain of one TT near block
   std::int32_t pad;
 };
 
+// K1 output table, passed by value (no host staging): per theta of the call,
+// its snapshot weights w (R doubles, device) and its D (device).
+struct InstPtrs {
+  const double* w[16];
+  double* d[16];
+};
+
 struct ClassMeta {
   std::int64_t mid_off, l_off, r_off, h_off, c_off;
   std::int32_t rl, rr, dims_off, pad;  // dims_off into class_mid_dims (3 per theta core)
