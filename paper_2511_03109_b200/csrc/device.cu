@@ -932,7 +932,6 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
       // Groups: sigma nodes of one level with the same child parity, in node
       // id (Morton) order, 32 per group; classes of a group split into items.
       constexpr int kSlots = dev::kGroupSlots;
-      constexpr int kItemClasses = 64;
       std::map<std::pair<int, int>, std::vector<int>> by_lp;  // (level, parity) -> sigmas
       for (int s = 0; s < M.nnodes; ++s) {
         if (by_sigma[s].empty()) continue;
@@ -943,6 +942,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
       std::vector<std::int32_t> grp_sigma, grp_items{0}, item_cls, cls_tau;
       std::vector<std::uint8_t> item_tiles;
       std::vector<dev::CouplingItem> items;
+      std::vector<std::array<int, 3>> granges;  // (group, first class entry, end)
       for (auto& kv : by_lp) {
         const auto& sigs = kv.second;
         for (size_t g0 = 0; g0 < sigs.size(); g0 += kSlots) {
@@ -971,10 +971,19 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
               if (cr.second[slot] >= 0) tiles |= static_cast<std::uint8_t>(1u << (slot >> 3));
             item_tiles.push_back(tiles);
           }
-          const int e_end = static_cast<int>(item_cls.size());
-          for (; e < e_end; e += kItemClasses) items.push_back({grp, e, std::min(e + kItemClasses, e_end), 0});
-          grp_items.push_back(static_cast<std::int32_t>(items.size()));
+          granges.push_back({grp, e, static_cast<int>(item_cls.size())});
+          grp_items.push_back(0);  // filled below
         }
+      }
+      // Items of up to kItemClasses classes, sized so the launch has at least
+      // ~4 items per SM: a small matrix (C2: ~40 groups) would otherwise run
+      // ~40 CTAs that each walk ~60 classes one after another.
+      const int kItemClasses = static_cast<int>(std::min<std::size_t>(
+          64, std::max<std::size_t>(4, (item_cls.size() + 4 * 148 - 1) / (4 * 148))));
+      for (const auto& gr : granges) {
+        for (int e = gr[1]; e < gr[2]; e += kItemClasses)
+          items.push_back({gr[0], e, std::min(e + kItemClasses, gr[2]), 0});
+        grp_items[gr[0] + 1] = static_cast<std::int32_t>(items.size());
       }
       M.n_cg_items = static_cast<int>(items.size());
       M.n_cg_groups = static_cast<int>(grp_items.size()) - 1;
