@@ -323,6 +323,7 @@ struct DevMatrix {
   // apply workspace
   DBuf xp, yp, xhat, yhat, xdev, ydev;
   Index ws_m = 0;
+  std::int64_t ws_gen = 0;  // bumped whenever the workspace is reallocated
   // pooled instance buffers
   std::vector<DBuf> pool_D;
   std::mutex mu;
@@ -339,7 +340,20 @@ struct DevInstance {
   std::shared_ptr<DevMatrix> M;
   std::vector<double> theta;
   DBuf D, H, C, w;
+  // apply_tree_order captured as a CUDA graph per RHS count (the launch
+  // sequence is fixed for an instance: the buffers never move); tagged with
+  // the matrix's workspace generation, which changes when the workspace is
+  // reallocated.
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    std::int64_t ws_gen = -1;
+    std::int64_t launches = 0;  // kernels in the graph (for the launch count)
+    bool seen = false;          // the first call runs directly (lazy buffers)
+  };
+  std::map<Index, Graph> graphs;
   ~DevInstance() {
+    for (auto& g : graphs)
+      if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
     if (M && D.p) {
       std::lock_guard<std::mutex> lk(M->mu);
       M->pool_D.push_back(std::move(D));
@@ -378,6 +392,7 @@ void ensure_workspace(DevMatrix& M, Index m) {
     M.yhat.alloc(sizeof(double) * M.nnodes * M.P * m);
   }
   M.ws_m = m;
+  ++M.ws_gen;
 }
 
 }  // namespace
@@ -1589,6 +1604,53 @@ void apply_tree_order(DevInstance& I, Index m) {
 
 }  // namespace
 
+// apply_tree_order through the instance's CUDA graph for m (captured on first
+// use; the whole fork/join launch sequence replays as one graph launch).
+// Per-kernel timing (ctx.timing) and PHM_APPLY_GRAPH=0 take the direct path.
+void apply_tree_order_graphed(DevInstance& I, Index m) {
+  DevMatrix& M = *I.M;
+  Context& ctx = *M.ctx;
+  static const bool use = [] {
+    const char* e = std::getenv("PHM_APPLY_GRAPH");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (!use || ctx.timing) {
+    apply_tree_order(I, m);
+    return;
+  }
+  DevInstance::Graph& g = I.graphs[m];
+  if (!g.seen || g.ws_gen != M.ws_gen) {
+    // first call for this m (or after the workspace moved): direct launches,
+    // which also perform any lazy allocation; the next call captures
+    if (g.exec) CK(cudaGraphExecDestroy(g.exec));
+    g.exec = nullptr;
+    g.seen = true;
+    g.ws_gen = M.ws_gen;
+    apply_tree_order(I, m);
+    return;
+  }
+  if (!g.exec) {
+    cudaGraph_t graph = nullptr;
+    const std::int64_t l0 = ctx.launches;
+    CK(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      apply_tree_order(I, m);
+    } catch (...) {
+      cudaStreamEndCapture(ctx.stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    CK(cudaStreamEndCapture(ctx.stream, &graph));
+    CK(cudaGraphInstantiate(&g.exec, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    g.ws_gen = M.ws_gen;
+    g.launches = ctx.launches - l0;
+    ctx.launches = l0;  // counted when the graph runs
+  }
+  CK(cudaGraphLaunch(g.exec, ctx.stream));
+  ctx.launches += g.launches;
+}
+
 void apply_device(DevInstance& I, const double* x_dev, double* y_dev, Index m) {
   std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
   DevMatrix& M = *I.M;
@@ -1597,7 +1659,7 @@ void apply_device(DevInstance& I, const double* x_dev, double* y_dev, Index m) {
   ensure_workspace(M, m);
   cudaStream_t st = M.st();
   M.ctx->run("gather", [&] { dev::launch_gather(st, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
-  apply_tree_order(I, m);
+  apply_tree_order_graphed(I, m);
   M.ctx->run("scatter", [&] { dev::launch_scatter(st, M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev); });
 }
 
