@@ -1182,7 +1182,10 @@ void inst_near(DevInstance& I, const double* theta, const std::vector<std::vecto
       dev::InstPtrs tab{};
       tab.w[0] = I.w.as<double>();
       tab.d[0] = I.D.as<double>();
-      if (!k1_tma() || !dev::launch_inst_tma(s, M.G.as<double>(), M.E, M.R_snap, 1, tab))
+      // the TMA ring pays off on large snapshot sets; small ones (C1: 160 MB)
+      // run faster as the plain 256-bit stream
+      const bool big = static_cast<double>(M.E) * M.R_snap * 8.0 > 1e9;
+      if (!big || !k1_tma() || !dev::launch_inst_tma(s, M.G.as<double>(), M.E, M.R_snap, 1, tab))
         dev::launch_inst_flat(s, M.G.as<double>(), M.E, M.R_snap, I.w.as<double>(), I.D.as<double>());
     });
   } else if (M.mode == NearMode::TT) {
