@@ -669,25 +669,31 @@ __global__ void __launch_bounds__(P / 16 * 32) k_coupling_mma(const CouplingItem
     __syncthreads();
     const double* Ck = C + static_cast<std::int64_t>(item_cls[e]) * P * P;
     const unsigned tiles = item_tiles[e];
-    double a[KS][2];
+    // k in two halves: half the C_k fragments live in registers at a time
+    // (occupancy), each half still feeds every tile
+    constexpr int KH = KS / 2 > 0 ? KS / 2 : 1;
 #pragma unroll
-    for (int s2 = 0; s2 < KS; ++s2) {
-      const std::int64_t k = 4 * s2 + t0;
-      a[s2][0] = __ldg(Ck + (row0 + g) + k * P);
-      a[s2][1] = __ldg(Ck + (row0 + g + 8) + k * P);
-    }
+    for (int h = 0; h < KS / KH; ++h) {
+      double a[KH][2];
 #pragma unroll
-    for (int c = 0; c < MC; ++c) {
-      if (c >= ncol) break;
-      const double* X = smem + (buf * MC + c) * PANEL;
-      // tile-outer so an empty tile is a branch around its KS MMAs (a
-      // predicated MMA would still occupy the pipe)
+      for (int s2 = 0; s2 < KH; ++s2) {
+        const std::int64_t k = 4 * (h * KH + s2) + t0;
+        a[s2][0] = __ldg(Ck + (row0 + g) + k * P);
+        a[s2][1] = __ldg(Ck + (row0 + g + 8) + k * P);
+      }
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        if (!((tiles >> j) & 1u)) continue;
+      for (int c = 0; c < MC; ++c) {
+        if (c >= ncol) break;
+        const double* X = smem + (buf * MC + c) * PANEL;
+        // tile-outer so an empty tile is a branch around its MMAs (a
+        // predicated MMA would still occupy the pipe)
 #pragma unroll
-        for (int s2 = 0; s2 < KS; ++s2)
-          dmma_16x8x4(acc[c][j], a[s2][0], a[s2][1], X[(8 * j + g) * LD + 4 * s2 + t0]);
+        for (int j = 0; j < NT; ++j) {
+          if (!((tiles >> j) & 1u)) continue;
+#pragma unroll
+          for (int s2 = 0; s2 < KH; ++s2)
+            dmma_16x8x4(acc[c][j], a[s2][0], a[s2][1], X[(8 * j + g) * LD + 4 * (h * KH + s2) + t0]);
+        }
       }
     }
     __syncthreads();  // X[buf] is refilled two classes later
