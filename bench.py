@@ -379,7 +379,9 @@ def run_ours(args):
     k1_name, k1_desc = "near_inst_mvm", "k_near_tma (K1+K6 fused TMA pass: forms, stores and applies D)"
     k1_ms, k1_n = ctx.timer(k1_name)
     if k1_n == 0:
-        k1_name, k1_desc = "near_inst", "k_inst_flat (K1 near instantiate)"
+        k1_name = "near_inst"
+        k1_desc = ("k_inst_tma (K1 near instantiate over TMA)" if 8 * info["near_stream_elems"] > 1.1e9 and
+                   os.environ.get("PHM_K1_TMA", "1") != "0" else "k_inst_flat (K1 near instantiate)")
         k1_ms, k1_n = ctx.timer(k1_name)
     timers = {}
     for name in ("near_inst_mvm", "near_inst", "class_inst", "near_w", "near_mvm", "near_gather", "near_mrhs", "coupling",
