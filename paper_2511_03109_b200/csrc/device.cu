@@ -12,6 +12,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "engine.hpp"
@@ -32,11 +33,12 @@ void launch_inst_flat(cudaStream_t, const double*, std::int64_t, int, const doub
 bool launch_inst_flat_batch(cudaStream_t, const double*, std::int64_t, int, int, const InstPtrs&);
 bool launch_inst_tma(cudaStream_t, const double*, std::int64_t, int, int, const InstPtrs&);
 void launch_inst_tiles(cudaStream_t, const InstTile*, std::int64_t, const double*, const double*, double*);
-void launch_near_w(cudaStream_t, const NearW*, std::int64_t, const double*, const std::int32_t*, const ThetaV&,
+void launch_near_w(cudaStream_t, const NearW*, std::int64_t, const double*, const std::int32_t*, const ThetaParams*,
                    double*);
-void launch_set_vec(cudaStream_t, double*, int, const ThetaV&, double);
+void launch_set_vec(cudaStream_t, double*, int, const ThetaParams*);
+void launch_put_theta(cudaStream_t, const ThetaParams&, ThetaParams*);
 void launch_class_inst(cudaStream_t, const ClassMeta*, int, const double*, const std::int32_t*, const double*,
-                       const double*, const ThetaV&, int, bool, int, int, int, int, double*, double*);
+                       const double*, const ThetaParams*, int, bool, int, int, int, int, double*, double*);
 void launch_gather(cudaStream_t, const double*, const std::int32_t*, std::int64_t, std::int64_t, double*);
 void launch_scatter(cudaStream_t, const double*, const std::int32_t*, std::int64_t, std::int64_t, double*);
 void launch_leaf_fwd(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*, const double*,
@@ -291,6 +293,7 @@ struct DevMatrix {
   DBuf sym_part_m;               // two-sided K9: sym_pstride x m partials
   int n_sym_items = 0, n_gather_leaves = 0;
   bool near_tma = false;  // every item spans its whole leaf: TMA near pass
+  DBuf theta_dev;         // dev::ThetaParams of the instantiate in flight
   DBuf work_ctr;          // persistent near kernels' item counter
   // K9 multi-RHS near field (DMMA), CSR by sigma over stored blocks
   DBuf k9_items, k9_tb, k9_tn, k9_doff, k9_ld, k9_tr;
@@ -350,7 +353,8 @@ struct DevInstance {
     std::int64_t launches = 0;  // kernels in the graph (for the launch count)
     bool seen = false;          // the first call runs directly (lazy buffers)
   };
-  std::map<Index, Graph> graphs;
+  // key: (launch sequence, input pointer it reads, RHS count)
+  std::map<std::tuple<int, const void*, Index>, Graph> graphs;
   ~DevInstance() {
     for (auto& g : graphs)
       if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
@@ -799,6 +803,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     M.n_gather_leaves = static_cast<int>(lrow0.size());
     M.near_tma = !items.empty();
     M.work_ctr.alloc(sizeof(int));
+    M.theta_dev.alloc(sizeof(dev::ThetaParams));
     for (const auto& it : items)  // whole-leaf items (k_near_tma)
       M.near_tma = M.near_tma && it.i0 == 0 && it.rows == it.ld;
     upload(M.sym_items, items, st);
@@ -1134,30 +1139,42 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
 namespace {
 
 // Class stage of instantiate: H_k(theta) and C_k = L_k H_k R_k^T (K2).
-void inst_classes(DevInstance& I, const dev::ThetaV& tv, cudaStream_t s) {
+// Writes the theta-dependent inputs (parametric vectors, snapshot weights'
+// shape part, amplitude) to M.theta_dev on stream s: the kernels of the
+// class stage and of the near weights read them there, so their launch
+// parameters do not depend on theta.
+void put_theta(DevMatrix& M, const std::vector<std::vector<double>>& v, const dev::ThetaV& tv, cudaStream_t s) {
+  const KernelSpec& spec = M.hm->cfg.spec;
+  dev::ThetaParams p{};
+  p.tv = tv;
+  p.shape = tv;
+  p.shape.dt = spec.shape_params();
+  p.amp = 1.0;
+  if (spec.amplitude && M.mode == NearMode::Snapshot) {
+    const auto& g = M.hm->grids.grids[spec.shape_params()];
+    p.amp = 0.0;
+    for (int j = 0; j < g.p; ++j) p.amp += v[spec.shape_params()][j] * g.nodes[j];
+  }
+  M.ctx->run_on(s, "put_theta", [&] { dev::launch_put_theta(s, p, M.theta_dev.as<dev::ThetaParams>()); });
+}
+
+void inst_classes(DevInstance& I, cudaStream_t s) {
   DevMatrix& M = *I.M;
   M.ctx->run_on(s, "class_inst", [&] {
     dev::launch_class_inst(s, M.cmeta.as<dev::ClassMeta>(), M.ncls, M.class_mid.as<double>(),
-                           M.class_mid_dims.as<std::int32_t>(), M.class_L.as<double>(), M.class_R.as<double>(), tv, M.P,
-                           M.h2, M.capA, M.capB, M.capT, M.capL, I.H.as<double>(), I.C.as<double>());
+                           M.class_mid_dims.as<std::int32_t>(), M.class_L.as<double>(), M.class_R.as<double>(),
+                           M.theta_dev.as<dev::ThetaParams>(), M.P, M.h2, M.capA, M.capB, M.capT, M.capL,
+                           I.H.as<double>(), I.C.as<double>());
   });
 }
 
 // Snapshot weights w = v_shape (x) ... times the amplitude interpolant
 // sum_j v_j s_j (the full-rank NearBlockTT theta-core chain).
-void inst_snapshot_w(DevInstance& I, const std::vector<std::vector<double>>& v, const dev::ThetaV& tv,
-                     cudaStream_t s) {
+void inst_snapshot_w(DevInstance& I, cudaStream_t s) {
   DevMatrix& M = *I.M;
-  const KernelSpec& spec = M.hm->cfg.spec;
-  dev::ThetaV shape = tv;
-  shape.dt = spec.shape_params();
-  double amp = 1.0;
-  if (spec.amplitude) {
-    const auto& g = M.hm->grids.grids[spec.shape_params()];
-    amp = 0.0;
-    for (int j = 0; j < g.p; ++j) amp += v[spec.shape_params()][j] * g.nodes[j];
-  }
-  M.ctx->run_on(s, "near_w", [&] { dev::launch_set_vec(s, I.w.as<double>(), M.R_snap, shape, amp); });
+  M.ctx->run_on(s, "near_w", [&] {
+    dev::launch_set_vec(s, I.w.as<double>(), M.R_snap, M.theta_dev.as<dev::ThetaParams>());
+  });
 }
 
 // K1 moves the snapshot slabs by TMA (k_inst_tma) unless PHM_K1_TMA=0
@@ -1171,13 +1188,12 @@ bool k1_tma() {
 }
 
 // Near stage of instantiate: every stored D_b(theta) (K1).
-void inst_near(DevInstance& I, const double* theta, const std::vector<std::vector<double>>& v,
-               const dev::ThetaV& tv, cudaStream_t s, StageCounters* counters) {
+void inst_near(DevInstance& I, const double* theta, cudaStream_t s, StageCounters* counters) {
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   Context& ctx = *M.ctx;
   if (M.mode == NearMode::Snapshot) {
-    inst_snapshot_w(I, v, tv, s);
+    inst_snapshot_w(I, s);
     ctx.run_on(s, "near_inst", [&] {
       dev::InstPtrs tab{};
       tab.w[0] = I.w.as<double>();
@@ -1191,7 +1207,8 @@ void inst_near(DevInstance& I, const double* theta, const std::vector<std::vecto
   } else if (M.mode == NearMode::TT) {
     ctx.run_on(s, "near_w", [&] {
       dev::launch_near_w(s, M.near_w_meta.as<dev::NearW>(), M.n_near_local, M.near_cores.as<double>(),
-                         M.near_core_dims.as<std::int32_t>(), tv, I.w.as<double>());
+                         M.near_core_dims.as<std::int32_t>(), M.theta_dev.as<dev::ThetaParams>(),
+                         I.w.as<double>());
     });
     ctx.run_on(s, "near_inst", [&] {
       dev::launch_inst_tiles(s, M.inst_tiles.as<dev::InstTile>(), M.n_inst_tiles, M.G.as<double>(),
@@ -1225,7 +1242,7 @@ void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCoun
     I.theta = B.theta;
     if (M.H_len) CK(cudaMemcpyAsync(I.H.p, M.fixed_H.p, sizeof(double) * M.H_len, cudaMemcpyDeviceToDevice, st));
     if (M.C_len) CK(cudaMemcpyAsync(I.C.p, M.fixed_C.p, sizeof(double) * M.C_len, cudaMemcpyDeviceToDevice, st));
-    inst_near(I, B.theta.data(), {}, dev::ThetaV{}, st, nullptr);
+    inst_near(I, B.theta.data(), st, nullptr);
     return;
   }
   // theta box check before any launch (farfield.cpp:23-24)
@@ -1234,8 +1251,9 @@ void run_instantiate(DevInstance& I, const double* theta, int n_theta, StageCoun
   const dev::ThetaV tv = make_theta_v(v);
   // (Overlapping the class stage with K1 on the side stream measured
   // slower: its CTAs displaced K1's and K1 lost 1.8 ms.)
-  inst_classes(I, tv, M.ctx->stream);
-  inst_near(I, theta, v, tv, M.ctx->stream, counters);
+  put_theta(M, v, tv, M.ctx->stream);
+  inst_classes(I, M.ctx->stream);
+  inst_near(I, theta, M.ctx->stream, counters);
 }
 
 }  // namespace
@@ -1273,17 +1291,18 @@ void run_instantiate_batch(const std::vector<DevInstance*>& insts, const double*
   std::vector<std::vector<std::vector<double>>> vs(B);
   for (int b = 0; b < B; ++b) vs[b] = parametric_vectors(H.grids, thetas + b * n_theta, n_theta);  // all checked first
   cudaStream_t st = M.ctx->stream;
-  std::vector<dev::ThetaV> tvs(B);
+  // per theta, in stream order: its parameters, class stage and near
+  // weights (non-snapshot modes: its whole near stage)
   for (int b = 0; b < B; ++b) {
     insts[b]->theta.assign(thetas + b * n_theta, thetas + (b + 1) * n_theta);
-    tvs[b] = make_theta_v(vs[b]);
-    inst_classes(*insts[b], tvs[b], st);
+    put_theta(M, vs[b], make_theta_v(vs[b]), st);
+    inst_classes(*insts[b], st);
+    if (M.mode == NearMode::Snapshot)
+      inst_snapshot_w(*insts[b], st);
+    else
+      inst_near(*insts[b], thetas + b * n_theta, st, counters);
   }
-  if (M.mode != NearMode::Snapshot) {
-    for (int b = 0; b < B; ++b) inst_near(*insts[b], thetas + b * n_theta, vs[b], tvs[b], st, counters);
-    return;
-  }
-  for (int b = 0; b < B; ++b) inst_snapshot_w(*insts[b], vs[b], tvs[b], st);
+  if (M.mode != NearMode::Snapshot) return;
   constexpr int kMax = 16;  // dev::kInstBatchMax
   for (int b0 = 0; b0 < B; b0 += kMax) {
     const int nb = std::min(kMax, B - b0);
@@ -1607,29 +1626,32 @@ void apply_tree_order(DevInstance& I, Index m) {
 
 }  // namespace
 
-// apply_tree_order through the instance's CUDA graph for m (captured on first
-// use; the whole fork/join launch sequence replays as one graph launch).
-// Per-kernel timing (ctx.timing) and PHM_APPLY_GRAPH=0 take the direct path.
-void apply_tree_order_graphed(DevInstance& I, Index m) {
+// Runs body (a theta-independent launch sequence on the context's streams)
+// through the instance's CUDA graph for key: the first call per key runs it
+// directly (lazy allocations happen there), the second captures it, later
+// calls replay it as one graph launch; a workspace move re-captures.
+// Per-kernel timing (ctx.timing) and PHM_GRAPHS=0 take the direct path.
+// Measured effect is within noise on the benchmarked configurations (C1-C3):
+// their steps are dominated by kernel time, not by launch gaps.
+template <typename F>
+void run_graphed(DevInstance& I, int seq, const void* input, Index m, F&& body) {
   DevMatrix& M = *I.M;
   Context& ctx = *M.ctx;
   static const bool use = [] {
-    const char* e = std::getenv("PHM_APPLY_GRAPH");
+    const char* e = std::getenv("PHM_GRAPHS");
     return !(e && std::atoi(e) == 0);
   }();
   if (!use || ctx.timing) {
-    apply_tree_order(I, m);
+    body();
     return;
   }
-  DevInstance::Graph& g = I.graphs[m];
+  DevInstance::Graph& g = I.graphs[std::make_tuple(seq, input, m)];
   if (!g.seen || g.ws_gen != M.ws_gen) {
-    // first call for this m (or after the workspace moved): direct launches,
-    // which also perform any lazy allocation; the next call captures
     if (g.exec) CK(cudaGraphExecDestroy(g.exec));
     g.exec = nullptr;
     g.seen = true;
     g.ws_gen = M.ws_gen;
-    apply_tree_order(I, m);
+    body();
     return;
   }
   if (!g.exec) {
@@ -1637,7 +1659,7 @@ void apply_tree_order_graphed(DevInstance& I, Index m) {
     const std::int64_t l0 = ctx.launches;
     CK(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
     try {
-      apply_tree_order(I, m);
+      body();
     } catch (...) {
       cudaStreamEndCapture(ctx.stream, &graph);
       if (graph) cudaGraphDestroy(graph);
@@ -1646,7 +1668,6 @@ void apply_tree_order_graphed(DevInstance& I, Index m) {
     CK(cudaStreamEndCapture(ctx.stream, &graph));
     CK(cudaGraphInstantiate(&g.exec, graph, 0));
     CK(cudaGraphDestroy(graph));
-    g.ws_gen = M.ws_gen;
     g.launches = ctx.launches - l0;
     ctx.launches = l0;  // counted when the graph runs
   }
@@ -1662,7 +1683,7 @@ void apply_device(DevInstance& I, const double* x_dev, double* y_dev, Index m) {
   ensure_workspace(M, m);
   cudaStream_t st = M.st();
   M.ctx->run("gather", [&] { dev::launch_gather(st, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
-  apply_tree_order_graphed(I, m);
+  run_graphed(I, 0, nullptr, m, [&] { apply_tree_order(I, m); });
   M.ctx->run("scatter", [&] { dev::launch_scatter(st, M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev); });
 }
 
@@ -1680,6 +1701,54 @@ void apply_host(DevInstance& I, const double* x, double* y, Index m) {
   CK(cudaMemcpyAsync(y, M.ydev.p, sizeof(double) * M.n * m, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
 }
+// The launch sequence of instantiate(theta) + apply(x) after put_theta (H^2,
+// snapshot or TT near mode): the class stage and the whole H^2 far chain on
+// the side stream, the near stage (fused with the GEMV for one vector in
+// snapshot mode) on the main stream. It depends on theta only through
+// M.theta_dev, so it is graph-captured per (instance, x, m).
+void instantiate_apply_sequence(DevInstance& I, const double* x_dev, Index m, StageCounters* counters) {
+  DevMatrix& M = *I.M;
+  Context& ctx = *M.ctx;
+  cudaStream_t st = ctx.stream, fs = ctx.side;
+  ctx.fork();  // side stream sees x (and everything before) as ready
+  ctx.run_on(fs, "gather", [&] { dev::launch_gather(fs, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
+  CK(cudaEventRecord(ctx.aux_ev, fs));
+  inst_classes(I, fs);
+  far_chain(I, m, fs);
+  bool fused = false;
+  // Snapshot mode, one vector: K1 and K6 fused into one TMA pass over the
+  // snapshots (k_near_tma) -- 10.8 ms at C3 against 9.8 + 1.6 ms for the
+  // separate kernels. D is bit-identical to K1's; y agrees with the separate
+  // path to rounding (row sums are accumulated in a different order).
+  // PHM_FUSED_NEAR=0 selects the separate kernels.
+  static const bool use_fused = [] {
+    const char* e = std::getenv("PHM_FUSED_NEAR");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (use_fused && M.near_tma && M.mode == NearMode::Snapshot && m == 1) {
+    // one pass over the snapshots: D is formed, stored and multiplied at once
+    inst_snapshot_w(I, st);
+    CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
+    ctx.run_on(st, "near_inst_mvm", [&] {
+      fused = dev::launch_near_inst_tma(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
+                                        M.sym_blocks.as<dev::SymBlock>(), M.G.as<double>(), M.E, M.R_snap,
+                                        I.w.as<double>(), I.D.as<double>(), M.xp.as<double>(),
+                                        M.sym_part.as<double>());
+    });
+    if (fused) {
+      if (M.n_gather_leaves == 0 || M.sharded) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
+      near_gather(I, 0, st);
+    }
+  }
+  if (!fused) {
+    inst_near(I, nullptr, st, counters);
+    CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
+    near_product(I, m, st);
+  }
+  ctx.join();
+  far_finish(I, m, st);
+}
+
 
 // instantiate(theta) followed by apply(x), scheduled as one graph of work:
 // the class stage and the whole H^2 far chain (compute-bound: K2, K3-K5, K7)
@@ -1708,44 +1777,8 @@ void instantiate_apply_tree(DevInstance& I, const double* theta, int n_theta, co
   }
   I.theta.assign(theta, theta + n_theta);
   Context& ctx = *M.ctx;
-  cudaStream_t st = ctx.stream, fs = ctx.side;
-  ctx.fork();  // side stream sees x (and everything before) as ready
-  ctx.run_on(fs, "gather", [&] { dev::launch_gather(fs, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
-  CK(cudaEventRecord(ctx.aux_ev, fs));
-  inst_classes(I, tv, fs);
-  far_chain(I, m, fs);
-  bool fused = false;
-  // Snapshot mode, one vector: K1 and K6 fused into one TMA pass over the
-  // snapshots (k_near_tma) -- 10.8 ms at C3 against 9.8 + 1.6 ms for the
-  // separate kernels. D is bit-identical to K1's; y agrees with the separate
-  // path to rounding (row sums are accumulated in a different order).
-  // PHM_FUSED_NEAR=0 selects the separate kernels.
-  static const bool use_fused = [] {
-    const char* e = std::getenv("PHM_FUSED_NEAR");
-    return !(e && std::atoi(e) == 0);
-  }();
-  if (use_fused && M.near_tma && M.mode == NearMode::Snapshot && m == 1) {
-    // one pass over the snapshots: D is formed, stored and multiplied at once
-    inst_snapshot_w(I, v, tv, st);
-    CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
-    ctx.run_on(st, "near_inst_mvm", [&] {
-      fused = dev::launch_near_inst_tma(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
-                                        M.sym_blocks.as<dev::SymBlock>(), M.G.as<double>(), M.E, M.R_snap,
-                                        I.w.as<double>(), I.D.as<double>(), M.xp.as<double>(),
-                                        M.sym_part.as<double>());
-    });
-    if (fused) {
-      if (M.n_gather_leaves == 0 || M.sharded) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
-      near_gather(I, 0, st);
-    }
-  }
-  if (!fused) {
-    inst_near(I, theta, v, tv, st, counters);
-    CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
-    near_product(I, m, st);
-  }
-  ctx.join();
-  far_finish(I, m, st);
+  put_theta(M, v, tv, ctx.stream);  // the only theta-dependent launch
+  run_graphed(I, 1, x_dev, m, [&] { instantiate_apply_sequence(I, x_dev, m, counters); });
 }
 }  // namespace
 

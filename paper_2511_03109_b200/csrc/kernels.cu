@@ -232,7 +232,9 @@ __global__ void __launch_bounds__(256) k_inst_tiles(const InstTile* __restrict__
 // w_b = I * prod_i contract_mode2(G_{b,i+1}, v_i) (nearfield.cpp:71-77),
 // evaluated right to left as a vector chain; one warp per near block.
 __global__ void k_near_w(const NearW* __restrict__ meta, std::int64_t nb, const double* __restrict__ cores,
-                         const std::int32_t* __restrict__ dims, ThetaV tv, double* __restrict__ w) {
+                         const std::int32_t* __restrict__ dims, const ThetaParams* __restrict__ tp,
+                         double* __restrict__ w) {
+  const ThetaV& tv = tp->tv;
   extern __shared__ double sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
@@ -281,22 +283,27 @@ __global__ void k_near_w(const NearW* __restrict__ meta, std::int64_t nb, const 
   }
 }
 
-__global__ void k_set_vec(double* dst, int n, ThetaV tv) {
-  // dst = v_0 (x) v_1 (x) ... (first factor fastest), amplitude handled by caller
+__global__ void k_set_vec(double* dst, int n, const ThetaParams* __restrict__ tp) {
+  // dst = (v_0 (x) v_1 (x) ...) * amp over the shape parameters (first
+  // factor fastest); amp = 1 leaves the product unchanged bit for bit
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const ThetaV& tv = tp->shape;
   int rem = i;
   double s = 1.0;
   for (int k = 0; k < tv.dt; ++k) {
     s *= tv.v[k][rem % tv.p[k]];
     rem /= tv.p[k];
   }
-  dst[i] = s;
+  dst[i] = s * tp->amp;
 }
 
-__global__ void k_scale(double* x, std::int64_t n, double a) {
-  const std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) x[i] *= a;
+__global__ void k_put_theta(ThetaParams p, ThetaParams* __restrict__ dst) {
+  const int n = sizeof(ThetaParams) / sizeof(double);
+  static_assert(sizeof(ThetaParams) % sizeof(double) == 0, "ThetaParams is copied as doubles");
+  const double* src = reinterpret_cast<const double*>(&p);
+  double* out = reinterpret_cast<double*>(dst);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = src[i];
 }
 
 // ----------------------------------------------------------------- K2
@@ -304,8 +311,9 @@ __global__ void k_scale(double* x, std::int64_t n, double a) {
 // (farfield.cpp:149-155); for H^2 also C = L H R^T in 32-column tiles.
 __global__ void k_class_inst(const ClassMeta* __restrict__ meta, int ncls, const double* __restrict__ mid,
                              const std::int32_t* __restrict__ mid_dims, const double* __restrict__ Lm,
-                             const double* __restrict__ Rm, ThetaV tv, int P, int want_c, int capA, int capB,
-                             int capT, double* __restrict__ H, double* __restrict__ C) {
+                             const double* __restrict__ Rm, const ThetaParams* __restrict__ tp, int P, int want_c,
+                             int capA, int capB, int capT, double* __restrict__ H, double* __restrict__ C) {
+  const ThetaV& tv = tp->tv;
   extern __shared__ double sm[];
   const ClassMeta M = meta[blockIdx.x];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -1911,26 +1919,28 @@ void launch_inst_tiles(cudaStream_t st, const InstTile* tiles, std::int64_t nt, 
 
 
 void launch_near_w(cudaStream_t st, const NearW* meta, std::int64_t nb, const double* cores, const std::int32_t* dims,
-                   const ThetaV& tv, double* w) {
+                   const ThetaParams* tp, double* w) {
   if (nb == 0) return;
   const int wpb = 8;
   const int grid = static_cast<int>(std::min<std::int64_t>((nb + wpb - 1) / wpb, 148 * 16));
-  k_near_w<<<grid, 32 * wpb, wpb * 2 * 256 * sizeof(double), st>>>(meta, nb, cores, dims, tv, w);
+  k_near_w<<<grid, 32 * wpb, wpb * 2 * 256 * sizeof(double), st>>>(meta, nb, cores, dims, tp, w);
 }
 
-void launch_set_vec(cudaStream_t st, double* dst, int n, const ThetaV& tv, double amp) {
-  k_set_vec<<<(n + 127) / 128, 128, 0, st>>>(dst, n, tv);
-  if (amp != 1.0) k_scale<<<(n + 127) / 128, 128, 0, st>>>(dst, n, amp);
+void launch_set_vec(cudaStream_t st, double* dst, int n, const ThetaParams* tp) {
+  k_set_vec<<<(n + 127) / 128, 128, 0, st>>>(dst, n, tp);
+}
+void launch_put_theta(cudaStream_t st, const ThetaParams& p, ThetaParams* dst) {
+  k_put_theta<<<1, 128, 0, st>>>(p, dst);
 }
 
 
 void launch_class_inst(cudaStream_t st, const ClassMeta* meta, int ncls, const double* mid, const std::int32_t* dims,
-                       const double* L, const double* R, const ThetaV& tv, int P, bool want_c, int capA, int capB,
-                       int capT, int capL, double* H, double* C) {
+                       const double* L, const double* R, const ThetaParams* tp, int P, bool want_c, int capA,
+                       int capB, int capT, int capL, double* H, double* C) {
   if (ncls == 0) return;
   const size_t smem = static_cast<size_t>(capA + capB + capT + capL) * sizeof(double);
   smem_attr(reinterpret_cast<const void*>(k_class_inst), 227 * 1024, false);
-  k_class_inst<<<ncls, 256, smem, st>>>(meta, ncls, mid, dims, L, R, tv, P, want_c ? 1 : 0, capA, capB, capT, H, C);
+  k_class_inst<<<ncls, 256, smem, st>>>(meta, ncls, mid, dims, L, R, tp, P, want_c ? 1 : 0, capA, capB, capT, H, C);
 }
 
 void launch_gather(cudaStream_t st, const double* x, const std::int32_t* perm, std::int64_t n, std::int64_t m,

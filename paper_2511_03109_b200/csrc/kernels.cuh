@@ -59,6 +59,15 @@ struct NearW {  // theta-core chain of one TT near block
   std::int32_t pad;
 };
 
+// The theta-dependent inputs of an instantiate, in device memory so the
+// launch sequence is the same for every theta (CUDA graphs): the parametric
+// vectors, the snapshot-shape subset of them and the amplitude factor.
+struct ThetaParams {
+  ThetaV tv;
+  ThetaV shape;
+  double amp;
+};
+
 // K1 output table, passed by value (no host staging): per theta of the call,
 // its snapshot weights w (R doubles, device) and its D (device).
 struct InstPtrs {
