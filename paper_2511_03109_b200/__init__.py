@@ -36,7 +36,12 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def library_path() -> str:
-    return os.path.join(_HERE, "libphmat_b200.so")
+    # PHM_LIB selects another in-tree build (tools/check_build.sh builds
+    # libphmat_b200_checked.so with device-side invariant checks)
+    name = os.environ.get("PHM_LIB", "libphmat_b200.so")
+    if os.path.basename(name) != name or not name.startswith("libphmat_b200"):
+        raise ImportError("PHM_LIB must name an in-tree libphmat_b200*.so")
+    return os.path.join(_HERE, name)
 
 
 class PhmatError(RuntimeError):

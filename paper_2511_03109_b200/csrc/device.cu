@@ -3,6 +3,7 @@
 // online stage (instantiate, apply) as a sequence of sm_100a kernels on one
 // stream. No CPU fallback: every online computation is a kernel launch.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -130,6 +131,15 @@ void upload(DBuf& buf, const std::vector<T>& v, cudaStream_t st) {
 }  // namespace
 
 // ---------------------------------------------------------------- context
+// NVTX range for the lifetime of the object (header-only NVTX 3; a no-op
+// unless a tool is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct Context {
   int device = 0;
   cudaStream_t own = nullptr;
@@ -174,6 +184,7 @@ struct Context {
   template <typename F>
   void run_on(cudaStream_t s, const char* name, F&& f) {
     ++launches;
+    NvtxRange nvtx(name);  // host-side launch range (nsys / ncu --nvtx)
     if (!timing) {
       f();
       CK(cudaGetLastError());
@@ -1385,6 +1396,7 @@ void reinstantiate_batch(const std::vector<DevInstance*>& insts, const double* t
 
 void reinstantiate(DevInstance& inst, const double* theta, int n_theta, StageCounters* counters) {
   std::lock_guard<std::recursive_mutex> exec_lock(inst.M->exec_mu);
+  NvtxRange nvtx("phm::instantiate");
   if (inst.M->baseline) throw std::logic_error("reinstantiate: a baseline matrix is built at a fixed theta");
   run_instantiate(inst, theta, n_theta, counters);
 }
@@ -1677,6 +1689,7 @@ void run_graphed(DevInstance& I, int seq, const void* input, Index m, F&& body) 
 
 void apply_device(DevInstance& I, const double* x_dev, double* y_dev, Index m) {
   std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  NvtxRange nvtx("phm::apply");
   DevMatrix& M = *I.M;
   PHM_CHECK(m >= 1, "apply: m must be >= 1");
   CK(cudaSetDevice(M.ctx->device));
@@ -1785,6 +1798,7 @@ void instantiate_apply_tree(DevInstance& I, const double* theta, int n_theta, co
 void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, const double* x_dev, double* y_dev,
                               Index m, StageCounters* counters) {
   std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  NvtxRange nvtx("phm::instantiate_apply");
   DevMatrix& M = *I.M;
   if (M.sharded)
     throw std::logic_error("fused instantiate+apply on a row shard: use the partial apply and sum across ranks");

@@ -12,6 +12,20 @@
 
 #include "kernels.cuh"
 
+// Device-side invariant checks of the TMA / shared-memory kernels (built
+// into libphmat_b200_checked.so only): a violated layout assumption traps,
+// which the host sees as a CUDA error on the next call.
+#ifdef PHM_DEVICE_CHECKS
+#define PHM_DCHECK(cond) \
+  do {                   \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define PHM_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace phm {
 namespace dev {
 
@@ -885,6 +899,7 @@ __global__ void __launch_bounds__(256) k_near_mrhs2(const SymRowItem* __restrict
   const int R4 = (R + 3) & ~3;          // rows staged (zero beyond R)
   const int hp = R4 >> 1;               // pairs per staged column
   const int mtiles = (R + 15) >> 4;
+  PHM_DCHECK(R >= 1 && R <= 128 && it.i0 + R <= it.ld);
   const int ypairs = mtiles * NTN;
   // X_sigma once per item: warp w stages columns w, w + 8, ..., lane l the
   // row pairs l, l + 32 (no index division on the staging path)
@@ -1160,6 +1175,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_near_tma(const SymRowItem* _
   const int ld = it.ld;  // == rows (the TMA path takes whole-height blocks)
   const int nb = it.bend - it.bbeg;
   const int jc = min(128, (CH / ld) & ~1);  // even column count per chunk
+  PHM_DCHECK(ld >= 1 && ld <= 128 && it.rows == ld && it.i0 == 0 && nb <= kTmaMaxBlocks && jc >= 2);
   if (tid < it.rows) xs_sh[tid] = xp[it.x_row0 + tid];
   if (tid < nb) bl[tid] = blocks[it.bbeg + tid];
   if (tid == 0) {
@@ -1181,6 +1197,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_near_tma(const SymRowItem* _
           if (c >= NST) mbar_wait(&empty[slot], ((c / NST) - 1) & 1);
           const int ncols = min(jc, ncol - j0);
           const unsigned bytes = static_cast<unsigned>(((static_cast<std::int64_t>(ncols) * ld * 8) + 15) & ~15LL);
+          PHM_DCHECK(bytes <= CH * 8u && ((reinterpret_cast<std::uintptr_t>(G + d_off + static_cast<std::int64_t>(j0) * ld) & 15) == 0));
           mbar_expect_tx(&full[slot], bytes * R);
           const double* src = G + d_off + static_cast<std::int64_t>(j0) * ld;
 #pragma unroll
@@ -1332,10 +1349,12 @@ __global__ void __maxnreg__(96) k_near_tma_apply(const SymRowItem* __restrict__ 
             const std::int64_t e0 = d_off + static_cast<std::int64_t>(j0) * ld;
             const std::int64_t ea = e0 & ~std::int64_t(1);
             const std::int64_t nbytes = (((e0 + static_cast<std::int64_t>(ncols) * ld - ea) + 1) & ~std::int64_t(1)) * 8;
+            PHM_DCHECK(ld <= 128 && it.rows == ld && nbytes <= (CH + 2) * 8 && ncols <= 64);
             // x_tau panel: xp + column may sit on an odd element (odd n, RHS > 0)
             const double* xsrc = xp + x_col0 + j0;
             const int xsh = static_cast<int>((reinterpret_cast<std::uintptr_t>(xsrc) >> 3) & 1);
             const unsigned xbytes = static_cast<unsigned>(((ncols + xsh + 1) & ~1) * 8);
+            PHM_DCHECK(xbytes <= 66 * 8);
             mbar_expect_tx(&full[slot], static_cast<unsigned>(nbytes) + xbytes);
             bulk_g2s(sm + slot * kStage, D + ea, static_cast<unsigned>(nbytes), &full[slot]);
             bulk_g2s(sm + slot * kStage + CH + 2, xsrc - xsh, xbytes, &full[slot]);
@@ -1485,6 +1504,7 @@ __global__ void __maxnreg__(96) k_inst_tma(const double* __restrict__ G, std::in
     const std::int64_t e0 = ch * CH;
     const std::int64_t left = E - e0;
     const int len = static_cast<int>(left < CH ? left : CH);  // a multiple of 4
+    PHM_DCHECK((len & 3) == 0 && B >= 1 && B <= kInstBatchMax);
     mbar_wait(&full[slot], (c / NST) & 1);
     const double* S = sm + slot * R * CH;
     for (int q = tid; q < (len >> 2); q += 256) {
@@ -1533,6 +1553,7 @@ __global__ void __launch_bounds__(128) k_near_gather(const std::int64_t* __restr
       double s = 0.0;
       for (int k = sb; k < se; ++k) {
         const GatherSeg g = segs[k];
+        PHM_DCHECK(g.base >= 0 && g.len >= 0 && g.base + g.len <= rows);
         const int o = r - g.base;
         if (o >= 0 && o < g.len) s += pc[g.poff + o];
       }
