@@ -516,3 +516,22 @@ def test_clustered_points_large_leaves(ph, po):
         assert rel(inst.apply(X), oi.apply(X)) <= TOL_Y
     x = rng.standard_normal(n)
     assert rel(inst.instantiate_apply([0.33, 0.7], x), om.instantiate([0.33, 0.7]).apply(x)) <= TOL_Y
+
+
+@pytest.mark.parametrize("n,d,l_max", [(1, 3, 2), (7, 2, 2), (33, 1, 3), (200, 3, 0)])
+def test_tiny_and_degenerate_sizes(ph, po, n, d, l_max):
+    """Edge cases: a single point, fewer points than leaves (empty leaves),
+    1D, and l_max = 0 (one leaf, no far field) through every entry point."""
+    pts = ph.generate_points(n, d, 5)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=l_max, p_s=3, p_theta=5, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    for fmt in (ph.Format.H2, ph.Format.H):
+        pm, om = _build(ph, po, pts, cfg, fmt)
+        inst = ph.instantiate(pm, [0.2])
+        oi = om.instantiate([0.2])
+        x = ph.generate_normal(n, 1)
+        assert rel(inst.apply(x), oi.apply(x)) <= TOL_Y
+        X = np.stack([x, 2 * x, ph.generate_normal(n, 2), x, x], axis=1)
+        assert rel(inst.apply(X), oi.apply(X)) <= TOL_Y
+        assert rel(inst.instantiate_apply([0.4], x), om.instantiate([0.4]).apply(x)) <= TOL_Y
+        assert rel(inst.to_dense(), om.instantiate([0.4]).to_dense()) <= TOL_Y
