@@ -57,6 +57,8 @@ void launch_near_tma_apply(cudaStream_t, const SymRowItem*, int, const SymBlock*
                            double*, int*);
 void launch_near_mrhs2(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
                        std::int64_t, int, std::int64_t, double*);
+void launch_near_mrhs3(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
+                       std::int64_t, int, std::int64_t, double*);
 void launch_near_mvm_symcsr(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
                             double*);
 bool launch_near_inst_tma(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, std::int64_t, int,
@@ -398,7 +400,8 @@ constexpr Index kMrhsMin = 4;
 
 void ensure_workspace(DevMatrix& M, Index m) {
   if (M.ws_m >= m) return;
-  M.xp.alloc(sizeof(double) * M.n * m);
+  // +4: the TMA panel copies of K9 may read one double past a column
+  M.xp.alloc(sizeof(double) * (M.n * m + 4));
   M.yp.alloc(sizeof(double) * M.n * m);
   M.xdev.alloc(sizeof(double) * M.n * m);
   M.ydev.alloc(sizeof(double) * M.n * m);
@@ -1536,9 +1539,17 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
   if (m >= kMrhsMin && M.n_sym_items > 0 && two_sided && (m <= 32 || (M.sym && M.sharded))) {
     const size_t need = sizeof(double) * M.sym_pstride * m;
     if (M.sym_part_m.bytes < need) M.sym_part_m.alloc(need);
+    static const int k9v = [] {
+      const char* e = std::getenv("PHM_K9_TMA");
+      return e ? std::atoi(e) : 1;
+    }();
     ctx.run_on(st, "near_mrhs", [&] {
-      dev::launch_near_mrhs2(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items, M.sym_blocks.as<dev::SymBlock>(),
-                             I.D.as<double>(), M.xp.as<double>(), M.n, mm, M.sym_pstride, M.sym_part_m.as<double>());
+      if (k9v == 1 && m <= 32)
+        dev::launch_near_mrhs3(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items, M.sym_blocks.as<dev::SymBlock>(),
+                               I.D.as<double>(), M.xp.as<double>(), M.n, mm, M.sym_pstride, M.sym_part_m.as<double>());
+      else
+        dev::launch_near_mrhs2(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items, M.sym_blocks.as<dev::SymBlock>(),
+                               I.D.as<double>(), M.xp.as<double>(), M.n, mm, M.sym_pstride, M.sym_part_m.as<double>());
     });
     ctx.run_on(st, "near_gather", [&] {
       dev::launch_near_gather(st, M.n_gather_leaves, M.g_row0.as<std::int64_t>(), M.g_rows.as<std::int32_t>(),

@@ -1528,6 +1528,180 @@ __global__ void __maxnreg__(96) k_inst_tma(const double* __restrict__ G, std::in
 }
 
 
+// K9, two-sided over TMA (k_near_mrhs3): k_near_mrhs2's products with the
+// staging moved to a producer warp. Per 32-column chunk its lanes issue one
+// cp.async.bulk per D column (into the padded column-major chunk; a column
+// that starts 8 bytes past a 16-byte boundary is copied from the aligned
+// address below and read with a one-element shift) and one per RHS column of
+// the X_tau panel; a 2-stage ring with full/empty mbarriers decouples them
+// from the 8 consumer warps, which only run DMMA. Reads past the chunk (odd
+// lengths, k beyond the chunk, rows beyond the slice) are masked to zero
+// before they reach an MMA, so stale shared memory never contributes.
+template <int NC>
+__global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ items,
+                                              const SymBlock* __restrict__ blocks, const double* __restrict__ D,
+                                              const double* __restrict__ X, std::int64_t n, int m,
+                                              std::int64_t pstride, double* __restrict__ part) {
+  constexpr int NTN = NC / 8;
+  constexpr int YQ = NC / 8;  // Y (m-tile, n-tile) pairs per consumer warp (<= 8 m-tiles x NTN / 8 warps)
+  constexpr int LDX = kK9bKc + 4;
+  constexpr int STAGE = kK9bKc * kK9bLd + NC * LDX;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) std::uint64_t full[2], empty[2];
+  double* Xs = sm;                      // X_sigma: [c][r], ld 132 (consumers stage it)
+  double* St = sm + NC * kK9bLd;        // 2 stages: D chunk [k][shift + r] then X_tau [c][shift + k]
+  const SymRowItem it = items[blockIdx.x];
+  const int c0 = blockIdx.y * NC;
+  const int ncr = min(NC, m - c0);      // RHS columns of this tile
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t0 = lane & 3;
+  const int R = it.rows;
+  const std::int64_t ld = it.ld;
+  const int R4 = (R + 3) & ~3;
+  const int mtiles = (R + 15) >> 4;
+  const int ypairs = mtiles * NTN;
+  PHM_DCHECK(R >= 1 && R <= 128 && it.i0 + R <= it.ld);
+  if (tid == 0) {
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 8) {  // --------------------------------------------- producer
+    int c = 0;
+    for (int b = it.bbeg; b < it.bend; ++b) {
+      const SymBlock blk = blocks[b];
+      for (int j0 = 0; j0 < blk.ncol; j0 += kK9bKc, ++c) {
+        const int slot = c & 1;
+        if (c >= 2) mbar_wait(&empty[slot], ((c >> 1) - 1) & 1);
+        const int kc = min(kK9bKc, blk.ncol - j0);
+        double* Dc = St + slot * STAGE;
+        double* Xt = Dc + kK9bKc * kK9bLd;
+        // lane k: column k of the chunk; lane c (< ncr): RHS column c of X_tau
+        unsigned bytes_d = 0, bytes_x = 0;
+        const double* src_d = nullptr;
+        const double* src_x = nullptr;
+        if (lane < kc) {
+          const double* col = D + blk.d_off + it.i0 + static_cast<std::int64_t>(j0 + lane) * ld;
+          const int sh = static_cast<int>((reinterpret_cast<std::uintptr_t>(col) >> 3) & 1);
+          src_d = col - sh;
+          bytes_d = static_cast<unsigned>(((R + sh + 1) & ~1) * 8);
+        }
+        if (lane < ncr) {
+          const double* xc = X + blk.x_col0 + j0 + static_cast<std::int64_t>(c0 + lane) * n;
+          const int sh = static_cast<int>((reinterpret_cast<std::uintptr_t>(xc) >> 3) & 1);
+          src_x = xc - sh;
+          bytes_x = static_cast<unsigned>(((kc + sh + 1) & ~1) * 8);
+        }
+        unsigned total = bytes_d + bytes_x;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+        if (lane == 0) mbar_expect_tx(&full[slot], total);
+        __syncwarp();
+        if (bytes_d) bulk_g2s(Dc + lane * kK9bLd, src_d, bytes_d, &full[slot]);
+        if (bytes_x) bulk_g2s(Xt + lane * LDX, src_x, bytes_x, &full[slot]);
+      }
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  for (int q = tid; q < NC * R4; q += 256) {  // X_sigma, zero beyond the slice / the RHS count
+    const int cc = q / R4, r = q - cc * R4;
+    Xs[cc * kK9bLd + r] = (cc < ncr && r < R) ? X[it.x_row0 + r + static_cast<std::int64_t>(c0 + cc) * n] : 0.0;
+  }
+  consumers_sync();
+  double yacc[YQ][4];
+#pragma unroll
+  for (int q = 0; q < YQ; ++q) yacc[q][0] = yacc[q][1] = yacc[q][2] = yacc[q][3] = 0.0;
+  int c = 0;
+  for (int b = it.bbeg; b < it.bend; ++b) {
+    const SymBlock blk = blocks[b];
+    const std::uintptr_t dbase = reinterpret_cast<std::uintptr_t>(D + blk.d_off + it.i0);
+    for (int j0 = 0; j0 < blk.ncol; j0 += kK9bKc, ++c) {
+      const int slot = c & 1;
+      const int kc = min(kK9bKc, blk.ncol - j0);
+      mbar_wait(&full[slot], (c >> 1) & 1);
+      const double* Dc = St + slot * STAGE;
+      const double* Xt = Dc + kK9bKc * kK9bLd;
+      // element (r, k) of the chunk sits at Dc[k * 132 + sh(k) + r]
+      auto dsh = [&](int k) { return static_cast<int>(((dbase >> 3) + static_cast<std::uintptr_t>((j0 + k) * ld)) & 1); };
+      const int ksy = (kc + 3) >> 2;
+      // Y_sigma += D(:, chunk) X_tau(chunk, :)
+#pragma unroll
+      for (int q = 0; q < YQ; ++q) {
+        const int p = warp + 8 * q;
+        if (p < ypairs) {
+          const int mt = p / NTN, nt = p - mt * NTN;
+          const int ncol_b = 8 * nt + g;  // this lane's B column
+          const int xsh = ncol_b < ncr ? static_cast<int>(((reinterpret_cast<std::uintptr_t>(
+                                                               X + blk.x_col0 + j0 + static_cast<std::int64_t>(c0 + ncol_b) * n)) >> 3) & 1)
+                                       : 0;
+          for (int s2 = 0; s2 < ksy; ++s2) {
+            const int k = 4 * s2 + t0;
+            const bool kin = k < kc;
+            const int sh = kin ? dsh(k) : 0;
+            const double a0 = kin ? Dc[k * kK9bLd + sh + 16 * mt + g] : 0.0;
+            const double a1 = kin ? Dc[k * kK9bLd + sh + 16 * mt + g + 8] : 0.0;
+            const double b0 = (kin && ncol_b < ncr) ? Xt[ncol_b * LDX + xsh + k] : 0.0;
+            dmma_16x8x4(yacc[q], a0, a1, b0);
+          }
+        }
+      }
+      // Z_tau(chunk, :) = D(:, chunk)^T X_sigma (off-diagonal blocks)
+      if (blk.p_col >= 0) {
+        const int zpairs = ((kc + 15) >> 4) * NTN;
+        for (int p = warp; p < zpairs; p += 8) {
+          const int mt = p / NTN, nt = p - mt * NTN;
+          const int j_a0 = 16 * mt + g, j_a1 = j_a0 + 8;  // chunk columns of this lane's A rows
+          const bool in0 = j_a0 < kc, in1 = j_a1 < kc;
+          const int sh0 = in0 ? dsh(j_a0) : 0, sh1 = in1 ? dsh(j_a1) : 0;
+          double z[4] = {0.0, 0.0, 0.0, 0.0}, z1[4] = {0.0, 0.0, 0.0, 0.0};
+          const int ksz = R4 >> 2;
+          int s2 = 0;
+          for (; s2 + 1 < ksz; s2 += 2) {
+            const int k = 4 * s2 + t0;
+            dmma_16x8x4(z, (in0 && k < R) ? Dc[j_a0 * kK9bLd + sh0 + k] : 0.0,
+                        (in1 && k < R) ? Dc[j_a1 * kK9bLd + sh1 + k] : 0.0, Xs[(8 * nt + g) * kK9bLd + k]);
+            dmma_16x8x4(z1, (in0 && k + 4 < R) ? Dc[j_a0 * kK9bLd + sh0 + k + 4] : 0.0,
+                        (in1 && k + 4 < R) ? Dc[j_a1 * kK9bLd + sh1 + k + 4] : 0.0, Xs[(8 * nt + g) * kK9bLd + k + 4]);
+          }
+          if (s2 < ksz) {
+            const int k = 4 * s2 + t0;
+            dmma_16x8x4(z, (in0 && k < R) ? Dc[j_a0 * kK9bLd + sh0 + k] : 0.0,
+                        (in1 && k < R) ? Dc[j_a1 * kK9bLd + sh1 + k] : 0.0, Xs[(8 * nt + g) * kK9bLd + k]);
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) z[e] += z1[e];
+#pragma unroll
+          for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+              const int j = 16 * mt + g + 8 * r2, col = c0 + 8 * nt + 2 * t0 + cc;
+              if (j < kc && col < m) part[static_cast<std::int64_t>(col) * pstride + blk.p_col + j0 + j] = z[2 * r2 + cc];
+            }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the stage
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < YQ; ++q) {
+    const int p = warp + 8 * q;
+    if (p < ypairs) {
+      const int mt = p / NTN, nt = p - mt * NTN;
+#pragma unroll
+      for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int r = 16 * mt + g + 8 * r2, col = c0 + 8 * nt + 2 * t0 + cc;
+          if (r < R && col < m) part[static_cast<std::int64_t>(col) * pstride + it.p_row + r] = yacc[q][2 * r2 + cc];
+        }
+    }
+  }
+}
+
 // y[rows of leaf] = sum of the leaf's partial segments, in list order. Small
 // leaves: a thread per row walks the segments. Large leaves (clustered
 // points): the rows are accumulated in shared memory (chunks of 4096 rows)
@@ -2079,6 +2253,23 @@ void launch_near_gather(cudaStream_t st, int nleaves, const std::int64_t* leaf_r
                         std::int64_t n, int m, double* yp) {
   if (nleaves == 0 || m == 0) return;
   k_near_gather<<<dim3(nleaves, m), 128, 0, st>>>(leaf_row0, leaf_rows, seg_beg, segs, part, pstride, n, yp);
+}
+
+void launch_near_mrhs3(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks, const double* D,
+                       const double* X, std::int64_t n, int m, std::int64_t pstride, double* part) {
+  if (nitems == 0) return;
+#define PHM_K9C(NC)                                                                                         \
+  {                                                                                                         \
+    const size_t smem = (NC * kK9bLd + 2 * (kK9bKc * kK9bLd + NC * (kK9bKc + 4))) * sizeof(double);       \
+    smem_attr(reinterpret_cast<const void*>(k_near_mrhs3<NC>), static_cast<int>(smem), true);              \
+    const dim3 grid(static_cast<unsigned>(nitems), static_cast<unsigned>((m + NC - 1) / NC));               \
+    k_near_mrhs3<NC><<<grid, kTmaThreads, smem, st>>>(items, blocks, D, X, n, m, pstride, part);            \
+    return;                                                                                                 \
+  }
+  if (m <= 8) PHM_K9C(8)
+  if (m <= 16) PHM_K9C(16)
+  PHM_K9C(32)
+#undef PHM_K9C
 }
 
 void launch_near_mrhs2(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks, const double* D,
