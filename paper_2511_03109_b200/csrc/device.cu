@@ -1533,9 +1533,9 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
     return !(e && std::atoi(e) == 0);
   }();
   // up to 32 RHS: each stored block read once, both products on DMMA
-  // (k_near_mrhs2; C3 at 10 RHS 6.4 -> 5.0 ms). At 64 RHS its 172 KB of
-  // shared memory leaves one CTA per SM and the one-sided K9 is faster
-  // (13.8 vs 15.1 ms), except on a symmetric shard, which needs both sides.
+  // (k_near_mrhs3, TMA-staged: C3 at 10 RHS 3.5 ms against 6.4 for the
+  // one-sided K9). At 64 RHS the one-sided K9 is faster (13.8 vs 16.8 ms +
+  // 3.3 ms of gather), except on a symmetric shard, which needs both sides.
   if (m >= kMrhsMin && M.n_sym_items > 0 && two_sided && (m <= 32 || (M.sym && M.sharded))) {
     const size_t need = sizeof(double) * M.sym_pstride * m;
     if (M.sym_part_m.bytes < need) M.sym_part_m.alloc(need);
@@ -1544,7 +1544,7 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
       return e ? std::atoi(e) : 1;
     }();
     ctx.run_on(st, "near_mrhs", [&] {
-      if (k9v == 1 && m <= 32)
+      if (k9v == 1)
         dev::launch_near_mrhs3(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items, M.sym_blocks.as<dev::SymBlock>(),
                                I.D.as<double>(), M.xp.as<double>(), M.n, mm, M.sym_pstride, M.sym_part_m.as<double>());
       else
