@@ -1773,15 +1773,11 @@ void instantiate_apply_sequence(DevInstance& I, const double* x_dev, Index m, St
   far_finish(I, m, st);
 }
 
-
-// instantiate(theta) followed by apply(x), scheduled as one graph of work:
-// the class stage and the whole H^2 far chain (compute-bound: K2, K3-K5, K7)
-// run on the side stream while K1 streams the near field on the main
-// stream; the near GEMV then waits for the gathered x and the far chain.
-// Results are identical to reinstantiate() + apply_device().
 namespace {
 // instantiate(theta) + apply(x) leaving y (this shard's part) in tree order
-// in M.yp.
+// in M.yp: put_theta, then instantiate_apply_sequence (replayed as a CUDA
+// graph). H form and direct mode run instantiate and apply one after the
+// other. y equals reinstantiate() + apply_device() to rounding (D bitwise).
 void instantiate_apply_tree(DevInstance& I, const double* theta, int n_theta, const double* x_dev, Index m,
                             StageCounters* counters) {
   DevMatrix& M = *I.M;
