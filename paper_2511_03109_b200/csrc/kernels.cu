@@ -2315,7 +2315,10 @@ void launch_coupling_mma(cudaStream_t st, const CouplingItem* items, int nitems,
                          const std::uint8_t* item_tiles, const std::int32_t* cls_tau, const double* C, int P,
                          const double* xhat, int m, double* partial) {
   if (nitems == 0) return;
-  const int mc = m >= 2 ? 2 : 1;
+  // one RHS column per CTA (grid.y walks the columns): at C3 it beat two
+  // columns sharing each C_k fragment load at every m measured (4: 3.3 vs
+  // 3.5 ms, 10: 7.9 vs 8.4, 64: 49.4 vs 52.2) -- occupancy over reuse
+  const int mc = 1;
   const size_t smem = 2 * mc * kGroupSlots * (P + 4) * sizeof(double);
   const dim3 grid(static_cast<unsigned>(nitems), static_cast<unsigned>((m + mc - 1) / mc));
 #define PHM_CASE(PP, MC)                                                                                    \
@@ -2326,13 +2329,9 @@ void launch_coupling_mma(cudaStream_t st, const CouplingItem* items, int nitems,
     return;                                                                                                 \
   }
   PHM_CASE(16, 1)
-  PHM_CASE(16, 2)
   PHM_CASE(32, 1)
-  PHM_CASE(32, 2)
   PHM_CASE(64, 1)
-  PHM_CASE(64, 2)
   PHM_CASE(128, 1)
-  PHM_CASE(128, 2)
 #undef PHM_CASE
 }
 
