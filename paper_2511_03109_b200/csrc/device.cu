@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -38,6 +39,8 @@ void launch_near_w(cudaStream_t, const NearW*, std::int64_t, const double*, cons
                    double*);
 void launch_set_vec(cudaStream_t, double*, int, const ThetaParams*);
 void launch_put_theta(cudaStream_t, const ThetaParams&, ThetaParams*);
+void launch_stamp(cudaStream_t, unsigned long long*, int);
+void launch_zero(cudaStream_t, double*, std::int64_t);
 void launch_class_inst(cudaStream_t, const ClassMeta*, int, const double*, const std::int32_t*, const double*,
                        const double*, const ThetaParams*, int, bool, int, int, int, int, double*, double*);
 void launch_gather(cudaStream_t, const double*, const std::int32_t*, std::int64_t, std::int64_t, double*);
@@ -49,8 +52,10 @@ void launch_up(cudaStream_t, const std::int32_t*, int, const std::int32_t*, cons
 void launch_coupling(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*,
                      const std::int32_t*, const double*, int, int, const double*, double*);
 bool coupling_mma_supported(int P);
-void launch_coupling_mma(cudaStream_t, const CouplingItem*, int, const std::int32_t*, const std::uint8_t*,
-                         const std::int32_t*, const double*, int, const double*, int, double*);
+int coupling_beside_near(int R, int P);
+void launch_coupling_mma(cudaStream_t, const CouplingItem*, const std::int32_t*, int, const std::int32_t*,
+                         const std::uint8_t*,
+                         const std::int32_t*, const double*, int, const double*, int, double*, int);
 void launch_coupling_reduce(cudaStream_t, const std::int32_t*, const std::int32_t*, int, const double*, int, int,
                             double*);
 void launch_near_tma_apply(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
@@ -144,6 +149,7 @@ struct NvtxRange {
 
 struct Context {
   int device = 0;
+  int sms = 148;  // multiprocessors of the device
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   bool timing = false;
@@ -165,6 +171,7 @@ struct Context {
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (join_ev) cudaEventDestroy(join_ev);
     if (aux_ev) cudaEventDestroy(aux_ev);
+    if (stamps) cudaFree(stamps);
     if (side) cudaStreamDestroy(side);
     if (own) cudaStreamDestroy(own);
   }
@@ -190,6 +197,7 @@ struct Context {
     if (!timing) {
       f();
       CK(cudaGetLastError());
+      keep_priority(s);
       return;
     }
     Rec r{name, ev(), ev()};
@@ -198,6 +206,51 @@ struct Context {
     CK(cudaGetLastError());
     CK(cudaEventRecord(r.b, s));
     recs.push_back(r);
+  }
+  // Under stream capture, give the kernel node just captured on s the
+  // priority of s: graph nodes otherwise carry no priority, and the far
+  // chain would queue behind the near pass's CTAs instead of taking SM
+  // slots beside it (graphs are instantiated with UseNodePriority).
+  static void keep_priority(cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &deps, &nd));
+    if (cs != cudaStreamCaptureStatusActive) return;
+    int prio = 0;
+    CK(cudaStreamGetPriority(s, &prio));
+    for (size_t i = 0; i < nd; ++i) {
+      cudaGraphNodeType t;
+      CK(cudaGraphNodeGetType(deps[i], &t));
+      if (t != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeAttrValue v{};
+      v.priority = prio;
+      CK(cudaGraphKernelNodeSetAttribute(deps[i], cudaKernelNodeAttributePriority, &v));
+    }
+  }
+  // PHM_STAMPS=1: device-clock stamps at fixed points of the fused step,
+  // printed to stderr after each step (schedule diagnostics only)
+  unsigned long long* stamps = nullptr;
+  static bool stamps_on() {
+    static const bool on = [] {
+      const char* e = std::getenv("PHM_STAMPS");
+      return e && std::atoi(e) == 1;
+    }();
+    return on;
+  }
+  void stamp(cudaStream_t s, int id) {
+    if (!stamps_on()) return;
+    if (!stamps) CK(cudaMallocManaged(&stamps, 16 * sizeof(unsigned long long)));
+    dev::launch_stamp(s, stamps, id);
+    keep_priority(s);
+  }
+  void print_stamps() {
+    if (!stamps_on() || !stamps) return;
+    CK(cudaDeviceSynchronize());
+    std::fprintf(stderr, "stamps(us):");
+    for (int i = 1; i < 16; ++i)
+      if (stamps[i] >= stamps[0]) std::fprintf(stderr, " %d:%.1f", i, (stamps[i] - stamps[0]) * 1e-3);
+    std::fprintf(stderr, "\n");
   }
   // Second stream for the H^2 far-field chain, which overlaps the near-field
   // GEMV (compute-bound DMMA next to an HBM stream); fork/join by events.
@@ -238,6 +291,7 @@ std::shared_ptr<Context> context_create(int device) {
                                                  std::to_string(prop.major) + std::to_string(prop.minor));
   auto ctx = std::make_shared<Context>();
   ctx->device = device;
+  ctx->sms = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
   {
     // the side stream carries the compute-bound far chain that runs beside
@@ -324,7 +378,7 @@ struct DevMatrix {
   int n_cp_sig = 0;
   // H^2 coupling, grouped DMMA path (P in {16, 32, 64, 128})
   bool cp_mma = false;
-  DBuf cg_items, cg_cls, cg_tiles, cg_tau, cg_grp_sigma, cg_grp_items, cg_partial;
+  DBuf cg_items, cg_order, cg_cls, cg_tiles, cg_tau, cg_grp_sigma, cg_grp_items, cg_partial;
   int n_cg_items = 0, n_cg_groups = 0;
   // H form far CSR by level
   DBuf fh_items, fh_tb, fh_tn, fh_cls, fh_soff, fh_toff, fh_S, fh_T, fh_bitem, fh_poff, fh_part;
@@ -759,12 +813,12 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     // splits each leaf's blocks over several items, so the near pass does
     // not end on a partial wave of long CTAs; the unsharded C3 keeps one
     // item per leaf.
-    std::size_t kItemBlocks = 128;
+    std::size_t kItemBlocks = dev::kTmaMaxBlocks;
     {
       std::size_t total = 0;
       for (const auto& o : owned) total += o.size();
       const std::size_t target = 8 * 2 * 148;
-      kItemBlocks = std::min<std::size_t>(128, std::max<std::size_t>(8, (total + target - 1) / target));
+      kItemBlocks = std::min<std::size_t>(dev::kTmaMaxBlocks, std::max<std::size_t>(8, (total + target - 1) / target));
     }
     for (int s = 0; s < M.nnodes; ++s) {
       if (owned[s].empty()) continue;
@@ -1021,6 +1075,30 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
       }
       M.n_cg_items = static_cast<int>(items.size());
       M.n_cg_groups = static_cast<int>(grp_items.size()) - 1;
+      // Traversal order: by (level, first class, group), so that the CTAs
+      // running at one time stream the same C_k (L2 hits instead of HBM
+      // re-reads while the near pass floods L2); partial sums stay indexed by
+      // item, so the reduction order does not change.
+      {
+        std::vector<int> grp_level(M.n_cg_groups);
+        for (int g = 0; g < M.n_cg_groups; ++g) grp_level[g] = T.nodes[grp_sigma[g * kSlots]].level;
+        std::vector<std::int32_t> order(items.size());
+        for (size_t i = 0; i < items.size(); ++i) order[i] = static_cast<std::int32_t>(i);
+        std::stable_sort(order.begin(), order.end(), [&](std::int32_t a, std::int32_t b) {
+          const auto& ia = items[a];
+          const auto& ib = items[b];
+          const auto ka = std::make_tuple(grp_level[ia.group], item_cls[ia.e_begin], ia.group);
+          const auto kb = std::make_tuple(grp_level[ib.group], item_cls[ib.e_begin], ib.group);
+          return ka < kb;
+        });
+        static const bool ordered = [] {
+          const char* e = std::getenv("PHM_COUPLING_ORDER");
+          return !(e && std::atoi(e) == 0);
+        }();
+        if (!ordered)
+          for (size_t i = 0; i < items.size(); ++i) order[i] = static_cast<std::int32_t>(i);
+        upload(M.cg_order, order, st);
+      }
       upload(M.cg_items, items, st);
       upload(M.cg_cls, item_cls, st);
       upload(M.cg_tiles, item_tiles, st);
@@ -1456,7 +1534,7 @@ namespace {
 
 // H^2 far-field chain on stream fs: forward (K3, K4), coupling (K5),
 // downward (K7 internal). Reads xp and C_k; writes yhat.
-void far_chain(DevInstance& I, Index m, cudaStream_t fs) {
+void far_chain(DevInstance& I, Index m, cudaStream_t fs, int coupling_ctas) {
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   Context& ctx = *M.ctx;
@@ -1476,15 +1554,20 @@ void far_chain(DevInstance& I, Index m, cudaStream_t fs) {
                      M.ps, P, mm, M.xhat.as<double>());
     });
   }
-  CK(cudaMemsetAsync(M.yhat.p, 0, sizeof(double) * M.nnodes * P * m, fs));
+  // a kernel, not a memset: a memset node of a graph carries no priority and
+  // would wait behind the near pass's CTAs
+  ctx.run_on(fs, "zero", [&] { dev::launch_zero(fs, M.yhat.as<double>(), static_cast<std::int64_t>(M.nnodes) * P * m); });
   if (M.cp_mma) {
     const size_t need = sizeof(double) * std::max(1, M.n_cg_items) * m * dev::kGroupSlots * P;
     if (M.cg_partial.bytes < need) M.cg_partial.alloc(need);
+    ctx.stamp(fs, 5);
     ctx.run_on(fs, "coupling", [&] {
-      dev::launch_coupling_mma(fs, M.cg_items.as<dev::CouplingItem>(), M.n_cg_items, M.cg_cls.as<std::int32_t>(),
+      dev::launch_coupling_mma(fs, M.cg_items.as<dev::CouplingItem>(), M.cg_order.as<std::int32_t>(), M.n_cg_items,
+                               M.cg_cls.as<std::int32_t>(),
                                M.cg_tiles.as<std::uint8_t>(), M.cg_tau.as<std::int32_t>(), I.C.as<double>(), P,
-                               M.xhat.as<double>(), mm, M.cg_partial.as<double>());
+                               M.xhat.as<double>(), mm, M.cg_partial.as<double>(), coupling_ctas);
     });
+    ctx.stamp(fs, 6);
     ctx.run_on(fs, "coupling_reduce", [&] {
       dev::launch_coupling_reduce(fs, M.cg_grp_sigma.as<std::int32_t>(), M.cg_grp_items.as<std::int32_t>(),
                                   M.n_cg_groups, M.cg_partial.as<double>(), P, mm, M.yhat.as<double>());
@@ -1627,20 +1710,20 @@ void apply_tree_order(DevInstance& I, Index m) {
     return e ? std::atoi(e) : 1;
   }();
   if (M.h2 && overlap == 0) {  // serial: far chain, then the near GEMV
-    far_chain(I, m, ctx.stream);
+    far_chain(I, m, ctx.stream, 0);
     near_product(I, m, ctx.stream);
     far_finish(I, m, ctx.stream);
     return;
   }
   if (M.h2 && overlap == 2) {  // serial: near GEMV first
     near_product(I, m, ctx.stream);
-    far_chain(I, m, ctx.stream);
+    far_chain(I, m, ctx.stream, 0);
     far_finish(I, m, ctx.stream);
     return;
   }
   if (M.h2) {
     ctx.fork();
-    far_chain(I, m, ctx.side);
+    far_chain(I, m, ctx.side, 0);
   }
   near_product(I, m, ctx.stream);
   if (M.h2) ctx.join();
@@ -1689,7 +1772,26 @@ void run_graphed(DevInstance& I, int seq, const void* input, Index m, F&& body) 
       throw;
     }
     CK(cudaStreamEndCapture(ctx.stream, &graph));
-    CK(cudaGraphInstantiate(&g.exec, graph, 0));
+    if (Context::stamps_on()) {
+      size_t nn = 0;
+      CK(cudaGraphGetNodes(graph, nullptr, &nn));
+      std::vector<cudaGraphNode_t> nodes(nn);
+      CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+      int nk = 0, np = 0;
+      for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        CK(cudaGraphNodeGetType(nd, &t));
+        if (t != cudaGraphNodeTypeKernel) continue;
+        ++nk;
+        cudaKernelNodeAttrValue v{};
+        CK(cudaGraphKernelNodeGetAttribute(nd, cudaKernelNodeAttributePriority, &v));
+        if (v.priority != 0) ++np;
+      }
+      std::fprintf(stderr, "graph: %zu nodes, %d kernels, %d with priority\n", nn, nk, np);
+    }
+    // keep the side stream's priority per node (a graph otherwise runs every
+    // node at the priority of the stream it is launched into)
+    CK(cudaGraphInstantiate(&g.exec, graph, cudaGraphInstantiateFlagUseNodePriority));
     CK(cudaGraphDestroy(graph));
     g.launches = ctx.launches - l0;
     ctx.launches = l0;  // counted when the graph runs
@@ -1734,31 +1836,53 @@ void instantiate_apply_sequence(DevInstance& I, const double* x_dev, Index m, St
   DevMatrix& M = *I.M;
   Context& ctx = *M.ctx;
   cudaStream_t st = ctx.stream, fs = ctx.side;
+  ctx.stamp(st, 0);
   ctx.fork();  // side stream sees x (and everything before) as ready
+  ctx.stamp(fs, 1);
   ctx.run_on(fs, "gather", [&] { dev::launch_gather(fs, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
+  ctx.stamp(fs, 9);
   CK(cudaEventRecord(ctx.aux_ev, fs));
   inst_classes(I, fs);
-  far_chain(I, m, fs);
+  ctx.stamp(fs, 2);
+  // The coupling as a capped grid that stays resident beside the fused near
+  // pass (one CTA per SM where it fits next to the pass's two) instead of
+  // taking the pass's SM slots as its CTAs retire: C3 9.6 -> 9.2 ms per step
+  // (DESIGN.md). PHM_COUPLING_RESIDENT=0 restores the full grid.
+  static const int resident_env = [] {
+    const char* e = std::getenv("PHM_COUPLING_RESIDENT");
+    return e ? std::atoi(e) : -1;
+  }();
+  static const bool use_fused = [] {
+    const char* e = std::getenv("PHM_FUSED_NEAR");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool fuse = use_fused && M.near_tma && M.mode == NearMode::Snapshot && m == 1;
+  int coupling_ctas = 0;
+  if (fuse && M.cp_mma && resident_env != 0) {
+    const int fit = dev::coupling_beside_near(M.R_snap, M.P);
+    const int per_sm = resident_env > 0 ? resident_env : std::min(fit, 1);
+    coupling_ctas = per_sm * ctx.sms;
+  }
+  far_chain(I, m, fs, coupling_ctas);
   bool fused = false;
   // Snapshot mode, one vector: K1 and K6 fused into one TMA pass over the
   // snapshots (k_near_tma) -- 10.8 ms at C3 against 9.8 + 1.6 ms for the
   // separate kernels. D is bit-identical to K1's; y agrees with the separate
   // path to rounding (row sums are accumulated in a different order).
   // PHM_FUSED_NEAR=0 selects the separate kernels.
-  static const bool use_fused = [] {
-    const char* e = std::getenv("PHM_FUSED_NEAR");
-    return !(e && std::atoi(e) == 0);
-  }();
-  if (use_fused && M.near_tma && M.mode == NearMode::Snapshot && m == 1) {
+  if (fuse) {
     // one pass over the snapshots: D is formed, stored and multiplied at once
     inst_snapshot_w(I, st);
+    ctx.stamp(st, 10);
     CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
+    ctx.stamp(st, 3);
     ctx.run_on(st, "near_inst_mvm", [&] {
       fused = dev::launch_near_inst_tma(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items,
                                         M.sym_blocks.as<dev::SymBlock>(), M.G.as<double>(), M.E, M.R_snap,
                                         I.w.as<double>(), I.D.as<double>(), M.xp.as<double>(),
                                         M.sym_part.as<double>());
     });
+    ctx.stamp(st, 4);
     if (fused) {
       if (M.n_gather_leaves == 0 || M.sharded) CK(cudaMemsetAsync(M.yp.p, 0, sizeof(double) * M.n * m, st));
       near_gather(I, 0, st);
@@ -1769,8 +1893,10 @@ void instantiate_apply_sequence(DevInstance& I, const double* x_dev, Index m, St
     CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
     near_product(I, m, st);
   }
+  ctx.stamp(fs, 7);
   ctx.join();
   far_finish(I, m, st);
+  ctx.stamp(st, 8);
 }
 
 namespace {
@@ -1813,6 +1939,7 @@ void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, 
   M.ctx->run("scatter", [&] {
     dev::launch_scatter(M.st(), M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev);
   });
+  M.ctx->print_stamps();
 }
 
 void instantiate_apply_partial_device(DevInstance& I, const double* theta, int n_theta, const double* x_dev,

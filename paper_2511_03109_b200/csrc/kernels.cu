@@ -312,6 +312,26 @@ __global__ void k_set_vec(double* dst, int n, const ThetaParams* __restrict__ tp
   dst[i] = s * tp->amp;
 }
 
+// Schedule diagnostics (PHM_STAMPS=1): the device clock when the stream
+// reaches this point.
+__global__ void k_stamp(unsigned long long* __restrict__ buf, int id) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  buf[id] = t;
+}
+void launch_stamp(cudaStream_t st, unsigned long long* buf, int id) { k_stamp<<<1, 1, 0, st>>>(buf, id); }
+
+__global__ void k_zero(double* __restrict__ p, std::int64_t n) {
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    p[i] = 0.0;
+}
+void launch_zero(cudaStream_t st, double* p, std::int64_t n) {
+  if (n <= 0) return;
+  const std::int64_t blocks = std::min<std::int64_t>((n + 255) / 256, 4 * 148);
+  k_zero<<<static_cast<int>(blocks), 256, 0, st>>>(p, n);
+}
+
 __global__ void k_put_theta(ThetaParams p, ThetaParams* __restrict__ dst) {
   const int n = sizeof(ThetaParams) / sizeof(double);
   static_assert(sizeof(ThetaParams) % sizeof(double) == 0, "ThetaParams is copied as doubles");
@@ -630,107 +650,106 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// MC right-hand-side columns per CTA share every C_k fragment load
-// (grid.y walks the column chunks); X holds MC gathered 32-slot panels.
-// item_tiles[e] has bit j set when n-tile j (slots 8j .. 8j + 7) holds any
-// partner of class item_cls[e]; empty tiles skip their MMAs and loads
-// (the slot order of a group is Morton order, so boundary sigmas missing an
-// offset cluster: at C3 this lifts the useful fraction of the MMA work from
-// 64% to 83%).
-template <int P, int MC>
-__global__ void __launch_bounds__(P / 16 * 32) k_coupling_mma(const CouplingItem* __restrict__ items,
+// One (item, RHS column) pair per CTA iteration; X is the gathered 32-slot
+// panel of the column, double-buffered. item_tiles[e] has bit j set when
+// n-tile j (slots 8j .. 8j + 7) holds any partner of class item_cls[e];
+// empty tiles skip their MMAs and loads (the slot order of a group is Morton
+// order, so boundary sigmas missing an offset cluster: at C3 this lifts the
+// useful fraction of the MMA work from 64% to 83%).
+// The C_k fragments are loaded in two k-halves per class (registers for
+// occupancy; each half still feeds every tile). Prefetching the next class's
+// fragments instead made the capped grid beside the near pass faster
+// (6.0 vs 8.1 ms) but slowed the near pass more (9.4 vs 8.9 ms).
+template <int P>
+__global__ void __maxnreg__(P >= 128 ? 128 : 88) k_coupling_mma(const CouplingItem* __restrict__ items,
+                                                              const std::int32_t* __restrict__ order,
                                                               const std::int32_t* __restrict__ item_cls,
                                                               const std::uint8_t* __restrict__ item_tiles,
                                                               const std::int32_t* __restrict__ cls_tau,
                                                               const double* __restrict__ C,
                                                               const double* __restrict__ xhat, int m,
-                                                              double* __restrict__ partial) {
+                                                              double* __restrict__ partial, int nitems) {
   constexpr int LD = P + 4;           // conflict-free B-fragment reads
   constexpr int KS = P / 4;           // k-steps of the m16n8k4 MMA
   constexpr int NT = kGroupSlots / 8; // n-tiles of 8 slots
   constexpr int PANEL = kGroupSlots * LD;
-  extern __shared__ double smem[];    // 2 stages x MC panels of [32][LD]
-  const CouplingItem it = items[blockIdx.x];
-  const int col0 = blockIdx.y * MC;
-  const int ncol = min(MC, m - col0);
+  constexpr int KH = KS / 2 > 0 ? KS / 2 : 1;  // k-steps per fragment load
+  extern __shared__ double smem[];    // 2 stages of [32][LD]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t0 = lane & 3;
   const int row0 = warp * 16;
-  double acc[MC][NT][4];
+  // (item, column) pairs strided over the grid: one pair per CTA for a full
+  // grid, several for a capped one; items in class-major order (device.cu)
+  const int nvb = nitems * m;
+  for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    const int item = order[vb % nitems];
+    const CouplingItem it = items[item];
+    const int col = vb / nitems;
+    double acc[NT][4];
 #pragma unroll
-  for (int c = 0; c < MC; ++c)
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[c][j][0] = acc[c][j][1] = acc[c][j][2] = acc[c][j][3] = 0.0;
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
 
-  auto gather = [&](int e, int buf) {
-    const std::int32_t* taus = cls_tau + static_cast<std::int64_t>(e) * kGroupSlots;
-    const unsigned tiles = item_tiles[e];
-    for (int c = 0; c < ncol; ++c) {
-      double* X = smem + (buf * MC + c) * PANEL;
+    auto gather = [&](int e, int buf) {
+      const std::int32_t* taus = cls_tau + static_cast<std::int64_t>(e) * kGroupSlots;
+      const unsigned tiles = item_tiles[e];
+      double* X = smem + buf * PANEL;
       for (int q2 = threadIdx.x; q2 < kGroupSlots * (P / 2); q2 += blockDim.x) {
         const int slot = q2 / (P / 2), q = q2 % (P / 2);
         if (!((tiles >> (slot >> 3)) & 1u)) continue;  // tile skipped by the MMAs
         const int tau = taus[slot];
-        const double* src =
-            xhat + (static_cast<std::int64_t>(tau < 0 ? 0 : tau) * m + col0 + c) * P + 2 * q;
+        const double* src = xhat + (static_cast<std::int64_t>(tau < 0 ? 0 : tau) * m + col) * P + 2 * q;
         cp_async16(X + slot * LD + 2 * q, src, tau >= 0);
       }
-    }
-    cp_async_commit();
-  };
-
-  const int e0 = it.e_begin;
-  if (e0 < it.e_end) gather(e0, 0);
-  for (int e = e0; e < it.e_end; ++e) {
-    const int buf = (e - e0) & 1;
-    if (e + 1 < it.e_end) {
-      gather(e + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* Ck = C + static_cast<std::int64_t>(item_cls[e]) * P * P;
-    const unsigned tiles = item_tiles[e];
-    // k in two halves: half the C_k fragments live in registers at a time
-    // (occupancy), each half still feeds every tile
-    constexpr int KH = KS / 2 > 0 ? KS / 2 : 1;
-#pragma unroll
-    for (int h = 0; h < KS / KH; ++h) {
-      double a[KH][2];
+      cp_async_commit();
+    };
+    auto load_a = [&](int e, int h, double (&a)[KH][2]) {
+      const double* Ck = C + static_cast<std::int64_t>(item_cls[e]) * P * P;
 #pragma unroll
       for (int s2 = 0; s2 < KH; ++s2) {
         const std::int64_t k = 4 * (h * KH + s2) + t0;
         a[s2][0] = __ldg(Ck + (row0 + g) + k * P);
         a[s2][1] = __ldg(Ck + (row0 + g + 8) + k * P);
       }
+    };
+    auto mma = [&](const double (&a)[KH][2], int h, const double* X, unsigned tiles) {
+      // tile-outer so an empty tile is a branch around its MMAs (a
+      // predicated MMA would still occupy the pipe)
 #pragma unroll
-      for (int c = 0; c < MC; ++c) {
-        if (c >= ncol) break;
-        const double* X = smem + (buf * MC + c) * PANEL;
-        // tile-outer so an empty tile is a branch around its MMAs (a
-        // predicated MMA would still occupy the pipe)
+      for (int j = 0; j < NT; ++j) {
+        if (!((tiles >> j) & 1u)) continue;
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          if (!((tiles >> j) & 1u)) continue;
-#pragma unroll
-          for (int s2 = 0; s2 < KH; ++s2)
-            dmma_16x8x4(acc[c][j], a[s2][0], a[s2][1], X[(8 * j + g) * LD + 4 * (h * KH + s2) + t0]);
-        }
+        for (int s2 = 0; s2 < KH; ++s2)
+          dmma_16x8x4(acc[j], a[s2][0], a[s2][1], X[(8 * j + g) * LD + 4 * (h * KH + s2) + t0]);
       }
-    }
-    __syncthreads();  // X[buf] is refilled two classes later
-  }
+    };
+
+    const int e0 = it.e_begin;
+    if (e0 < it.e_end) gather(e0, 0);
+    for (int e = e0; e < it.e_end; ++e) {
+      const int buf = (e - e0) & 1;
+      if (e + 1 < it.e_end) {
+        gather(e + 1, buf ^ 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const unsigned tiles = item_tiles[e];
 #pragma unroll
-  for (int c = 0; c < MC; ++c) {
-    if (c >= ncol) break;
-    double* out = partial + (static_cast<std::int64_t>(blockIdx.x) * m + col0 + c) * kGroupSlots * P;
+      for (int h = 0; h < KS / KH; ++h) {
+        double a[KH][2];
+        load_a(e, h, a);
+        mma(a, h, smem + buf * PANEL, tiles);
+      }
+      __syncthreads();  // X[buf] is refilled two classes later
+    }
+    double* out = partial + (static_cast<std::int64_t>(item) * m + col) * kGroupSlots * P;
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       const int n0 = 8 * j + 2 * t0;
-      out[n0 * P + row0 + g] = acc[c][j][0];
-      out[(n0 + 1) * P + row0 + g] = acc[c][j][1];
-      out[n0 * P + row0 + g + 8] = acc[c][j][2];
-      out[(n0 + 1) * P + row0 + g + 8] = acc[c][j][3];
+      out[n0 * P + row0 + g] = acc[j][0];
+      out[(n0 + 1) * P + row0 + g] = acc[j][1];
+      out[n0 * P + row0 + g + 8] = acc[j][2];
+      out[(n0 + 1) * P + row0 + g + 8] = acc[j][3];
     }
   }
 }
@@ -1151,7 +1170,6 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
 // refills. Shared memory (doubles): NST R CH stages + 2 CH formed + 2 x 128
 // x_tau panels.
 constexpr int tma_smem_doubles(int R, int CH, int NST) { return NST * R * CH + 2 * CH + 256; }
-constexpr int kTmaMaxBlocks = 128;  // owned blocks per item (device.cu splits longer runs)
 constexpr int kTmaThreads = 288;    // 8 consumer warps + 1 producer warp
 
 __device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
@@ -2205,13 +2223,75 @@ void launch_near_mvm_symcsr(cudaStream_t st, const SymRowItem* items, int nitems
   if (nitems == 0) return;
   k_near_mvm_symcsr<<<nitems, 256, 0, st>>>(items, blocks, D, xp, part);
 }
+// Chunk length (doubles per slab) of k_near_tma for rank R: about 40 KB per
+// stage, 256 <= CH <= 1024, a multiple of 64.
+constexpr int near_tma_ch(int R) {
+  return ((5120 / R) & ~63) < 256 ? 256 : (((5120 / R) & ~63) > 1024 ? 1024 : ((5120 / R) & ~63));
+}
+
+namespace {
+// CTAs of kernel b that fit on one SM beside na CTAs of kernel a (registers,
+// shared memory, threads; per-warp register allocation in units of 256).
+int fit_beside(const void* fa, size_t dyn_a, int thr_a, int na, const void* fb, size_t dyn_b, int thr_b) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceProp pr;
+  cudaFuncAttributes a, b;
+  if (cudaGetDeviceProperties(&pr, dev) != cudaSuccess || cudaFuncGetAttributes(&a, fa) != cudaSuccess ||
+      cudaFuncGetAttributes(&b, fb) != cudaSuccess)
+    return 0;
+  auto regs = [](const cudaFuncAttributes& f, int thr) {
+    return ((thr + 31) / 32) * ((f.numRegs * 32 + 255) / 256 * 256);
+  };
+  auto smem = [&](const cudaFuncAttributes& f, size_t dyn) {
+    return static_cast<long>(f.sharedSizeBytes + dyn + pr.reservedSharedMemPerBlock);
+  };
+  long r = pr.regsPerMultiprocessor - static_cast<long>(na) * regs(a, thr_a);
+  long sm = static_cast<long>(pr.sharedMemPerMultiprocessor) - na * smem(a, dyn_a);
+  long th = pr.maxThreadsPerMultiProcessor - static_cast<long>(na) * thr_a;
+  int k = 0;
+  while (r >= regs(b, thr_b) && sm >= smem(b, dyn_b) && th >= thr_b && k < 8) {
+    r -= regs(b, thr_b);
+    sm -= smem(b, dyn_b);
+    th -= thr_b;
+    ++k;
+  }
+  return k;
+}
+}  // namespace
+
+// Coupling CTAs (k_coupling_mma<P>) that fit on one SM beside the two CTAs
+// per SM of the fused near pass (k_near_tma for rank R); 0 when none does.
+int coupling_beside_near(int R, int P) {
+  const size_t cpl = 2 * kGroupSlots * (P + 4) * sizeof(double);
+  const void* fb = nullptr;
+  switch (P) {
+    case 16: fb = reinterpret_cast<const void*>(k_coupling_mma<16>); break;
+    case 32: fb = reinterpret_cast<const void*>(k_coupling_mma<32>); break;
+    case 64: fb = reinterpret_cast<const void*>(k_coupling_mma<64>); break;
+    case 128: fb = reinterpret_cast<const void*>(k_coupling_mma<128>); break;
+    default: return 0;
+  }
+  switch (R) {
+#define PHM_FIT(RR)                                                                                             \
+  case RR:                                                                                                      \
+    return fit_beside(reinterpret_cast<const void*>(k_near_tma<RR, near_tma_ch(RR), 2>),                        \
+                      static_cast<size_t>(tma_smem_doubles(RR, near_tma_ch(RR), 2)) * sizeof(double), kTmaThreads, 2, \
+                      fb, cpl, P / 16 * 32);
+    PHM_FIT(1) PHM_FIT(2) PHM_FIT(3) PHM_FIT(4) PHM_FIT(5) PHM_FIT(6) PHM_FIT(7) PHM_FIT(8)
+    PHM_FIT(9) PHM_FIT(10) PHM_FIT(11) PHM_FIT(12) PHM_FIT(13) PHM_FIT(14) PHM_FIT(15) PHM_FIT(16)
+#undef PHM_FIT
+    default: return 0;
+  }
+}
+
 // Snapshot-mode instantiate fused with apply (K1 + K6 in one pass over the
 // snapshots). Returns false for a rank without an instantiation (R > 16).
 bool launch_near_inst_tma(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks,
                           const double* G, std::int64_t E, int R, const double* w, double* D, const double* xp,
                           double* part) {
   if (nitems == 0) return true;
-#define PHM_TMA(RR, NST) PHM_TMA_CH(RR, ((5120 / RR) & ~63) < 256 ? 256 : (((5120 / RR) & ~63) > 1024 ? 1024 : ((5120 / RR) & ~63)), NST)
+#define PHM_TMA(RR, NST) PHM_TMA_CH(RR, near_tma_ch(RR), NST)
 #define PHM_TMA_CH(RR, CHv, NST)                                                                              \
   {                                                                                                           \
     constexpr int CHc = CHv;                                                                                  \
@@ -2311,27 +2391,27 @@ void launch_near_mrhs(cudaStream_t st, const MrhsItem* items, int nitems, const 
 
 bool coupling_mma_supported(int P) { return P == 16 || P == 32 || P == 64 || P == 128; }
 
-void launch_coupling_mma(cudaStream_t st, const CouplingItem* items, int nitems, const std::int32_t* item_cls,
-                         const std::uint8_t* item_tiles, const std::int32_t* cls_tau, const double* C, int P,
-                         const double* xhat, int m, double* partial) {
+void launch_coupling_mma(cudaStream_t st, const CouplingItem* items, const std::int32_t* order, int nitems,
+                         const std::int32_t* item_cls, const std::uint8_t* item_tiles, const std::int32_t* cls_tau,
+                         const double* C, int P, const double* xhat, int m, double* partial, int max_ctas) {
   if (nitems == 0) return;
-  // one RHS column per CTA (grid.y walks the columns): at C3 it beat two
-  // columns sharing each C_k fragment load at every m measured (4: 3.3 vs
-  // 3.5 ms, 10: 7.9 vs 8.4, 64: 49.4 vs 52.2) -- occupancy over reuse
-  const int mc = 1;
-  const size_t smem = 2 * mc * kGroupSlots * (P + 4) * sizeof(double);
-  const dim3 grid(static_cast<unsigned>(nitems), static_cast<unsigned>((m + mc - 1) / mc));
-#define PHM_CASE(PP, MC)                                                                                    \
-  if (P == PP && mc == MC) {                                                                                \
-    smem_attr(reinterpret_cast<const void*>(k_coupling_mma<PP, MC>), 200 * 1024, false);                   \
-    k_coupling_mma<PP, MC><<<grid, PP / 16 * 32, smem, st>>>(items, item_cls, item_tiles, cls_tau, C, xhat, m,     \
-                                                             partial);                                          \
+  // one RHS column per CTA iteration: at C3 it beat two columns sharing each
+  // C_k fragment load at every m measured (4: 3.3 vs 3.5 ms, 10: 7.9 vs 8.4,
+  // 64: 49.4 vs 52.2) -- occupancy over reuse
+  const size_t smem = 2 * kGroupSlots * (P + 4) * sizeof(double);
+  const std::int64_t nvb = static_cast<std::int64_t>(nitems) * m;
+  const int grid = static_cast<int>(max_ctas > 0 && max_ctas < nvb ? max_ctas : nvb);
+#define PHM_CASE(PP)                                                                                        \
+  if (P == PP) {                                                                                            \
+    smem_attr(reinterpret_cast<const void*>(k_coupling_mma<PP>), 200 * 1024, false);                       \
+    k_coupling_mma<PP><<<grid, PP / 16 * 32, smem, st>>>(items, order, item_cls, item_tiles, cls_tau, C, xhat, m, \
+                                                         partial, nitems);                                      \
     return;                                                                                                 \
   }
-  PHM_CASE(16, 1)
-  PHM_CASE(32, 1)
-  PHM_CASE(64, 1)
-  PHM_CASE(128, 1)
+  PHM_CASE(16)
+  PHM_CASE(32)
+  PHM_CASE(64)
+  PHM_CASE(128)
 #undef PHM_CASE
 }
 

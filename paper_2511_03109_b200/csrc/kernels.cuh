@@ -96,6 +96,10 @@ struct SymRowItem {
   std::int64_t x_row0, p_row;
   std::int32_t rows, ld, i0, bbeg, bend, pad;
 };
+// Owned blocks per near item at most (the TMA passes cache an item's block
+// list in shared memory; device.cu splits longer runs). Small, so that a
+// coupling CTA fits beside two near CTAs on one SM.
+constexpr int kTmaMaxBlocks = 32;
 struct SymBlock {
   std::int64_t d_off, x_col0, p_col;  // p_col < 0: diagonal block
   std::int32_t ncol, pad;
