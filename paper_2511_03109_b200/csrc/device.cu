@@ -940,7 +940,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     std::vector<double> mid, L, R;
     std::vector<std::int32_t> mdims;
     std::int64_t hoff = 0;
-    int maxrl = 1, maxA = 1, maxB = 1, maxs1 = 1;
+    int maxrl = 1, maxrr = 1, maxA = 1, maxB = 1, maxs1 = 1;
     for (int k = 0; k < M.ncls; ++k) {
       const Coupling& c = H.couplings[k];
       dev::ClassMeta cm{};
@@ -966,6 +966,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
       (void)cur;
       maxA = std::max(maxA, cm.rl * cm.rr);
       maxrl = std::max(maxrl, cm.rl);
+      maxrr = std::max(maxrr, cm.rr);
       cm.h_off = hoff;
       hoff += static_cast<std::int64_t>(cm.rl) * cm.rr;
       if (M.h2) {
@@ -983,7 +984,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     M.capT = std::max(maxrl * 32, maxrl * maxs1);
     if (M.h2 && M.P == 64) {  // register-tiled C = L (H R^T): T (rl x 64) and L (64 x rl) staged
       M.capT = std::max(M.capT, maxrl * 64);
-      M.capL = 64 * maxrl;
+      M.capL = 64 * std::max(maxrl, maxrr);  // L, and R before it
     }
     PHM_CHECK((M.capA + M.capB + M.capT + M.capL) * 8 <= 227 * 1024, "class instantiate shared memory over 227 KB");
     M.H_len = hoff;

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <set>
 #include <tuple>
@@ -401,14 +402,20 @@ __global__ void k_class_inst(const ClassMeta* __restrict__ meta, int ncls, const
     // L staged (64 x rl), then thread (a4, b4) accumulates the 4 x 4 tile
     // rows a4 + 16 q, columns b4 + 16 q' over i < rl (conflict-free reads:
     // consecutive a4 hit consecutive banks, b4 is a broadcast per half-warp).
+    // R (64 x rr) and then L (64 x rl) are staged through the same region
+    // with all loads in flight at once (reading R inside the dot products
+    // put one L2 round trip per 8 terms on the critical path: 239 us at C3).
     double* Ts = Tt;             // rl x 64, column-major (ld rl)
-    double* Ls = Tt + capT;      // 64 x rl, column-major (ld 64)
+    double* Ls = Tt + capT;      // 64 x rl (or R: 64 x rr), column-major (ld 64)
+    for (int e = tid; e < 64 * rr; e += nt) Ls[e] = Rm[M.r_off + e];
+    __syncthreads();
     for (int e = tid; e < rl * 64; e += nt) {
       const int i = e % rl, b = e / rl;
       double t = 0.0;
-      for (int c = 0; c < rr; ++c) t += A[i + c * rl] * Rm[M.r_off + b + static_cast<std::int64_t>(c) * 64];
+      for (int c = 0; c < rr; ++c) t += A[i + c * rl] * Ls[b + c * 64];
       Ts[e] = t;
     }
+    __syncthreads();
     for (int e = tid; e < 64 * rl; e += nt) Ls[e] = Lm[M.l_off + e];
     __syncthreads();
     const int a4 = tid & 15, b4 = tid >> 4;
@@ -2235,10 +2242,15 @@ namespace {
 int fit_beside(const void* fa, size_t dyn_a, int thr_a, int na, const void* fb, size_t dyn_b, int thr_b) {
   int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceProp pr;
+  struct {
+    int regsPerMultiprocessor, sharedMemPerMultiprocessor, reservedSharedMemPerBlock, maxThreadsPerMultiProcessor;
+  } pr{};
   cudaFuncAttributes a, b;
-  if (cudaGetDeviceProperties(&pr, dev) != cudaSuccess || cudaFuncGetAttributes(&a, fa) != cudaSuccess ||
-      cudaFuncGetAttributes(&b, fb) != cudaSuccess)
+  if (cudaDeviceGetAttribute(&pr.regsPerMultiprocessor, cudaDevAttrMaxRegistersPerMultiprocessor, dev) ||
+      cudaDeviceGetAttribute(&pr.sharedMemPerMultiprocessor, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) ||
+      cudaDeviceGetAttribute(&pr.reservedSharedMemPerBlock, cudaDevAttrReservedSharedMemoryPerBlock, dev) ||
+      cudaDeviceGetAttribute(&pr.maxThreadsPerMultiProcessor, cudaDevAttrMaxThreadsPerMultiProcessor, dev) ||
+      cudaFuncGetAttributes(&a, fa) != cudaSuccess || cudaFuncGetAttributes(&b, fb) != cudaSuccess)
     return 0;
   auto regs = [](const cudaFuncAttributes& f, int thr) {
     return ((thr + 31) / 32) * ((f.numRegs * 32 + 255) / 256 * 256);
@@ -2260,9 +2272,22 @@ int fit_beside(const void* fa, size_t dyn_a, int thr_a, int na, const void* fb, 
 }
 }  // namespace
 
+int coupling_fit(int R, int P);
 // Coupling CTAs (k_coupling_mma<P>) that fit on one SM beside the two CTAs
 // per SM of the fused near pass (k_near_tma for rank R); 0 when none does.
+// Memoised: it runs on every (ungraphed) step.
 int coupling_beside_near(int R, int P) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, int> memo;  // (device, R, P) -> CTAs
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, R, P);
+  const auto hit = memo.find(key);
+  if (hit != memo.end()) return hit->second;
+  return memo[key] = coupling_fit(R, P);
+}
+int coupling_fit(int R, int P) {
   const size_t cpl = 2 * kGroupSlots * (P + 4) * sizeof(double);
   const void* fb = nullptr;
   switch (P) {
