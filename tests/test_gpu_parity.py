@@ -535,3 +535,45 @@ def test_tiny_and_degenerate_sizes(ph, po, n, d, l_max):
         assert rel(inst.apply(X), oi.apply(X)) <= TOL_Y
         assert rel(inst.instantiate_apply([0.4], x), om.instantiate([0.4]).apply(x)) <= TOL_Y
         assert rel(inst.to_dense(), om.instantiate([0.4]).to_dense()) <= TOL_Y
+
+
+_SCHEDULE_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2511_03109_b200 as ph
+pts = ph.generate_points(12000, 3, 21)
+cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=3, p_s=4, p_theta=8, eta=1.0,
+                  near_mode=ph.NearMode.SNAPSHOT)
+pm = ph.offline_h2(pts, cfg)
+inst = ph.instantiate(pm, [0.3])
+x = ph.generate_normal(12000, 2)
+ys = [inst.instantiate_apply(t, x) for t in ([0.12], [0.29], [0.12], [0.29])]
+np.save(sys.argv[2], np.stack(ys))
+"""
+
+
+def test_coupling_schedule_does_not_change_results(ph, tmp_path):
+    """The fused step's coupling runs as a capped grid resident beside the
+    near pass, items in class-major order. Per-item
+    partials and their reduction order are fixed, so y is bitwise the same
+    with the full grid (PHM_COUPLING_RESIDENT=0) and the item order
+    (PHM_COUPLING_ORDER=0), with and without CUDA graphs (the first call per
+    key runs directly, the second captures, later ones replay)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "sched.py"
+    script.write_text(_SCHEDULE_SCRIPT)
+    outs = {}
+    for tag, env in (("default", {}), ("full", {"PHM_COUPLING_RESIDENT": "0"}),
+                     ("unordered", {"PHM_COUPLING_ORDER": "0"}), ("nographs", {"PHM_GRAPHS": "0"})):
+        out = tmp_path / f"{tag}.npy"
+        subprocess.run([sys.executable, str(script), root, str(out)], check=True, timeout=600,
+                       env={**os.environ, **env})
+        outs[tag] = np.load(out)
+    ref = outs["default"]
+    assert np.array_equal(ref[0], ref[2]) and np.array_equal(ref[1], ref[3])  # direct vs captured vs replayed
+    for tag in ("full", "unordered", "nographs"):
+        assert np.array_equal(outs[tag], ref), tag
