@@ -1584,6 +1584,10 @@ __global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ item
   const int R4 = (R + 3) & ~3;
   const int mtiles = (R + 15) >> 4;
   const int ypairs = mtiles * NTN;
+  // whole-leaf item: a chunk of kc columns is contiguous in D, staged by one
+  // bulk copy with column stride R (else one copy per column, stride 132)
+  const bool dense = it.i0 == 0 && ld == R;
+  const int cs = dense ? R : kK9bLd;
   PHM_DCHECK(R >= 1 && R <= 128 && it.i0 + R <= it.ld);
   if (tid == 0) {
     for (int q = 0; q < 2; ++q) {
@@ -1603,11 +1607,19 @@ __global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ item
         const int kc = min(kK9bKc, blk.ncol - j0);
         double* Dc = St + slot * STAGE;
         double* Xt = Dc + kK9bKc * kK9bLd;
-        // lane k: column k of the chunk; lane c (< ncr): RHS column c of X_tau
+        // lane k: column k of the chunk (whole-leaf items: lane 0 copies the
+        // contiguous chunk at once); lane c (< ncr): RHS column c of X_tau
         unsigned bytes_d = 0, bytes_x = 0;
         const double* src_d = nullptr;
         const double* src_x = nullptr;
-        if (lane < kc) {
+        if (dense) {
+          if (lane == 0) {
+            const double* ch = D + blk.d_off + static_cast<std::int64_t>(j0) * ld;
+            const int sh = static_cast<int>((reinterpret_cast<std::uintptr_t>(ch) >> 3) & 1);
+            src_d = ch - sh;
+            bytes_d = static_cast<unsigned>(((kc * R + sh + 1) & ~1) * 8);
+          }
+        } else if (lane < kc) {
           const double* col = D + blk.d_off + it.i0 + static_cast<std::int64_t>(j0 + lane) * ld;
           const int sh = static_cast<int>((reinterpret_cast<std::uintptr_t>(col) >> 3) & 1);
           src_d = col - sh;
@@ -1649,8 +1661,11 @@ __global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ item
       mbar_wait(&full[slot], (c >> 1) & 1);
       const double* Dc = St + slot * STAGE;
       const double* Xt = Dc + kK9bKc * kK9bLd;
-      // element (r, k) of the chunk sits at Dc[k * 132 + sh(k) + r]
-      auto dsh = [&](int k) { return static_cast<int>(((dbase >> 3) + static_cast<std::uintptr_t>((j0 + k) * ld)) & 1); };
+      // element (r, k) of the chunk sits at Dc[k * cs + sh(k) + r]
+      const int sh_chunk = static_cast<int>(((dbase >> 3) + static_cast<std::uintptr_t>(j0 * ld)) & 1);
+      auto dsh = [&](int k) {
+        return dense ? sh_chunk : static_cast<int>(((dbase >> 3) + static_cast<std::uintptr_t>((j0 + k) * ld)) & 1);
+      };
       const int ksy = (kc + 3) >> 2;
       // Y_sigma += D(:, chunk) X_tau(chunk, :)
 #pragma unroll
@@ -1666,8 +1681,8 @@ __global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ item
             const int k = 4 * s2 + t0;
             const bool kin = k < kc;
             const int sh = kin ? dsh(k) : 0;
-            const double a0 = kin ? Dc[k * kK9bLd + sh + 16 * mt + g] : 0.0;
-            const double a1 = kin ? Dc[k * kK9bLd + sh + 16 * mt + g + 8] : 0.0;
+            const double a0 = kin ? Dc[k * cs + sh + 16 * mt + g] : 0.0;
+            const double a1 = kin ? Dc[k * cs + sh + 16 * mt + g + 8] : 0.0;
             const double b0 = (kin && ncol_b < ncr) ? Xt[ncol_b * LDX + xsh + k] : 0.0;
             dmma_16x8x4(yacc[q], a0, a1, b0);
           }
@@ -1686,15 +1701,15 @@ __global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ item
           int s2 = 0;
           for (; s2 + 1 < ksz; s2 += 2) {
             const int k = 4 * s2 + t0;
-            dmma_16x8x4(z, (in0 && k < R) ? Dc[j_a0 * kK9bLd + sh0 + k] : 0.0,
-                        (in1 && k < R) ? Dc[j_a1 * kK9bLd + sh1 + k] : 0.0, Xs[(8 * nt + g) * kK9bLd + k]);
-            dmma_16x8x4(z1, (in0 && k + 4 < R) ? Dc[j_a0 * kK9bLd + sh0 + k + 4] : 0.0,
-                        (in1 && k + 4 < R) ? Dc[j_a1 * kK9bLd + sh1 + k + 4] : 0.0, Xs[(8 * nt + g) * kK9bLd + k + 4]);
+            dmma_16x8x4(z, (in0 && k < R) ? Dc[j_a0 * cs + sh0 + k] : 0.0,
+                        (in1 && k < R) ? Dc[j_a1 * cs + sh1 + k] : 0.0, Xs[(8 * nt + g) * kK9bLd + k]);
+            dmma_16x8x4(z1, (in0 && k + 4 < R) ? Dc[j_a0 * cs + sh0 + k + 4] : 0.0,
+                        (in1 && k + 4 < R) ? Dc[j_a1 * cs + sh1 + k + 4] : 0.0, Xs[(8 * nt + g) * kK9bLd + k + 4]);
           }
           if (s2 < ksz) {
             const int k = 4 * s2 + t0;
-            dmma_16x8x4(z, (in0 && k < R) ? Dc[j_a0 * kK9bLd + sh0 + k] : 0.0,
-                        (in1 && k < R) ? Dc[j_a1 * kK9bLd + sh1 + k] : 0.0, Xs[(8 * nt + g) * kK9bLd + k]);
+            dmma_16x8x4(z, (in0 && k < R) ? Dc[j_a0 * cs + sh0 + k] : 0.0,
+                        (in1 && k < R) ? Dc[j_a1 * cs + sh1 + k] : 0.0, Xs[(8 * nt + g) * kK9bLd + k]);
           }
 #pragma unroll
           for (int e = 0; e < 4; ++e) z[e] += z1[e];
