@@ -501,9 +501,13 @@ def run_ours(args):
         cp = timers.get("coupling")
         k9 = timers.get("near_mrhs")
         dmma = {
-            "coupling_tflops": (2.0 * info["n_far"] * info["P"] ** 2 * m / (cp["ms_per_launch"] * 1e-3) / 1e12)
+            "note": ("useful fp64 flop over each kernel's event-timed duration inside the step, where it "
+                     "time-shares the SMs with the near pass (the fused step's coupling is a capped grid "
+                     "resident beside it); DMMA pipe utilisation of the kernels alone: profiles/r01_*_full_summary.txt"),
+            "coupling_tflops_in_step": (2.0 * info["n_far"] * info["P"] ** 2 * m / (cp["ms_per_launch"] * 1e-3) / 1e12)
             if cp else None,
-            "near_mrhs_tflops": (2.0 * info["near_entries"] * m / (k9["ms_per_launch"] * 1e-3) / 1e12) if k9 else None,
+            "near_mrhs_tflops_in_step": (2.0 * info["near_entries"] * m / (k9["ms_per_launch"] * 1e-3) / 1e12)
+            if k9 else None,
         }
         what, config = describe(args, c, m, tb, world)
         line = {
