@@ -1858,8 +1858,12 @@ void instantiate_apply_sequence(DevInstance& I, const double* x_dev, Index m, St
     return !(e && std::atoi(e) == 0);
   }();
   const bool fuse = use_fused && M.near_tma && M.mode == NearMode::Snapshot && m == 1;
+  // Only for a long near pass (>= 16 GB streamed, ~2.5 ms): the capped grid
+  // needs about 8x the full grid's time, which a short pass does not cover
+  // (row shard 8 of C3: 1.48 vs 1.44 ms per step; shard 4 of 4: equal).
+  const bool long_pass = 8.0 * static_cast<double>(M.E_rank) >= 16e9;
   int coupling_ctas = 0;
-  if (fuse && M.cp_mma && resident_env != 0) {
+  if (fuse && M.cp_mma && resident_env != 0 && (long_pass || resident_env > 0)) {
     const int fit = dev::coupling_beside_near(M.R_snap, M.P);
     const int per_sm = resident_env > 0 ? resident_env : std::min(fit, 1);
     coupling_ctas = per_sm * ctx.sms;
