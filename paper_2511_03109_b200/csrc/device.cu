@@ -982,9 +982,15 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     M.capA = std::max(maxA, maxrl * maxs1);
     M.capB = maxB;
     M.capT = std::max(maxrl * 32, maxrl * maxs1);
-    if (M.h2 && M.P == 64) {  // register-tiled C = L (H R^T): T (rl x 64) and L (64 x rl) staged
-      M.capT = std::max(M.capT, maxrl * 64);
-      M.capL = 64 * std::max(maxrl, maxrr);  // L, and R before it
+    if (M.h2 && M.P == 64) {  // C = L (H R^T) on DMMA: T (rl4 x 64, ld ldT), then R / L (ld 68) staged
+      const int rl4 = (maxrl + 3) & ~3, rr4 = (maxrr + 3) & ~3;
+      int ldT = 0;  // k_class_inst's T stride: the least ld >= rl4 with ld = 4 mod 16, over all classes
+      for (const auto& cm : M.cmeta_h) {
+        const int r4 = (cm.rl + 3) & ~3;
+        ldT = std::max(ldT, r4 + ((4 - r4) & 15));
+      }
+      M.capT = std::max(M.capT, ldT * 64);
+      M.capL = 68 * std::max(rl4, rr4);  // L, and R before it
     }
     PHM_CHECK((M.capA + M.capB + M.capT + M.capL) * 8 <= 227 * 1024, "class instantiate shared memory over 227 KB");
     M.H_len = hoff;

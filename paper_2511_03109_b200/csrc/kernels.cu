@@ -341,6 +341,15 @@ __global__ void k_put_theta(ThetaParams p, ThetaParams* __restrict__ dst) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = src[i];
 }
 
+// fp64 tensor-core MMA (DMMA; sm_100 has no tcgen05 f64 kind): D += A B with
+// A 16x4 (a0 = A[g][t], a1 = A[g+8][t]), B 4x8 (b0 = B[t][g]), D 16x8
+// (d = D[g][2t], D[g][2t+1], D[g+8][2t], D[g+8][2t+1]); g = lane / 4, t = lane % 4.
+__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+
 // ----------------------------------------------------------------- K2
 // One CTA per translation class. H = prod_i contract(G_{d+i}, v_i)
 // (farfield.cpp:149-155); for H^2 also C = L H R^T in 32-column tiles.
@@ -397,50 +406,82 @@ __global__ void k_class_inst(const ClassMeta* __restrict__ meta, int ncls, const
   __syncthreads();
   for (int e = tid; e < rl * rr; e += nt) H[M.h_off + e] = A[e];
   if (!want_c) return;
-  if (P == 64 && nt == 256) {
-    // C = L (H R^T) register-tiled: T = H R^T (rl x 64) into shared memory,
-    // L staged (64 x rl), then thread (a4, b4) accumulates the 4 x 4 tile
-    // rows a4 + 16 q, columns b4 + 16 q' over i < rl (conflict-free reads:
-    // consecutive a4 hit consecutive banks, b4 is a broadcast per half-warp).
-    // R (64 x rr) and then L (64 x rl) are staged through the same region
-    // with all loads in flight at once (reading R inside the dot products
-    // put one L2 round trip per 8 terms on the critical path: 239 us at C3).
-    double* Ts = Tt;             // rl x 64, column-major (ld rl)
-    double* Ls = Tt + capT;      // 64 x rl (or R: 64 x rr), column-major (ld 64)
-    for (int e = tid; e < 64 * rr; e += nt) Ls[e] = Rm[M.r_off + e];
-    __syncthreads();
-    for (int e = tid; e < rl * 64; e += nt) {
-      const int i = e % rl, b = e / rl;
-      double t = 0.0;
-      for (int c = 0; c < rr; ++c) t += A[i + c * rl] * Ls[b + c * 64];
-      Ts[e] = t;
+  if (P == 64 && nt == 256 && rl <= 64) {
+    // Both products on the fp64 tensor cores (mma.sync m16n8k4): T = H R^T
+    // (rl x 64) into shared memory, then C = L T (64 x 64); warp w owns the
+    // 8 output columns 8w .. 8w + 7 of each, all 16-row tiles. R (64 x rr)
+    // and then L (64 x rl) are staged through one region with all loads in
+    // flight (ld 68, and T's ld = 4 mod 16: conflict-free fragment reads);
+    // the k padding (rr, rl up to a multiple of 4) is zero.
+    const int rl4 = (rl + 3) & ~3, rr4 = (rr + 3) & ~3;
+    const int ldT = rl4 + ((4 - rl4) & 15);  // the least ld >= rl4 with ld = 4 mod 16
+    constexpr int ldL = 68;
+    double* Ts = Tt;         // rl4 x 64, ld ldT
+    double* Ls = Tt + capT;  // R: 64 x rr4, then L: 64 x rl4 (ld 68)
+    for (int e = tid; e < 64 * rr4; e += nt) {
+      const int b = e & 63, c = e >> 6;
+      Ls[b + c * ldL] = c < rr ? Rm[M.r_off + b + static_cast<std::int64_t>(c) * 64] : 0.0;
     }
     __syncthreads();
-    for (int e = tid; e < 64 * rl; e += nt) Ls[e] = Lm[M.l_off + e];
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t0 = lane & 3;
+    const int mts = (rl + 15) >> 4;
+    {
+      double acc[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.0;
+      for (int s2 = 0; s2 < (rr4 >> 2); ++s2) {
+        const int k = 4 * s2 + t0;
+        const double b0 = Ls[(8 * warp + g) + k * ldL];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          if (mt >= mts) break;  // warp-uniform
+          const int r = 16 * mt + g;
+          const double a0 = (r < rl && k < rr) ? A[r + k * rl] : 0.0;
+          const double a1 = (r + 8 < rl && k < rr) ? A[r + 8 + k * rl] : 0.0;
+          dmma_16x8x4(acc[mt], a0, a1, b0);
+        }
+      }
+      const int c = 8 * warp + 2 * t0;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        if (mt >= mts) break;
+        const int r = 16 * mt + g;  // rows in [rl, rl4) come out zero (zero A rows)
+        if (r < rl4) {
+          Ts[r + c * ldT] = acc[mt][0];
+          Ts[r + (c + 1) * ldT] = acc[mt][1];
+        }
+        if (r + 8 < rl4) {
+          Ts[r + 8 + c * ldT] = acc[mt][2];
+          Ts[r + 8 + (c + 1) * ldT] = acc[mt][3];
+        }
+      }
+    }
+    __syncthreads();  // T complete, R no longer read
+    for (int e = tid; e < 64 * rl4; e += nt) {
+      const int a = e & 63, i = e >> 6;
+      Ls[a + i * ldL] = i < rl ? Lm[M.l_off + a + static_cast<std::int64_t>(i) * 64] : 0.0;
+    }
     __syncthreads();
-    const int a4 = tid & 15, b4 = tid >> 4;
     double acc[4][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.0;
+    for (int s2 = 0; s2 < (rl4 >> 2); ++s2) {
+      const int k = 4 * s2 + t0;
+      const double b0 = Ts[k + (8 * warp + g) * ldT];
 #pragma unroll
-      for (int r2 = 0; r2 < 4; ++r2) acc[q][r2] = 0.0;
-    for (int i = 0; i < rl; ++i) {
-      double l[4], t[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        l[q] = Ls[a4 + 16 * q + i * 64];
-        t[q] = Ts[i + (b4 + 16 * q) * rl];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int r2 = 0; r2 < 4; ++r2) acc[q][r2] += l[q] * t[r2];
+      for (int mt = 0; mt < 4; ++mt)
+        dmma_16x8x4(acc[mt], Ls[(16 * mt + g) + k * ldL], Ls[(16 * mt + g + 8) + k * ldL], b0);
     }
+    const int c = 8 * warp + 2 * t0;
+    double* Cb = C + M.c_off;
 #pragma unroll
-    for (int r2 = 0; r2 < 4; ++r2)
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        C[M.c_off + (a4 + 16 * q) + static_cast<std::int64_t>(b4 + 16 * r2) * 64] = acc[q][r2];
+    for (int mt = 0; mt < 4; ++mt) {
+      const int r = 16 * mt + g;
+      Cb[r + c * 64] = acc[mt][0];
+      Cb[r + (c + 1) * 64] = acc[mt][1];
+      Cb[r + 8 + c * 64] = acc[mt][2];
+      Cb[r + 8 + (c + 1) * 64] = acc[mt][3];
+    }
     return;
   }
   for (int b0 = 0; b0 < P; b0 += 32) {
@@ -641,11 +682,6 @@ __global__ void k_coupling(const std::int32_t* __restrict__ sig, const std::int6
 // shared memory by cp.async, double-buffered against the MMAs of the
 // previous class. Per-item partial sums are reduced in a fixed order by
 // k_coupling_reduce: deterministic, no atomics.
-__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
-  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
-               : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
-               : "d"(a0), "d"(a1), "d"(b0));
-}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   const int sz = valid ? 16 : 0;  // src-size 0 zero-fills (missing partner)
