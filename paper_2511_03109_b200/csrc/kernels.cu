@@ -371,9 +371,13 @@ __global__ void k_class_inst(const ClassMeta* __restrict__ meta, int ncls, const
   for (int e = tid; e < r0 * r1; e += nt) {
     const int a = e % r0, c = e / r0;
     double s = 0.0;
+    // loads unconditional (so the compiler issues them together), the sum
+    // still skips zero weights exactly as before
+#pragma unroll 8
     for (int j = 0; j < m0; ++j) {
       const double vj = tv.v[0][j];
-      if (vj != 0.0) s += vj * mid[off + a + j * r0 + static_cast<std::int64_t>(c) * r0 * m0];
+      const double x = mid[off + a + j * r0 + static_cast<std::int64_t>(c) * r0 * m0];
+      if (vj != 0.0) s += vj * x;
     }
     A[e] = s;
   }
@@ -385,9 +389,11 @@ __global__ void k_class_inst(const ClassMeta* __restrict__ meta, int ncls, const
     for (int e = tid; e < s0 * s1; e += nt) {
       const int a = e % s0, c = e / s0;
       double s = 0.0;
+#pragma unroll 8
       for (int j = 0; j < sm_; ++j) {
         const double vj = tv.v[q][j];
-        if (vj != 0.0) s += vj * mid[off + a + j * s0 + static_cast<std::int64_t>(c) * s0 * sm_];
+        const double x = mid[off + a + j * s0 + static_cast<std::int64_t>(c) * s0 * sm_];
+        if (vj != 0.0) s += vj * x;
       }
       B[e] = s;
     }
