@@ -63,7 +63,7 @@ void launch_near_tma_apply(cudaStream_t, const SymRowItem*, int, const SymBlock*
 void launch_near_mrhs2(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
                        std::int64_t, int, std::int64_t, double*);
 void launch_near_mrhs3(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
-                       std::int64_t, int, std::int64_t, double*);
+                       std::int64_t, int, std::int64_t, double*, int);
 void launch_near_mvm_symcsr(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, const double*,
                             double*);
 bool launch_near_inst_tma(cudaStream_t, const SymRowItem*, int, const SymBlock*, const double*, std::int64_t, int,
@@ -359,6 +359,7 @@ struct DevMatrix {
   std::int64_t sym_pstride = 0;  // partial segments per right-hand side
   DBuf sym_part_m;               // two-sided K9: sym_pstride x m partials
   int n_sym_items = 0, n_gather_leaves = 0;
+  int k9_dense_rows = 0;  // tallest whole-leaf item, 0 if some item is a row slice (K9 stage size)
   bool near_tma = false;  // every item spans its whole leaf: TMA near pass
   DBuf theta_dev;         // dev::ThetaParams of the instantiate in flight
   DBuf work_ctr;          // persistent near kernels' item counter
@@ -868,6 +869,9 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
       sbeg.push_back(static_cast<std::int32_t>(segs.size()));
     }
     M.n_sym_items = static_cast<int>(items.size());
+    M.k9_dense_rows = 1;
+    for (const auto& it : items)
+      M.k9_dense_rows = (it.i0 == 0 && it.rows == it.ld && M.k9_dense_rows > 0) ? std::max(M.k9_dense_rows, it.rows) : 0;
     M.n_gather_leaves = static_cast<int>(lrow0.size());
     M.near_tma = !items.empty();
     M.work_ctr.alloc(sizeof(int));
@@ -1636,7 +1640,8 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
     ctx.run_on(st, "near_mrhs", [&] {
       if (k9v == 1)
         dev::launch_near_mrhs3(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items, M.sym_blocks.as<dev::SymBlock>(),
-                               I.D.as<double>(), M.xp.as<double>(), M.n, mm, M.sym_pstride, M.sym_part_m.as<double>());
+                               I.D.as<double>(), M.xp.as<double>(), M.n, mm, M.sym_pstride, M.sym_part_m.as<double>(),
+                               M.k9_dense_rows);
       else
         dev::launch_near_mrhs2(st, M.sym_items.as<dev::SymRowItem>(), M.n_sym_items, M.sym_blocks.as<dev::SymBlock>(),
                                I.D.as<double>(), M.xp.as<double>(), M.n, mm, M.sym_pstride, M.sym_part_m.as<double>());

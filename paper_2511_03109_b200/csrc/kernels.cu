@@ -1604,19 +1604,22 @@ __global__ void __maxnreg__(96) k_inst_tma(const double* __restrict__ G, std::in
 // from the 8 consumer warps, which only run DMMA. Reads past the chunk (odd
 // lengths, k beyond the chunk, rows beyond the slice) are masked to zero
 // before they reach an MMA, so stale shared memory never contributes.
-template <int NC>
+template <int NC, int NST>
 __global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ items,
                                               const SymBlock* __restrict__ blocks, const double* __restrict__ D,
                                               const double* __restrict__ X, std::int64_t n, int m,
-                                              std::int64_t pstride, double* __restrict__ part) {
+                                              std::int64_t pstride, double* __restrict__ part, int dstage) {
   constexpr int NTN = NC / 8;
   constexpr int YQ = NC / 8;  // Y (m-tile, n-tile) pairs per consumer warp (<= 8 m-tiles x NTN / 8 warps)
   constexpr int LDX = kK9bKc + 4;
-  constexpr int STAGE = kK9bKc * kK9bLd + NC * LDX;
+  // dstage: doubles of D per stage -- 32 x 132 when some item is a row
+  // slice (column copies), else 32 x the tallest leaf (+2), which leaves
+  // room for a deeper ring (NST) at two CTAs per SM
+  const int STAGE = dstage + NC * LDX;
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) std::uint64_t full[2], empty[2];
+  __shared__ __align__(8) std::uint64_t full[NST], empty[NST];
   double* Xs = sm;                      // X_sigma: [c][r], ld 132 (consumers stage it)
-  double* St = sm + NC * kK9bLd;        // 2 stages: D chunk [k][shift + r] then X_tau [c][shift + k]
+  double* St = sm + NC * kK9bLd;        // NST stages: D chunk [k][shift + r] then X_tau [c][shift + k]
   const SymRowItem it = items[blockIdx.x];
   const int c0 = blockIdx.y * NC;
   const int ncr = min(NC, m - c0);      // RHS columns of this tile
@@ -1630,9 +1633,9 @@ __global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ item
   // bulk copy with column stride R (else one copy per column, stride 132)
   const bool dense = it.i0 == 0 && ld == R;
   const int cs = dense ? R : kK9bLd;
-  PHM_DCHECK(R >= 1 && R <= 128 && it.i0 + R <= it.ld);
+  PHM_DCHECK(R >= 1 && R <= 128 && it.i0 + R <= it.ld && (dense ? kK9bKc * R + 2 : kK9bKc * kK9bLd) <= dstage);
   if (tid == 0) {
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NST; ++q) {
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], 8);
     }
@@ -1644,11 +1647,11 @@ __global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ item
     for (int b = it.bbeg; b < it.bend; ++b) {
       const SymBlock blk = blocks[b];
       for (int j0 = 0; j0 < blk.ncol; j0 += kK9bKc, ++c) {
-        const int slot = c & 1;
-        if (c >= 2) mbar_wait(&empty[slot], ((c >> 1) - 1) & 1);
+        const int slot = c % NST;
+        if (c >= NST) mbar_wait(&empty[slot], ((c / NST) - 1) & 1);
         const int kc = min(kK9bKc, blk.ncol - j0);
         double* Dc = St + slot * STAGE;
-        double* Xt = Dc + kK9bKc * kK9bLd;
+        double* Xt = Dc + dstage;
         // lane k: column k of the chunk (whole-leaf items: lane 0 copies the
         // contiguous chunk at once); lane c (< ncr): RHS column c of X_tau
         unsigned bytes_d = 0, bytes_x = 0;
@@ -1698,11 +1701,11 @@ __global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ item
     const SymBlock blk = blocks[b];
     const std::uintptr_t dbase = reinterpret_cast<std::uintptr_t>(D + blk.d_off + it.i0);
     for (int j0 = 0; j0 < blk.ncol; j0 += kK9bKc, ++c) {
-      const int slot = c & 1;
+      const int slot = c % NST;
       const int kc = min(kK9bKc, blk.ncol - j0);
-      mbar_wait(&full[slot], (c >> 1) & 1);
+      mbar_wait(&full[slot], (c / NST) & 1);
       const double* Dc = St + slot * STAGE;
-      const double* Xt = Dc + kK9bKc * kK9bLd;
+      const double* Xt = Dc + dstage;
       // element (r, k) of the chunk sits at Dc[k * cs + sh(k) + r]
       const int sh_chunk = static_cast<int>(((dbase >> 3) + static_cast<std::uintptr_t>(j0 * ld)) & 1);
       auto dsh = [&](int k) {
@@ -2446,19 +2449,38 @@ void launch_near_gather(cudaStream_t st, int nleaves, const std::int64_t* leaf_r
 }
 
 void launch_near_mrhs3(cudaStream_t st, const SymRowItem* items, int nitems, const SymBlock* blocks, const double* D,
-                       const double* X, std::int64_t n, int m, std::int64_t pstride, double* part) {
+                       const double* X, std::int64_t n, int m, std::int64_t pstride, double* part, int dense_rows) {
   if (nitems == 0) return;
-#define PHM_K9C(NC)                                                                                         \
-  {                                                                                                         \
-    const size_t smem = (NC * kK9bLd + 2 * (kK9bKc * kK9bLd + NC * (kK9bKc + 4))) * sizeof(double);       \
-    smem_attr(reinterpret_cast<const void*>(k_near_mrhs3<NC>), static_cast<int>(smem), true);              \
+  // D per stage: 32 columns of the tallest leaf when every item is a whole
+  // leaf (one bulk copy per chunk), else 32 padded columns of 132
+  const int dstage = dense_rows > 0 ? ((kK9bKc * dense_rows + 2 + 1) & ~1) : kK9bKc * kK9bLd;
+  static const int nst_env = [] {  // tuning: ring depth
+    const char* e = std::getenv("PHM_K9_STAGES");
+    return e ? std::atoi(e) : 0;
+  }();
+  auto bytes = [&](int nc, int nst) {
+    return static_cast<size_t>(nc * kK9bLd + nst * (dstage + nc * (kK9bKc + 4))) * sizeof(double);
+  };
+  const int nc = m <= 8 ? 8 : (m <= 16 ? 16 : 32);
+  // the deepest ring (<= 4) that keeps two CTAs per SM
+  int nst = 2;
+  for (int q = 4; q > 2; --q)
+    if (bytes(nc, q) + 2048 <= 113 * 1024) {
+      nst = q;
+      break;
+    }
+  if (nst_env >= 2 && nst_env <= 4) nst = nst_env;
+#define PHM_K9C(NC, NST)                                                                                    \
+  if (nc == NC && nst == NST) {                                                                             \
+    const size_t smem = bytes(NC, NST);                                                                     \
+    smem_attr(reinterpret_cast<const void*>(k_near_mrhs3<NC, NST>), static_cast<int>(smem), true);         \
     const dim3 grid(static_cast<unsigned>(nitems), static_cast<unsigned>((m + NC - 1) / NC));               \
-    k_near_mrhs3<NC><<<grid, kTmaThreads, smem, st>>>(items, blocks, D, X, n, m, pstride, part);            \
+    k_near_mrhs3<NC, NST><<<grid, kTmaThreads, smem, st>>>(items, blocks, D, X, n, m, pstride, part, dstage); \
     return;                                                                                                 \
   }
-  if (m <= 8) PHM_K9C(8)
-  if (m <= 16) PHM_K9C(16)
-  PHM_K9C(32)
+  PHM_K9C(8, 2) PHM_K9C(8, 3) PHM_K9C(8, 4)
+  PHM_K9C(16, 2) PHM_K9C(16, 3) PHM_K9C(16, 4)
+  PHM_K9C(32, 2) PHM_K9C(32, 3) PHM_K9C(32, 4)
 #undef PHM_K9C
 }
 
