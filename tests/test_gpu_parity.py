@@ -578,3 +578,45 @@ def test_coupling_schedule_does_not_change_results(ph, tmp_path):
     assert np.array_equal(ref[0], ref[2]) and np.array_equal(ref[1], ref[3])  # direct vs captured vs replayed
     for tag in ("full", "unordered", "nographs"):
         assert np.array_equal(outs[tag], ref), tag
+
+
+_K9_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2511_03109_b200 as ph
+pts = ph.generate_points(9000, 3, 8)
+cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=3, p_s=4, p_theta=8, eta=1.0,
+                  near_mode=ph.NearMode.SNAPSHOT)
+pm = ph.offline_h2(pts, cfg)
+inst = ph.instantiate(pm, [0.21])
+X = np.stack([ph.generate_normal(9000, 30 + j) for j in range(int(sys.argv[3]))], axis=1)
+np.save(sys.argv[2], inst.apply(X))
+"""
+
+
+@pytest.mark.parametrize("m", [10, 24])
+def test_k9_ring_depth_does_not_change_results(ph, po, tmp_path, m):
+    """The two-sided K9 picks its ring depth from the tallest leaf
+    (PHM_K9_STAGES overrides it); every depth gives bitwise the same y, and
+    y matches the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "k9.py"
+    script.write_text(_K9_SCRIPT)
+    outs = {}
+    for st in ("0", "2", "3"):
+        out = tmp_path / f"y{st}.npy"
+        subprocess.run([sys.executable, str(script), root, str(out), str(m)], check=True, timeout=600,
+                       env={**os.environ, "PHM_K9_STAGES": st})
+        outs[st] = np.load(out)
+    assert np.array_equal(outs["0"], outs["2"]) and np.array_equal(outs["0"], outs["3"])
+    pts = ph.generate_points(9000, 3, 8)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=3, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    om = po.from_product(ph.offline_structure(pts, cfg), pts).instantiate([0.21])
+    X = np.stack([ph.generate_normal(9000, 30 + j) for j in range(m)], axis=1)
+    ref = np.stack([om.apply(X[:, j]) for j in range(m)], axis=1)
+    assert rel(outs["0"], ref) <= TOL_Y
