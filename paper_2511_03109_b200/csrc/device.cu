@@ -149,6 +149,7 @@ struct NvtxRange {
 
 struct Context {
   int device = 0;
+  std::recursive_mutex exec_mu;  // see DevMatrix::exec_mu()
   int sms = 148;  // multiprocessors of the device
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
@@ -309,17 +310,25 @@ std::shared_ptr<Context> context_create(int device) {
   ctx->stream = ctx->own;
   return ctx;
 }
-void context_set_stream(Context& ctx, void* s) { ctx.stream = s ? static_cast<cudaStream_t>(s) : ctx.own; }
+void context_set_stream(Context& ctx, void* s) {
+  std::lock_guard<std::recursive_mutex> lk(ctx.exec_mu);
+  ctx.stream = s ? static_cast<cudaStream_t>(s) : ctx.own;
+}
 void* context_stream(Context& ctx) { return ctx.stream; }
 void context_sync(Context& ctx) { CK(cudaStreamSynchronize(ctx.stream)); }
-void context_enable_timing(Context& ctx, bool on) { ctx.timing = on; }
+void context_enable_timing(Context& ctx, bool on) {
+  std::lock_guard<std::recursive_mutex> lk(ctx.exec_mu);
+  ctx.timing = on;
+}
 void context_timer(Context& ctx, const std::string& name, double* ms, std::int64_t* count) {
+  std::lock_guard<std::recursive_mutex> lk(ctx.exec_mu);
   ctx.flush_timers();
   auto it = ctx.totals.find(name);
   *ms = it == ctx.totals.end() ? 0.0 : it->second.first;
   *count = it == ctx.totals.end() ? 0 : it->second.second;
 }
 void context_reset_timers(Context& ctx) {
+  std::lock_guard<std::recursive_mutex> lk(ctx.exec_mu);
   ctx.flush_timers();
   ctx.totals.clear();
 }
@@ -398,10 +407,13 @@ struct DevMatrix {
   // pooled instance buffers
   std::vector<DBuf> pool_D;
   std::mutex mu;
-  // Serialises the public entry points on one matrix: they share its
-  // workspace (xp, yp, x-hat, ...) and enqueue on one stream, so two host
-  // threads must not interleave their launch sequences.
-  std::recursive_mutex exec_mu;
+  // Serialises the public entry points: a matrix's workspace (xp, yp,
+  // x-hat, ...) is its own, but its stream, side stream, fork / join events,
+  // launch counter and timer records live on the Context that every matrix
+  // built on it shares, so the lock is the Context's (own_mu for host-only
+  // matrices, which have none).
+  std::recursive_mutex own_mu;
+  std::recursive_mutex& exec_mu() { return ctx ? ctx->exec_mu : own_mu; }
   std::int64_t device_bytes = 0;
 
   cudaStream_t st() const { return ctx->stream; }
@@ -420,7 +432,12 @@ struct DevInstance {
     std::int64_t ws_gen = -1;
     std::int64_t launches = 0;  // kernels in the graph (for the launch count)
     bool seen = false;          // the first call runs directly (lazy buffers)
+    std::uint64_t last_use = 0;
   };
+  // LRU bound: the fused step's graphs are keyed by the caller's x pointer,
+  // which an HPO loop over a caching allocator may vary without end
+  static constexpr std::size_t kMaxGraphs = 16;
+  std::uint64_t graph_tick = 0;
   // key: (launch sequence, input pointer it reads, RHS count)
   std::map<std::tuple<int, const void*, Index>, Graph> graphs;
   ~DevInstance() {
@@ -987,12 +1004,17 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     M.capB = maxB;
     M.capT = std::max(maxrl * 32, maxrl * maxs1);
     if (M.h2 && M.P == 64) {  // C = L (H R^T) on DMMA: T (rl4 x 64, ld ldT), then R / L (ld 68) staged
-      const int rl4 = (maxrl + 3) & ~3, rr4 = (maxrr + 3) & ~3;
-      int ldT = 0;  // k_class_inst's T stride: the least ld >= rl4 with ld = 4 mod 16, over all classes
+      // only classes with rl <= 64 take the DMMA path in k_class_inst; the
+      // others use the plain path sized by maxrl above
+      int mrl = 0, mrr = 0, ldT = 0;  // ldT: the least ld >= rl4 with ld = 4 mod 16
       for (const auto& cm : M.cmeta_h) {
+        if (cm.rl > 64) continue;
+        mrl = std::max(mrl, cm.rl);
+        mrr = std::max(mrr, cm.rr);
         const int r4 = (cm.rl + 3) & ~3;
         ldT = std::max(ldT, r4 + ((4 - r4) & 15));
       }
+      const int rl4 = (mrl + 3) & ~3, rr4 = (mrr + 3) & ~3;
       M.capT = std::max(M.capT, ldT * 64);
       M.capL = 68 * std::max(rl4, rr4);  // L, and R before it
     }
@@ -1432,7 +1454,7 @@ void run_instantiate_batch(const std::vector<DevInstance*>& insts, const double*
 }  // namespace
 
 std::shared_ptr<DevInstance> baseline_instance(std::shared_ptr<DevMatrix> m) {
-  std::lock_guard<std::recursive_mutex> exec_lock(m->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(m->exec_mu());
   PHM_CHECK(m->baseline, "baseline_instance: not a baseline matrix");
   CK(cudaSetDevice(m->ctx->device));
   auto I = alloc_instance(m);
@@ -1448,7 +1470,7 @@ std::shared_ptr<DevMatrix> baseline_build(std::shared_ptr<Context> ctx, const do
 
 std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const double* theta, int n_theta,
                                          StageCounters* counters) {
-  std::lock_guard<std::recursive_mutex> exec_lock(m->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(m->exec_mu());
   if (!m->ctx) throw std::logic_error("instantiate: host-only matrix (built without a device)");
   if (m->baseline) throw std::logic_error("instantiate: a baseline matrix is built at a fixed theta");
   CK(cudaSetDevice(m->ctx->device));
@@ -1461,7 +1483,7 @@ std::shared_ptr<DevInstance> instantiate(std::shared_ptr<DevMatrix> m, const dou
 
 std::vector<std::shared_ptr<DevInstance>> instantiate_batch(std::shared_ptr<DevMatrix> m, const double* thetas,
                                                             int n_theta, int count, StageCounters* counters) {
-  std::lock_guard<std::recursive_mutex> exec_lock(m->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(m->exec_mu());
   if (!m->ctx) throw std::logic_error("instantiate: host-only matrix (built without a device)");
   if (m->baseline) throw std::logic_error("instantiate: a baseline matrix is built at a fixed theta");
   PHM_CHECK(count >= 1, "instantiate_batch: count must be >= 1");
@@ -1479,7 +1501,7 @@ std::vector<std::shared_ptr<DevInstance>> instantiate_batch(std::shared_ptr<DevM
 
 void reinstantiate_batch(const std::vector<DevInstance*>& insts, const double* thetas, int n_theta,
                          StageCounters* counters) {
-  std::lock_guard<std::recursive_mutex> exec_lock(insts.at(0)->M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(insts.at(0)->M->exec_mu());
   PHM_CHECK(!insts.empty(), "reinstantiate_batch: no instances");
   if (insts[0]->M->baseline) throw std::logic_error("reinstantiate: a baseline matrix is built at a fixed theta");
   for (DevInstance* I : insts) PHM_CHECK(I->M == insts[0]->M, "reinstantiate_batch: instances of different matrices");
@@ -1487,7 +1509,7 @@ void reinstantiate_batch(const std::vector<DevInstance*>& insts, const double* t
 }
 
 void reinstantiate(DevInstance& inst, const double* theta, int n_theta, StageCounters* counters) {
-  std::lock_guard<std::recursive_mutex> exec_lock(inst.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(inst.M->exec_mu());
   NvtxRange nvtx("phm::instantiate");
   if (inst.M->baseline) throw std::logic_error("reinstantiate: a baseline matrix is built at a fixed theta");
   run_instantiate(inst, theta, n_theta, counters);
@@ -1496,7 +1518,7 @@ const std::vector<double>& instance_theta(const DevInstance& inst) { return inst
 void instance_sync(DevInstance& inst) { CK(cudaStreamSynchronize(inst.M->st())); }
 
 void instance_far_h(DevInstance& I, Index far_index, std::vector<double>& out, Index& rows, Index& cols) {
-  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
   const DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   if (far_index < 0 || far_index >= static_cast<Index>(H.blocks.far.size())) throw std::out_of_range("far index");
@@ -1510,7 +1532,7 @@ void instance_far_h(DevInstance& I, Index far_index, std::vector<double>& out, I
 }
 
 void instance_near_d(DevInstance& I, Index b, std::vector<double>& out) {
-  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
   const DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   if (b < 0 || b >= static_cast<Index>(H.blocks.near.size())) throw std::out_of_range("near index");
@@ -1530,7 +1552,7 @@ void instance_near_d(DevInstance& I, Index b, std::vector<double>& out) {
 }
 
 void instance_class_c(DevInstance& I, Index k, std::vector<double>& out) {
-  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
   const DevMatrix& M = *I.M;
   if (!M.h2) throw std::invalid_argument("explicit C_k exists only for the H2 format");
   if (k < 0 || k >= M.ncls) throw std::out_of_range("class index");
@@ -1570,7 +1592,10 @@ void far_chain(DevInstance& I, Index m, cudaStream_t fs, int coupling_ctas) {
   ctx.run_on(fs, "zero", [&] { dev::launch_zero(fs, M.yhat.as<double>(), static_cast<std::int64_t>(M.nnodes) * P * m); });
   if (M.cp_mma) {
     const size_t need = sizeof(double) * std::max(1, M.n_cg_items) * m * dev::kGroupSlots * P;
-    if (M.cg_partial.bytes < need) M.cg_partial.alloc(need);
+    if (M.cg_partial.bytes < need) {
+      M.cg_partial.alloc(need);
+      ++M.ws_gen;  // captured graphs hold the old pointer
+    }
     ctx.stamp(fs, 5);
     ctx.run_on(fs, "coupling", [&] {
       dev::launch_coupling_mma(fs, M.cg_items.as<dev::CouplingItem>(), M.cg_order.as<std::int32_t>(), M.n_cg_items,
@@ -1632,7 +1657,10 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
   // 3.3 ms of gather), except on a symmetric shard, which needs both sides.
   if (m >= kMrhsMin && M.n_sym_items > 0 && two_sided && (m <= 32 || (M.sym && M.sharded))) {
     const size_t need = sizeof(double) * M.sym_pstride * m;
-    if (M.sym_part_m.bytes < need) M.sym_part_m.alloc(need);
+    if (M.sym_part_m.bytes < need) {
+      M.sym_part_m.alloc(need);
+      ++M.ws_gen;  // captured graphs hold the old pointer
+    }
     static const int k9v = [] {
       const char* e = std::getenv("PHM_K9_TMA");
       return e ? std::atoi(e) : 1;
@@ -1763,7 +1791,16 @@ void run_graphed(DevInstance& I, int seq, const void* input, Index m, F&& body) 
     body();
     return;
   }
-  DevInstance::Graph& g = I.graphs[std::make_tuple(seq, input, m)];
+  const auto key = std::make_tuple(seq, input, m);
+  if (I.graphs.find(key) == I.graphs.end() && I.graphs.size() >= DevInstance::kMaxGraphs) {
+    auto lru = I.graphs.begin();
+    for (auto it = I.graphs.begin(); it != I.graphs.end(); ++it)
+      if (it->second.last_use < lru->second.last_use) lru = it;
+    if (lru->second.exec) CK(cudaGraphExecDestroy(lru->second.exec));
+    I.graphs.erase(lru);
+  }
+  DevInstance::Graph& g = I.graphs[key];
+  g.last_use = ++I.graph_tick;
   if (!g.seen || g.ws_gen != M.ws_gen) {
     if (g.exec) CK(cudaGraphExecDestroy(g.exec));
     g.exec = nullptr;
@@ -1813,7 +1850,7 @@ void run_graphed(DevInstance& I, int seq, const void* input, Index m, F&& body) 
 }
 
 void apply_device(DevInstance& I, const double* x_dev, double* y_dev, Index m) {
-  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
   NvtxRange nvtx("phm::apply");
   DevMatrix& M = *I.M;
   PHM_CHECK(m >= 1, "apply: m must be >= 1");
@@ -1826,7 +1863,7 @@ void apply_device(DevInstance& I, const double* x_dev, double* y_dev, Index m) {
 }
 
 void apply_host(DevInstance& I, const double* x, double* y, Index m) {
-  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   if (H.row_begin != 0 || H.row_end != M.n)
@@ -1946,7 +1983,7 @@ void instantiate_apply_tree(DevInstance& I, const double* theta, int n_theta, co
 
 void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, const double* x_dev, double* y_dev,
                               Index m, StageCounters* counters) {
-  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
   NvtxRange nvtx("phm::instantiate_apply");
   DevMatrix& M = *I.M;
   if (M.sharded)
@@ -1960,7 +1997,7 @@ void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, 
 
 void instantiate_apply_partial_device(DevInstance& I, const double* theta, int n_theta, const double* x_dev,
                                       double* ypart_dev, Index m, StageCounters* counters) {
-  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
   DevMatrix& M = *I.M;
   instantiate_apply_tree(I, theta, n_theta, x_dev, m, counters);
   CK(cudaMemcpyAsync(ypart_dev, M.yp.p, sizeof(double) * M.n * m, cudaMemcpyDeviceToDevice, M.st()));
@@ -1974,7 +2011,7 @@ void instantiate_apply_partial_device(DevInstance& I, const double* theta, int n
 double estimate_error(DevInstance& I, Index probe_rows, std::uint64_t seed, StageCounters* counters,
                       std::vector<Index>* rows_out, std::vector<double>* exact_out, std::vector<double>* approx_out,
                       std::vector<double>* x_out) {
-  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   const Tree& T = *H.tree;
@@ -2028,7 +2065,7 @@ double estimate_error(DevInstance& I, Index probe_rows, std::uint64_t seed, Stag
 
 void instantiate_apply_host(DevInstance& I, const double* theta, int n_theta, const double* x, double* y, Index m,
                             StageCounters* counters) {
-  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
   DevMatrix& M = *I.M;
   CK(cudaSetDevice(M.ctx->device));
   ensure_workspace(M, m);
@@ -2040,7 +2077,7 @@ void instantiate_apply_host(DevInstance& I, const double* theta, int n_theta, co
 }
 
 void apply_device_partial(DevInstance& I, const double* x_dev, double* ypart_dev, Index m) {
-  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
   DevMatrix& M = *I.M;
   PHM_CHECK(m >= 1, "apply: m must be >= 1");
   CK(cudaSetDevice(M.ctx->device));
@@ -2052,7 +2089,7 @@ void apply_device_partial(DevInstance& I, const double* x_dev, double* ypart_dev
 }
 
 void apply_device_rows(DevInstance& I, const double* x_dev, double* yrows_dev, Index m) {
-  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu);
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   if (M.sym && M.sharded)

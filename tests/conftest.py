@@ -38,3 +38,12 @@ def po():
 
     pyoracle.lib()
     return pyoracle
+
+
+@pytest.fixture(scope="session")
+def pr():
+    """The compiled reference (oracle/_ref/libphmat_ref.so, test infrastructure)."""
+    from oracle import pyref
+
+    pyref.lib()
+    return pyref

@@ -1,16 +1,17 @@
 """Generates tests/golden/*.npz: small seeded cases of the parametric path
-with the oracle's outputs (instantiated near blocks D_b, class tensors H_k /
-C_k, and y = K(theta) x), so the GPU parity tests can check the CUDA path
-against committed vectors without running the oracle, and the CPU tests can
-detect any drift of the oracle itself.
+with the reference's outputs (instantiated near blocks D_b, class tensors
+H_k / C_k, and y = K(theta) x), so the GPU parity tests can check the CUDA
+path against committed vectors with no checker in the loop, and the CPU
+tests can detect any drift of the oracle or of the reference build.
 
-Provenance: the reference (proj/, C++ with Eigen3) cannot be built in this
-image, so these vectors come from the oracle (oracle/oracle.cpp, the CPU
-restatement of the reference's online path), which tests/test_oracle_pins.py
-pins against the reference's own known-answer tests. The offline data (the
-TT cores of the classes and of TT-mode near blocks) is the product's host
-build (phm_matrix_build_host), the same code on every machine; snapshot-mode
-near tensors are evaluated by the oracle.
+Provenance: the REFERENCE ITSELF -- the unmodified proj/src compiled by
+oracle/ref_build.sh against oracle/eigen_shim into oracle/_ref/libphmat_ref.so
+(pyref). The reference rebuilds tree, blocks, classes, grids and basis from
+the points, evaluates every snapshot-mode near tensor with its own
+near_oracle (nearfield.cpp:7-48), and runs its own instantiate / apply /
+pttk_online / assemble_L_R. The offline TT data both sides share (the TT
+cores of the classes and of TT-mode near blocks) is the product's host build
+(phm_matrix_build_host), the same code on every machine.
 
     python tests/golden/make_golden.py      # rewrites the .npz files
 """
@@ -48,11 +49,10 @@ def sample_ids(count, k):
     return np.unique(np.linspace(0, count - 1, min(k, count)).astype(np.int64))
 
 
-def generate(ph, po, name, spec):
+def generate(ph, pr, name, spec):
     pts, cfg, fmt, thetas, m = spec
     pm = ph.offline_structure(pts, cfg, fmt)
-    om = po.from_product(pm, pts)
-    sizes = pm.nodes()[0][:, 3]
+    R = pr.RefMatrix.from_product(pm, pts, near="tt" if cfg.near_mode == ph.NearMode.TT else "snapshot")
     near, far, key = pm.blocks()
     info = pm.info()
     nb = sample_ids(len(near), 8)
@@ -60,25 +60,24 @@ def generate(ph, po, name, spec):
     X = np.stack([ph.generate_normal(pts.shape[0], 7 + j) for j in range(m)], axis=1)
     out = {"points": pts, "x": X, "thetas": np.array(thetas, dtype=np.float64), "near_ids": nb, "class_ids": ks}
     for i, th in enumerate(thetas):
-        oi = om.instantiate(th)
-        out[f"y{i}"] = np.stack([oi.apply(X[:, j]) for j in range(m)], axis=1)
+        ri = R.instantiate(th)
+        out[f"y{i}"] = ri.apply(X)
         for b in nb:
-            s, t = near[b]
-            out[f"d{i}_{b}"] = oi.near(int(b), (int(sizes[s]), int(sizes[t])))
+            out[f"d{i}_{b}"] = ri.near_d(int(b))
         for k in ks:
-            out[f"h{i}_{k}"] = oi.class_h(int(k))
+            out[f"h{i}_{k}"] = R.class_h(int(k), th)
             if fmt == ph.Format.H2:
-                out[f"c{i}_{k}"] = oi.class_c(int(k), info["P"])
+                out[f"c{i}_{k}"] = R.class_c(int(k), th, info["P"])
     np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
     return out
 
 
 def main():
     import paper_2511_03109_b200 as ph
-    from oracle import pyoracle as po
+    from oracle import pyref as pr
 
     for name, spec in cases(ph).items():
-        out = generate(ph, po, name, spec)
+        out = generate(ph, pr, name, spec)
         print(name, sum(v.nbytes for v in out.values()), "bytes")
 
 

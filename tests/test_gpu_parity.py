@@ -620,3 +620,62 @@ def test_k9_ring_depth_does_not_change_results(ph, po, tmp_path, m):
     X = np.stack([ph.generate_normal(9000, 30 + j) for j in range(m)], axis=1)
     ref = np.stack([om.apply(X[:, j]) for j in range(m)], axis=1)
     assert rel(outs["0"], ref) <= TOL_Y
+
+
+def test_graph_replay_after_workspace_growth(ph, po):
+    """the lazily grown two-sided K9 partials must not be
+    left dangling in a captured graph. Sequence m = 64, 8, 8 (captured), 16
+    (grows the partials), 8 (replay) against the oracle, plus more distinct
+    x pointers than the graph cache holds (LRU eviction)."""
+    import torch
+
+    pts = ph.generate_points(2500, 3, 19)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    inst = ph.instantiate(pm, [0.25])
+    oi = om.instantiate([0.25])
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal((2500, 64))
+    Yo = oi.apply(X)
+    for m in (64, 8, 8, 16, 8, 8, 32, 8):
+        assert rel(inst.apply(X[:, :m]), Yo[:, :m]) <= TOL_Y, m
+    xs = [torch.from_numpy(X[:, j].copy()).cuda() for j in range(20)]
+    y = torch.zeros(2500, dtype=torch.float64, device="cuda")
+    oi2 = om.instantiate([0.37])
+    for rep in range(2):
+        for j, xd in enumerate(xs):
+            inst.instantiate_apply_device([0.37], xd.data_ptr(), y.data_ptr(), 1)
+            pm.ctx.sync()
+            if j % 7 == 0:
+                assert rel(y.cpu().numpy(), oi2.apply(X[:, j])) <= TOL_Y
+
+
+def test_two_matrices_on_one_context_from_two_threads(ph, po):
+    """matrices sharing a Context serialise on the
+    Context's lock (its stream, events and timers are shared)."""
+    import threading
+
+    pts = ph.generate_points(1800, 3, 23)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    a, oa = _build(ph, po, pts, cfg, ph.Format.H2)
+    b, ob = _build(ph, po, pts, cfg, ph.Format.H2)
+    assert a.ctx is b.ctx
+    x = ph.generate_normal(1800, 4)
+    ya, yb = oa.instantiate([0.2]).apply(x), ob.instantiate([0.4]).apply(x)
+    errs = []
+
+    def run(pm, th, yref):
+        inst = ph.instantiate(pm, th)
+        for _ in range(30):
+            e = rel(inst.instantiate_apply(th, x), yref)
+            if e > TOL_Y:
+                errs.append(e)
+
+    ts = [threading.Thread(target=run, args=(a, [0.2], ya)), threading.Thread(target=run, args=(b, [0.4], yb))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs

@@ -1,0 +1,191 @@
+"""GPU parity against the COMPILED REFERENCE (oracle/_ref/libphmat_ref.so: the
+unmodified proj/src built against oracle/eigen_shim), at every BASELINE
+config's own size that fits one GPU.
+
+The reference rebuilds tree / blocks / classes / grids / basis from the same
+points, evaluates every snapshot-mode near tensor itself (near_oracle,
+nearfield.cpp:7-48) and runs its own instantiate / apply / pttk_online /
+assemble_L_R / coupling_apply / nearfield_online. It is handed only the
+offline coupling TT cores (the data both sides share).
+
+Tolerances are the north_star's (fp64): D_b, H_k, C_k within 1e-12 relative
+Frobenius; y within 1e-11 relative 2-norm.
+
+* C1 (BASELINE configs[0]) at full size: n = 4096, 2D, param-H, Gaussian,
+  all 16 evenly spaced l; every D_b, every far H_b, S_b/T_b, and y.
+* C2 (configs[1]) at full size: n = 65,536, 2D, H^2, Matern-3/2, p_s = 8,
+  p_theta = 10; 3 harness theta draws; every D_b, H_k and C_k, and y.
+* C3 (configs[2], the headline) at full size: n = 2^18; 2,000 sampled D_b,
+  every H_k, 300 sampled C_k, and y (plain apply and the fused step) on
+  probe rows, composed by the reference from the blocks that reach them.
+* C4 form (configs[3]) at the largest n one GPU holds with the config's
+  leaf size: n = 2^17 mixture, leaf 32, Matern-5/2 x sigma^2 on 8 x 6,
+  64 RHS: sampled D_b / C_k and probe rows of 4 RHS columns.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_BLOCK = 1e-12
+TOL_Y = 1e-11
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+THREADS = os.cpu_count() or 1
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def _bench():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    return bench
+
+
+def _sizes(pm):
+    return pm.nodes()[0][:, 3]
+
+
+def _first_far_of_class(pm):
+    _, _, key = pm.blocks()
+    first = np.full(pm.info()["n_classes"], -1, dtype=np.int64)
+    for i in range(len(key) - 1, -1, -1):
+        first[key[i]] = i
+    return first
+
+
+def _check_blocks(ph, pm, inst, R, theta, near_ids, class_ids, ri=None):
+    sizes = _sizes(pm)
+    near, _, _ = pm.blocks()
+    first = _first_far_of_class(pm)
+    wd = 0.0
+    for b in near_ids:
+        s, t = near[b]
+        g = inst.near_d(int(b), (int(sizes[s]), int(sizes[t])))
+        r = ri.near_d(int(b)) if ri is not None else R.near_online(int(b), theta)
+        wd = max(wd, rel(g, r))
+    assert wd <= TOL_BLOCK, f"D_b rel err {wd:.3e}"
+    info = pm.info()
+    wh = wc = 0.0
+    for k in class_ids:
+        wh = max(wh, rel(inst.far_h(int(first[k])), R.class_h(int(k), theta)))
+        if pm.format == ph.Format.H2:
+            wc = max(wc, rel(inst.class_c(int(k)), R.class_c(int(k), theta, info["P"])))
+    assert wh <= TOL_BLOCK, f"H_k rel err {wh:.3e}"
+    assert wc <= TOL_BLOCK, f"C_k rel err {wc:.3e}"
+    return wd, wh, wc
+
+
+def test_c1_full_size_vs_reference(ph, pr):
+    b = _bench()
+    c = b.CONFIGS["c1"]
+    pts = b.make_points(ph, c, 0)
+    assert np.array_equal(pts, pr.generate_points(c["n"], c["d"], 0))
+    pm = ph.offline_h(pts, b.make_cfg(ph, c))
+    R = pr.RefMatrix.from_product(pm, pts, near="snapshot", threads=THREADS)
+    near, far, key = pm.blocks()
+    # S_b, T_b: the reference's own pttk_offline
+    for i in range(len(far)):
+        S, T = pm.far_st(i)
+        Sr, Tr = R.far_st(i)
+        assert rel(S, Sr) <= TOL_BLOCK and rel(T, Tr) <= TOL_BLOCK
+    x = ph.generate_normal(c["n"], 1)
+    for j in range(16):
+        theta = [0.1 + 0.9 * j / 15]
+        inst, ri = ph.instantiate(pm, theta), R.instantiate(theta)
+        _check_blocks(ph, pm, inst, R, theta, range(len(near)), range(pm.info()["n_classes"]), ri=ri)
+        wf = max(rel(inst.far_h(i), ri.far_h(i)) for i in range(len(far)))
+        assert wf <= TOL_BLOCK
+        assert rel(inst.apply(x), ri.apply(x)) <= TOL_Y
+        assert rel(inst.instantiate_apply(theta, x), ri.apply(x)) <= TOL_Y
+
+
+def test_c2_full_size_vs_reference(ph, pr):
+    b = _bench()
+    c = b.CONFIGS["c2"]
+    pts = b.make_points(ph, c, 0)
+    pm = ph.offline_h2(pts, b.make_cfg(ph, c))
+    R = pr.RefMatrix.from_product(pm, pts, near="snapshot", threads=THREADS)
+    near, _, _ = pm.blocks()
+    x = ph.generate_normal(c["n"], 1)
+    for theta in b.theta_vectors(c, 3, 0):
+        theta = list(theta)
+        inst, ri = ph.instantiate(pm, theta), R.instantiate(theta)
+        _check_blocks(ph, pm, inst, R, theta, range(len(near)), range(pm.info()["n_classes"]), ri=ri)
+        y = ri.apply(x)
+        assert rel(inst.apply(x), y) <= TOL_Y
+        assert rel(inst.instantiate_apply(theta, x), y) <= TOL_Y
+
+
+@pytest.fixture(scope="module")
+def c3(ph, pr):
+    b = _bench()
+    c = b.CONFIGS["c3"]
+    pts = b.make_points(ph, c, 0)
+    pm = ph.offline_h2(pts, b.make_cfg(ph, c))
+    R = pr.RefMatrix.from_product(pm, pts, near="none", finalize=False)
+    return pm, R, c, pts
+
+
+def test_c3_full_size_blocks_vs_reference(ph, c3):
+    pm, R, c, pts = c3
+    b = _bench()
+    info = pm.info()
+    rng = np.random.default_rng(3)
+    near_ids = np.sort(rng.choice(info["n_near"], 2000, replace=False))
+    cls = np.sort(rng.choice(info["n_classes"], 300, replace=False))
+    for theta in b.theta_vectors(c, 2, 0):
+        theta = list(theta)
+        inst = ph.instantiate(pm, theta)
+        _check_blocks(ph, pm, inst, R, theta, near_ids, cls)
+        # every class's H_k
+        first = _first_far_of_class(pm)
+        wh = max(rel(inst.far_h(int(first[k])), R.class_h(k, theta)) for k in range(info["n_classes"]))
+        assert wh <= TOL_BLOCK
+
+
+def test_c3_full_size_y_rows_vs_reference(ph, c3):
+    pm, R, c, pts = c3
+    b = _bench()
+    x = ph.generate_normal(c["n"], 1)
+    rows = np.sort(np.random.default_rng(5).choice(c["n"], 48, replace=False))
+    inst = ph.instantiate(pm, [0.3])
+    for theta in b.theta_vectors(c, 2, 1):
+        theta = list(theta)
+        yr = R.apply_rows(theta, x, rows, threads=THREADS)
+        inst.reinstantiate(theta)
+        assert rel(inst.apply(x)[rows], yr) <= TOL_Y
+        assert rel(inst.instantiate_apply(theta, x)[rows], yr) <= TOL_Y
+
+
+def test_c4_form_largest_single_gpu_vs_reference(ph, pr):
+    """BASELINE configs[3] form with its leaf size (32) at n = 2^17 (l_max 4):
+    mixture of 16 Gaussians, Matern-5/2 x sigma^2 on an 8 x 6 grid, 64 RHS
+    through the block (DMMA) path. 1.26e9 near entries, 45 GB on device."""
+    b = _bench()
+    c = dict(b.CONFIGS["c4"], n=1 << 17, l_max=4)
+    pts = b.make_points(ph, c, 0)
+    pm = ph.offline_h2(pts, b.make_cfg(ph, c))
+    R = pr.RefMatrix.from_product(pm, pts, near="none", finalize=False)
+    info = pm.info()
+    rng = np.random.default_rng(8)
+    near_ids = np.sort(rng.choice(info["n_near"], 150, replace=False))
+    cls = np.sort(rng.choice(info["n_classes"], 200, replace=False))
+    X = np.stack([ph.generate_normal(c["n"], 100 + j) for j in range(64)], axis=1)
+    rows = np.sort(rng.choice(c["n"], 6, replace=False))
+    for theta in ([0.083, 1.37], [0.41, 0.62]):
+        inst = ph.instantiate(pm, theta)
+        _check_blocks(ph, pm, inst, R, theta, near_ids, cls)
+        Y = inst.apply(X)
+        Yf = inst.instantiate_apply(theta, X)
+        cols = [0, 21, 42, 63]
+        yr = R.apply_rows(theta, X[:, cols], rows, threads=THREADS)
+        for q, j in enumerate(cols):
+            assert rel(Y[rows, j], yr[:, q]) <= TOL_Y
+            assert rel(Yf[rows, j], yr[:, q]) <= TOL_Y
