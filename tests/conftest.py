@@ -47,3 +47,26 @@ def pr():
 
     pyref.lib()
     return pyref
+
+
+PARITY = {}
+
+
+@pytest.fixture(scope="session")
+def parity_log():
+    """Records worst relative errors per test (dumped to $PHM_PARITY_REPORT)."""
+
+    def log(test, key, value):
+        rec = PARITY.setdefault(test, {})
+        rec[key] = max(float(value), rec.get(key, 0.0))
+
+    return log
+
+
+def pytest_sessionfinish(session, exitstatus):
+    path = os.environ.get("PHM_PARITY_REPORT")
+    if path and PARITY:
+        import json
+
+        with open(path, "w") as f:
+            json.dump(PARITY, f, indent=1, sort_keys=True)

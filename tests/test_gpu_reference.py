@@ -28,6 +28,8 @@ import sys
 import numpy as np
 import pytest
 
+from helpers import node_rows
+
 pytestmark = pytest.mark.gpu
 
 TOL_BLOCK = 1e-12
@@ -60,7 +62,7 @@ def _first_far_of_class(pm):
     return first
 
 
-def _check_blocks(ph, pm, inst, R, theta, near_ids, class_ids, ri=None):
+def _check_blocks(ph, pm, inst, R, theta, near_ids, class_ids, ri=None, log=None):
     sizes = _sizes(pm)
     near, _, _ = pm.blocks()
     first = _first_far_of_class(pm)
@@ -79,10 +81,16 @@ def _check_blocks(ph, pm, inst, R, theta, near_ids, class_ids, ri=None):
             wc = max(wc, rel(inst.class_c(int(k)), R.class_c(int(k), theta, info["P"])))
     assert wh <= TOL_BLOCK, f"H_k rel err {wh:.3e}"
     assert wc <= TOL_BLOCK, f"C_k rel err {wc:.3e}"
+    if log:
+        log("D_b", wd)
+        log("H_k", wh)
+        if pm.format == ph.Format.H2:
+            log("C_k", wc)
     return wd, wh, wc
 
 
-def test_c1_full_size_vs_reference(ph, pr):
+def test_c1_full_size_vs_reference(ph, pr, parity_log):
+    log = lambda k, v: parity_log("c1_full_size", k, v)  # noqa: E731
     b = _bench()
     c = b.CONFIGS["c1"]
     pts = b.make_points(ph, c, 0)
@@ -90,23 +98,32 @@ def test_c1_full_size_vs_reference(ph, pr):
     pm = ph.offline_h(pts, b.make_cfg(ph, c))
     R = pr.RefMatrix.from_product(pm, pts, near="snapshot", threads=THREADS)
     near, far, key = pm.blocks()
-    # S_b, T_b: the reference's own pttk_offline
+    # S_b, T_b: the reference's own pttk_offline (rows in the reference's
+    # ascending index order)
+    rows = node_rows(pm)
     for i in range(len(far)):
         S, T = pm.far_st(i)
         Sr, Tr = R.far_st(i)
+        S, T = S[np.argsort(rows(far[i, 0]))], T[np.argsort(rows(far[i, 1]))]
         assert rel(S, Sr) <= TOL_BLOCK and rel(T, Tr) <= TOL_BLOCK
+        log("S_b_T_b", max(rel(S, Sr), rel(T, Tr)))
     x = ph.generate_normal(c["n"], 1)
     for j in range(16):
         theta = [0.1 + 0.9 * j / 15]
         inst, ri = ph.instantiate(pm, theta), R.instantiate(theta)
-        _check_blocks(ph, pm, inst, R, theta, range(len(near)), range(pm.info()["n_classes"]), ri=ri)
+        _check_blocks(ph, pm, inst, R, theta, range(len(near)), range(pm.info()["n_classes"]), ri=ri, log=log)
         wf = max(rel(inst.far_h(i), ri.far_h(i)) for i in range(len(far)))
         assert wf <= TOL_BLOCK
-        assert rel(inst.apply(x), ri.apply(x)) <= TOL_Y
-        assert rel(inst.instantiate_apply(theta, x), ri.apply(x)) <= TOL_Y
+        log("far_h", wf)
+        y = ri.apply(x)
+        e1, e2 = rel(inst.apply(x), y), rel(inst.instantiate_apply(theta, x), y)
+        assert e1 <= TOL_Y and e2 <= TOL_Y
+        log("y_apply", e1)
+        log("y_fused", e2)
 
 
-def test_c2_full_size_vs_reference(ph, pr):
+def test_c2_full_size_vs_reference(ph, pr, parity_log):
+    log = lambda k, v: parity_log("c2_full_size", k, v)  # noqa: E731
     b = _bench()
     c = b.CONFIGS["c2"]
     pts = b.make_points(ph, c, 0)
@@ -117,10 +134,12 @@ def test_c2_full_size_vs_reference(ph, pr):
     for theta in b.theta_vectors(c, 3, 0):
         theta = list(theta)
         inst, ri = ph.instantiate(pm, theta), R.instantiate(theta)
-        _check_blocks(ph, pm, inst, R, theta, range(len(near)), range(pm.info()["n_classes"]), ri=ri)
+        _check_blocks(ph, pm, inst, R, theta, range(len(near)), range(pm.info()["n_classes"]), ri=ri, log=log)
         y = ri.apply(x)
-        assert rel(inst.apply(x), y) <= TOL_Y
-        assert rel(inst.instantiate_apply(theta, x), y) <= TOL_Y
+        e1, e2 = rel(inst.apply(x), y), rel(inst.instantiate_apply(theta, x), y)
+        assert e1 <= TOL_Y and e2 <= TOL_Y
+        log("y_apply", e1)
+        log("y_fused", e2)
 
 
 @pytest.fixture(scope="module")
@@ -133,7 +152,8 @@ def c3(ph, pr):
     return pm, R, c, pts
 
 
-def test_c3_full_size_blocks_vs_reference(ph, c3):
+def test_c3_full_size_blocks_vs_reference(ph, c3, parity_log):
+    log = lambda k, v: parity_log("c3_full_size_sampled", k, v)  # noqa: E731
     pm, R, c, pts = c3
     b = _bench()
     info = pm.info()
@@ -143,14 +163,15 @@ def test_c3_full_size_blocks_vs_reference(ph, c3):
     for theta in b.theta_vectors(c, 2, 0):
         theta = list(theta)
         inst = ph.instantiate(pm, theta)
-        _check_blocks(ph, pm, inst, R, theta, near_ids, cls)
+        _check_blocks(ph, pm, inst, R, theta, near_ids, cls, log=log)
         # every class's H_k
         first = _first_far_of_class(pm)
         wh = max(rel(inst.far_h(int(first[k])), R.class_h(k, theta)) for k in range(info["n_classes"]))
         assert wh <= TOL_BLOCK
 
 
-def test_c3_full_size_y_rows_vs_reference(ph, c3):
+def test_c3_full_size_y_rows_vs_reference(ph, c3, parity_log):
+    log = lambda k, v: parity_log("c3_full_size_sampled", k, v)  # noqa: E731
     pm, R, c, pts = c3
     b = _bench()
     x = ph.generate_normal(c["n"], 1)
@@ -160,11 +181,14 @@ def test_c3_full_size_y_rows_vs_reference(ph, c3):
         theta = list(theta)
         yr = R.apply_rows(theta, x, rows, threads=THREADS)
         inst.reinstantiate(theta)
-        assert rel(inst.apply(x)[rows], yr) <= TOL_Y
-        assert rel(inst.instantiate_apply(theta, x)[rows], yr) <= TOL_Y
+        e1, e2 = rel(inst.apply(x)[rows], yr), rel(inst.instantiate_apply(theta, x)[rows], yr)
+        assert e1 <= TOL_Y and e2 <= TOL_Y
+        log("y_rows_apply", e1)
+        log("y_rows_fused", e2)
 
 
-def test_c4_form_largest_single_gpu_vs_reference(ph, pr):
+def test_c4_form_largest_single_gpu_vs_reference(ph, pr, parity_log):
+    log = lambda k, v: parity_log("c4_form_n2^17_64rhs", k, v)  # noqa: E731
     """BASELINE configs[3] form with its leaf size (32) at n = 2^17 (l_max 4):
     mixture of 16 Gaussians, Matern-5/2 x sigma^2 on an 8 x 6 grid, 64 RHS
     through the block (DMMA) path. 1.26e9 near entries, 45 GB on device."""
@@ -181,11 +205,13 @@ def test_c4_form_largest_single_gpu_vs_reference(ph, pr):
     rows = np.sort(rng.choice(c["n"], 6, replace=False))
     for theta in ([0.083, 1.37], [0.41, 0.62]):
         inst = ph.instantiate(pm, theta)
-        _check_blocks(ph, pm, inst, R, theta, near_ids, cls)
+        _check_blocks(ph, pm, inst, R, theta, near_ids, cls, log=log)
         Y = inst.apply(X)
         Yf = inst.instantiate_apply(theta, X)
         cols = [0, 21, 42, 63]
         yr = R.apply_rows(theta, X[:, cols], rows, threads=THREADS)
         for q, j in enumerate(cols):
-            assert rel(Y[rows, j], yr[:, q]) <= TOL_Y
-            assert rel(Yf[rows, j], yr[:, q]) <= TOL_Y
+            e1, e2 = rel(Y[rows, j], yr[:, q]), rel(Yf[rows, j], yr[:, q])
+            assert e1 <= TOL_Y and e2 <= TOL_Y
+            log("Y_rows_apply", e1)
+            log("Y_rows_fused", e2)

@@ -16,6 +16,7 @@ import subprocess
 
 import numpy as np
 import pytest
+from helpers import node_rows
 
 from oracle import pyref as pr
 
@@ -202,16 +203,27 @@ def test_reference_apply_rows_equals_full_apply(ph):
 
 
 def test_h_form_far_factors_vs_reference_pttk_offline(ph):
-    """S_b, T_b of the product's host build = the reference's pttk_offline."""
-    c = ONLINE_CASES["h_gauss_2d_tt"]
-    pts, cfg, fmt = _product_case(ph, c)
-    pm = ph.offline_structure(pts, cfg, fmt)
-    R = pr.RefMatrix.from_product(pm, pts, near="tt")
-    nfar = pm.info()["n_far"]
-    for i in range(0, nfar, max(1, nfar // 100)):
+    """S_b, T_b of the product's host build = the reference's pttk_offline,
+    at BASELINE config 1's structure (far blocks at internal levels too; the
+    product's rows are in tree order, the reference's ascending)."""
+    pts = ph.generate_points(4096, 2, 0)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.GAUSS, [(0.1, 1.0)]), l_max=3, p_s=6, p_theta=8, eta=1.0,
+                      seed=0, near_mode=ph.NearMode.SNAPSHOT)
+    pm = ph.offline_structure(pts, cfg, ph.Format.H)
+    R = pr.RefMatrix.from_product(pm, pts, near="none", finalize=False)
+    R.make_near_snapshots()
+    R.finalize()
+    _, far, _ = pm.blocks()
+    rows = node_rows(pm)
+    ints, _ = pm.nodes()
+    levels = set()
+    for i in range(0, len(far), 7):
         S, T = pm.far_st(i)
         Sr, Tr = R.far_st(i)
+        S, T = S[np.argsort(rows(far[i, 0]))], T[np.argsort(rows(far[i, 1]))]
         assert rel(S, Sr) <= 1e-13 and rel(T, Tr) <= 1e-13
+        levels.add(int(ints[far[i, 0], 0]))
+    assert len(levels) >= 2
 
 
 def test_reference_domain_error_and_grid(ph):
