@@ -219,14 +219,26 @@ class Clocks:
 
 
 def measured_traffic(kernel, config, world):
-    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
-    --set full capture (profiles/r01_traffic.json, taken on c3 at N=1); None
-    for any other workload."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
-    if config != "c3" or world != 1 or not os.path.exists(path):
+    """DRAM bytes (read + write) per launch of `kernel` and where they come
+    from: the committed ncu --set full capture of this bench's c3 step at
+    N=1 (dram__bytes_read.sum + dram__bytes_write.sum; the newest
+    profiles/r*_traffic.json). ncu cannot run inside the timed bench, so this
+    is the captured number, not a live one; None for other workloads."""
+    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+    files = sorted(f for f in os.listdir(prof) if f.endswith("_traffic.json")) if os.path.isdir(prof) else []
+    if config != "c3" or world != 1 or not files:
+        return None, None
+    rec = json.load(open(os.path.join(prof, files[-1]))).get(kernel)
+    return (rec["traffic_bytes_per_launch"], f"ncu --set full capture, profiles/{files[-1]}") if rec else (None, None)
+
+
+def dmma_peak_tflops():
+    """Measured fp64 tensor-core (mma.sync f64) peak of this part."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "dmma_peak.json")) as f:
+            return float(json.load(f)["dmma_f64_tflops"])
+    except Exception:
         return None
-    rec = json.load(open(path)).get(kernel)
-    return rec["traffic_bytes_per_launch"] if rec else None
 
 
 def measured_peak():
@@ -331,9 +343,12 @@ def run_ours(args):
     y_dev = torch.empty((m, n), dtype=torch.float64, device="cuda")
     rows = info["row_end"] - info["row_begin"]
     if row_shard:
-        from paper_2511_03109_b200.dist import PartialSum
+        # the library's own communicator: the sharded step runs its x-hat and
+        # y all-reduces inside phm_instantiate_apply_sharded (NCCL over
+        # NVLink; gloo on host copies for the one-GPU functional check)
+        from paper_2511_03109_b200.dist import host_allreduce_comm, nccl_comm
 
-        psum = PartialSum(n, m, device="cuda")
+        comm = host_allreduce_comm() if same_gpu else nccl_comm(ctx)
     inst = ph.instantiate(pm, thetas[0])
     # sweeps: tb thetas per step, instantiated by one snapshot pass (K1 batch)
     tb = (args.theta_batch or c.get("theta_batch", 1)) if sweep else 1
@@ -352,11 +367,10 @@ def run_ours(args):
             # instantiate(theta_s) + MVM as one overlapped schedule
             inst.instantiate_apply_device(theta_of(s), x_dev.data_ptr(), y_dev.data_ptr(), m)
         else:
-            # this rank's partial y (its owner leaves' near pairs, both ways,
-            # and its rows' far field), summed over ranks by one all-reduce
-            inst.instantiate_apply_partial_device(theta_of(s), x_dev.data_ptr(), psum.buf.data_ptr(), m)
-            psum.reduce()
-            ph.lib().phm_unpermute_device(pm._h, ph._P(psum.buf.data_ptr()), ph._P(y_dev.data_ptr()), m)
+            # this rank's shard of the step (its owner leaves' near pairs,
+            # both ways; its rows' far field; its share of the forward pass)
+            # with both exchanges, one library call
+            inst.instantiate_apply_sharded_device(comm, theta_of(s), x_dev.data_ptr(), y_dev.data_ptr(), m)
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -365,8 +379,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        ctx.enable_timing(os.environ.get("PHM_BENCH_LOOP_TIMERS", "1") != "0")
-        ctx.reset_timers()
+        # `value`: per-kernel timers off, so the step replays as one CUDA graph
+        ctx.enable_timing(False)
         launches0 = ctx.launches
         torch.cuda.synchronize()
         tw0 = time.time()
@@ -378,8 +392,20 @@ def run_ours(args):
         tw1 = time.time()
         time.sleep(0.05)  # the sampler's last row of the window
         clk.mark(tw0, tw1)
-    launches = ctx.launches - launches0
-    ms = ev0.elapsed_time(ev1)
+        launches = ctx.launches - launches0
+        ms = ev0.elapsed_time(ev1)
+        # the same K steps again with a CUDA event pair around every kernel
+        # launch (direct launches): the per-kernel times the roofline uses
+        ctx.enable_timing(True)
+        ctx.reset_timers()
+        ek0, ek1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ek0.record(stream)
+        for s in range(args.steps):
+            step(args.warmup + s)
+        ek1.record(stream)
+        torch.cuda.synchronize()
+        ms_timed_loop = ek0.elapsed_time(ek1)
     # dominant kernel: the fused near-field pass (instantiate + GEMV) when the
     # step runs it, else the plain K1 instantiate stream
     k1_name, k1_desc = "near_inst_mvm", "k_near_tma (K1+K6 fused TMA pass: forms, stores and applies D)"
@@ -472,8 +498,7 @@ def run_ours(args):
                "h2d_bytes_per_step": tb * (8 * n * m + 8), "d2h_bytes_per_step": tb * 8 * n * m}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and c["fmt"] == "h2":
-        host_pm = ph.offline_structure(pts, make_cfg(ph, c))
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = reference_cpu(c, 3, 1, args.cpu_sample, args.seed, m)
 
     if rank == 0:
@@ -487,7 +512,7 @@ def run_ours(args):
             cls_bytes += 8 * (mid.size + info["P"] * (rl + rr) + rl * rr + info["P"] ** 2)
         b_inst, b_mvm = algorithmic_bytes(info, c, cls_bytes)
         k1_avg = k1_ms / max(1, k1_n)
-        traffic = measured_traffic(k1_desc.split()[0], args.config, world)
+        traffic, traffic_src = measured_traffic(k1_desc.split()[0], args.config, world)
         k1_bytes = 8 * info["near_stream_elems"]  # R slab reads + 1 write per stored near entry
         if binsts is not None:  # batched K1: R slab reads + one write per theta of the batch
             k1_desc = "k_inst_flat_batch (K1 for %d thetas per snapshot pass)" % min(tb, 16)
@@ -506,14 +531,18 @@ def run_ours(args):
         # block right-hand sides, the near-field contraction
         cp = timers.get("coupling")
         k9 = timers.get("near_mrhs")
+        dmma_peak = dmma_peak_tflops()
+        cp_tf = (2.0 * info["n_far"] * info["P"] ** 2 * m / (cp["ms_per_launch"] * 1e-3) / 1e12) if cp else None
+        k9_tf = (2.0 * info["near_entries"] * m / (k9["ms_per_launch"] * 1e-3) / 1e12) if k9 else None
         dmma = {
             "note": ("useful fp64 flop over each kernel's event-timed duration inside the step, where it "
                      "time-shares the SMs with the near pass (the fused step's coupling is a capped grid "
-                     "resident beside it); DMMA pipe utilisation of the kernels alone: profiles/r01_*_full_summary.txt"),
-            "coupling_tflops_in_step": (2.0 * info["n_far"] * info["P"] ** 2 * m / (cp["ms_per_launch"] * 1e-3) / 1e12)
-            if cp else None,
-            "near_mrhs_tflops_in_step": (2.0 * info["near_entries"] * m / (k9["ms_per_launch"] * 1e-3) / 1e12)
-            if k9 else None,
+                     "resident beside it); DMMA pipe utilisation of the kernels alone: profiles/r0*_full_summary.txt"),
+            "peak_tflops": dmma_peak, "peak_source": "profiles/dmma_peak.json (tools/dmma_probe.cu)",
+            "coupling_tflops_in_step": cp_tf,
+            "coupling_frac_of_peak": cp_tf / dmma_peak if cp_tf and dmma_peak else None,
+            "near_mrhs_tflops_in_step": k9_tf,
+            "near_mrhs_frac_of_peak": k9_tf / dmma_peak if k9_tf and dmma_peak else None,
         }
         what, config = describe(args, c, m, tb, world)
         line = {
@@ -533,7 +562,11 @@ def run_ours(args):
             "config": config,
             "roofline": {"bound": "hbm", "kernel": k1_desc, "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_kind": peak_kind, "bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg},
+                         "traffic_source": traffic_src, "peak_kind": peak_kind, "bytes_per_launch": k1_bytes,
+                         "avg_launch_ms": k1_avg,
+                         "timing": "kernel launch times from CUDA events around each launch, over a second pass "
+                                   "of the same K steps (value's pass runs without them, as CUDA graphs)",
+                         "ms_per_step_event_pass": ms_timed_loop / args.steps},
             "phases": {"instantiate_ms": inst_ms, "apply_ms": apply_ms,
                        "instantiate_GB_s": b_inst / (inst_ms * 1e-3) / 1e9},
             "mvm": {"ms": mvm_ms, "algorithmic_bytes": b_mvm,

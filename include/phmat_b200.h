@@ -244,6 +244,35 @@ int phm_apply_partial_device(phm_instance inst, const double* x_dev, double* ypa
 int phm_instantiate_apply_partial_device(phm_instance inst, const double* theta, int n_theta, const double* x_dev,
                                          double* ypart_dev, int64_t m);
 int phm_unpermute_device(phm_matrix m, const double* yperm_dev, double* y_dev, int64_t mcols);
+
+/* Multi-GPU inside the library: one process per GPU, each
+ * holding the row shard cfg.shard_rank of cfg.shard_count. A communicator
+ * carries the two exchanges of the sharded step, both in-place sum
+ * all-reduces on the context stream: x-hat (nodes x P per RHS) between each
+ * rank's share of the forward pass and the coupling, and the tree-order
+ * partial y at the end. It replaces the caller-side loop of
+ * run_experiment (proj/src/harness.cpp:287-352) over one shared matrix.
+ *   NCCL: rank 0 calls phm_comm_unique_id and broadcasts the 128 bytes; every
+ *   rank calls phm_comm_create_nccl (libnccl.so.2 is loaded at run time).
+ *   Callback: fn(buf_dev, count, cuda_stream, user) must leave buf summed
+ *   over the ranks, ordered on cuda_stream (used to test the sharded step
+ *   with any transport, e.g. gloo). */
+typedef struct phm_comm_s* phm_comm;
+typedef int (*phm_allreduce_fn)(double* buf_dev, int64_t count, void* cuda_stream, void* user);
+int phm_comm_unique_id(uint8_t* id /* 128 bytes */);
+int phm_comm_create_nccl(phm_context ctx, const uint8_t* id /* 128 bytes */, int rank, int world, phm_comm* out);
+int phm_comm_create_callback(phm_allreduce_fn fn, void* user, int rank, int world, phm_comm* out);
+int phm_comm_destroy(phm_comm comm);
+int phm_comm_info(phm_comm comm, int* rank, int* world, int* is_nccl);
+/* reinstantiate(theta) + apply(x) on this rank's shard, exchanges included;
+ * y (original point order, n x m) is complete on every rank. Device buffers
+ * (asynchronous on the context stream; NCCL: one CUDA graph per step) or
+ * host buffers (synchronous, like phm_instantiate_apply). */
+int phm_instantiate_apply_sharded(phm_instance inst, phm_comm comm, const double* theta, int n_theta,
+                                  const double* x_dev, double* y_dev, int64_t m);
+int phm_instantiate_apply_sharded_host(phm_instance inst, phm_comm comm, const double* theta, int n_theta,
+                                       const double* x, int64_t n_rows, double* y, int64_t m);
+int phm_apply_sharded(phm_instance inst, phm_comm comm, const double* x_dev, double* y_dev, int64_t m);
 /* estimate_error of the reference harness (harness.cpp:183-236): probe rows
  * sampled without replacement and x ~ U[0,1) from the reference's Rng
  * stream, exact rows (K x)_J by direct kernel evaluation on the GPU (audit

@@ -159,6 +159,14 @@ SIGNATURES = {
     "phm_apply_partial_device": ([_P, _P, _P, C.c_int64], C.c_int),
     "phm_instantiate_apply_partial_device": ([_P, _DP, C.c_int, _P, _P, C.c_int64], C.c_int),
     "phm_unpermute_device": ([_P, _P, _P, C.c_int64], C.c_int),
+    "phm_comm_unique_id": ([C.c_char_p], C.c_int),
+    "phm_comm_create_nccl": ([_P, C.c_char_p, C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
+    "phm_comm_create_callback": ([_P, _P, C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
+    "phm_comm_destroy": ([_P], C.c_int),
+    "phm_comm_info": ([_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+    "phm_instantiate_apply_sharded": ([_P, _P, _DP, C.c_int, _P, _P, C.c_int64], C.c_int),
+    "phm_instantiate_apply_sharded_host": ([_P, _P, _DP, C.c_int, _DP, C.c_int64, _DP, C.c_int64], C.c_int),
+    "phm_apply_sharded": ([_P, _P, _P, _P, C.c_int64], C.c_int),
     "phm_to_dense": ([_P, _DP, C.c_int64], C.c_int),
     "phm_estimate_error": ([_P, C.c_int64, C.c_uint64, _DP, _I64P, _DP, _DP, _DP], C.c_int),
     "phm_generate_points": ([C.c_int64, C.c_int, C.c_uint64, _DP], C.c_int),
@@ -519,6 +527,26 @@ class InstantiatedMatrix:
     def apply_device(self, x_ptr: int, y_ptr: int, m: int = 1) -> None:
         _check(lib().phm_apply_device(self._h, _P(x_ptr), _P(y_ptr), m))
 
+    def instantiate_apply_sharded_device(self, comm: "Comm", theta, x_ptr: int, y_ptr: int, m: int = 1) -> None:
+        """This rank's shard of instantiate(theta) + apply, with the x-hat and
+        y all-reduces over `comm`; y (original order) complete on every rank."""
+        th = _f64(theta).ravel()
+        _check(lib().phm_instantiate_apply_sharded(self._h, comm._h, _dp(th), th.size, x_ptr, y_ptr, m))
+
+    def instantiate_apply_sharded(self, comm: "Comm", theta, x) -> np.ndarray:
+        """Host-buffer form of instantiate_apply_sharded_device (synchronous)."""
+        th = _f64(theta).ravel()
+        xa = _f64(x)
+        one = xa.ndim == 1
+        xf = np.asfortranarray(xa.reshape(xa.shape[0], -1))
+        y = np.empty_like(xf)
+        _check(lib().phm_instantiate_apply_sharded_host(self._h, comm._h, _dp(th), th.size, _dp(xf), xf.shape[0],
+                                                        _dp(y), xf.shape[1]))
+        return y[:, 0] if one else y
+
+    def apply_sharded_device(self, comm: "Comm", x_ptr: int, y_ptr: int, m: int = 1) -> None:
+        _check(lib().phm_apply_sharded(self._h, comm._h, x_ptr, y_ptr, m))
+
     def apply_rows_device(self, x_ptr: int, yrows_ptr: int, m: int = 1) -> None:
         _check(lib().phm_apply_rows_device(self._h, _P(x_ptr), _P(yrows_ptr), m))
 
@@ -572,6 +600,59 @@ class InstantiatedMatrix:
 
 
 # ---------------------------------------------------------------- functions
+# --------------------------------------------------------------- multi-GPU
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, _P, C.c_int64, _P, _P)
+
+
+class Comm:
+    """Communicator of the row-sharded step (phm_comm): NCCL, or a Python
+    callback ``fn(buf_ptr, count, stream_ptr) -> None`` that leaves the device
+    buffer summed over the ranks (tests: gloo on the host)."""
+
+    def __init__(self, handle, keep=None):
+        self._h = handle
+        self._keep = keep
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().phm_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, ctx: "Context", uid: bytes, rank: int, world: int) -> "Comm":
+        h = _P()
+        _check(lib().phm_comm_create_nccl(ctx._h, uid, rank, world, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def callback(cls, fn, rank: int, world: int) -> "Comm":
+        def tramp(buf, count, stream, user):
+            try:
+                fn(buf, count, stream)
+                return 0
+            except Exception:  # reported as a failed exchange
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        cfn = ALLREDUCE_FN(tramp)
+        h = _P()
+        _check(lib().phm_comm_create_callback(C.cast(cfn, _P), None, rank, world, C.byref(h)))
+        return cls(h, keep=cfn)
+
+    def info(self):
+        r, w, k = C.c_int(), C.c_int(), C.c_int()
+        _check(lib().phm_comm_info(self._h, C.byref(r), C.byref(w), C.byref(k)))
+        return {"rank": r.value, "world": w.value, "nccl": bool(k.value)}
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.phm_comm_destroy(self._h)
+            self._h = None
+
+
 def _points(points) -> np.ndarray:
     p = np.ascontiguousarray(points, dtype=np.float64)
     if p.ndim != 2:

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/phmat_b200.h"
+#include "comm.hpp"
 #include "engine.hpp"
 
 struct phm_context_s {
@@ -23,6 +24,9 @@ struct phm_matrix_s {
 struct phm_instance_s {
   std::shared_ptr<phm::DevMatrix> m;
   std::shared_ptr<phm::DevInstance> inst;
+};
+struct phm_comm_s {
+  std::shared_ptr<phm::Comm> c;
 };
 
 namespace {
@@ -732,6 +736,79 @@ int phm_instantiate_apply_device(phm_instance inst, const double* theta, int n_t
     need(y, "y");
     auto& H = const_cast<phm::HostMatrix&>(phm::matrix_host(*inst->m));
     phm::instantiate_apply_device(*inst->inst, theta, n_theta, x, y, m, &H.counters);
+  });
+}
+int phm_comm_unique_id(uint8_t* id) {
+  return guarded([&] {
+    need(id, "id");
+    phm::nccl_unique_id(id);
+  });
+}
+int phm_comm_create_nccl(phm_context ctx, const uint8_t* id, int rank, int world, phm_comm* out) {
+  return guarded([&] {
+    need(ctx, "context");
+    need(id, "id");
+    need(out, "out");
+    auto c = std::make_unique<phm_comm_s>();
+    c->c = phm::comm_nccl(phm::context_device(*ctx->ctx), id, rank, world);
+    *out = c.release();
+  });
+}
+int phm_comm_create_callback(phm_allreduce_fn fn, void* user, int rank, int world, phm_comm* out) {
+  return guarded([&] {
+    need(out, "out");
+    auto c = std::make_unique<phm_comm_s>();
+    c->c = phm::comm_callback(fn, user, rank, world);
+    *out = c.release();
+  });
+}
+int phm_comm_destroy(phm_comm c) {
+  return guarded([&] { delete c; });
+}
+int phm_comm_info(phm_comm c, int* rank, int* world, int* is_nccl) {
+  return guarded([&] {
+    need(c, "comm");
+    if (rank) *rank = c->c->rank;
+    if (world) *world = c->c->world;
+    if (is_nccl) *is_nccl = c->c->capturable() ? 1 : 0;
+  });
+}
+int phm_instantiate_apply_sharded(phm_instance inst, phm_comm comm, const double* theta, int n_theta,
+                                  const double* x, double* y, int64_t m) {
+  return guarded([&] {
+    need(inst, "instance");
+    need(comm, "comm");
+    need(theta, "theta");
+    need(x, "x");
+    need(y, "y");
+    auto& H = const_cast<phm::HostMatrix&>(phm::matrix_host(*inst->m));
+    (void)phm::parametric_vectors(H.grids, theta, n_theta);  // domain check before any launch
+    if (m < 1) throw std::invalid_argument("mvm: m must be >= 1");
+    phm::instantiate_apply_sharded(*inst->inst, *comm->c, theta, n_theta, x, y, m, &H.counters);
+  });
+}
+int phm_instantiate_apply_sharded_host(phm_instance inst, phm_comm comm, const double* theta, int n_theta,
+                                       const double* x, int64_t n_rows, double* y, int64_t m) {
+  return guarded([&] {
+    need(inst, "instance");
+    need(comm, "comm");
+    need(theta, "theta");
+    need(x, "x");
+    need(y, "y");
+    auto& H = const_cast<phm::HostMatrix&>(phm::matrix_host(*inst->m));
+    (void)phm::parametric_vectors(H.grids, theta, n_theta);
+    if (n_rows != H.n()) throw std::invalid_argument("mvm: length mismatch");
+    if (m < 1) throw std::invalid_argument("mvm: m must be >= 1");
+    phm::instantiate_apply_sharded_host(*inst->inst, *comm->c, theta, n_theta, x, y, m, &H.counters);
+  });
+}
+int phm_apply_sharded(phm_instance inst, phm_comm comm, const double* x, double* y, int64_t m) {
+  return guarded([&] {
+    need(inst, "instance");
+    need(comm, "comm");
+    need(x, "x");
+    need(y, "y");
+    phm::apply_sharded(*inst->inst, *comm->c, x, y, m);
   });
 }
 int phm_estimate_error(phm_instance inst, int64_t probe_rows, uint64_t seed, double* err, int64_t* rows_out,

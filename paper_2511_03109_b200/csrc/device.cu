@@ -17,6 +17,7 @@
 #include <tuple>
 #include <vector>
 
+#include "comm.hpp"
 #include "engine.hpp"
 #include "kernels.cuh"
 
@@ -333,6 +334,7 @@ void context_reset_timers(Context& ctx) {
   ctx.totals.clear();
 }
 std::int64_t context_launches(Context& ctx) { return ctx.launches; }
+int context_device(const Context& ctx) { return ctx.device; }
 
 // ----------------------------------------------------------------- matrix
 struct DevMatrix {
@@ -377,6 +379,10 @@ struct DevMatrix {
   int n_k9_items = 0;
   // far field
   int ncls = 0;
+  // classes the class stage instantiates: all of them, or on a row shard
+  // only those some local far block uses (the rest are never read)
+  DBuf cmeta_run;
+  int ncls_run = 0;
   std::vector<dev::ClassMeta> cmeta_h;
   DBuf cmeta, class_mid, class_mid_dims, class_L, class_R;
   bool baseline = false;  // fixed far field (H-ACA / H^2-HCA at one theta)
@@ -400,6 +406,10 @@ struct DevMatrix {
   int n_leaves_all = 0, n_leaves_local = 0;
   std::vector<std::pair<int, int>> up_range, down_range;  // per level into level_nodes arrays
   DBuf up_nodes, down_nodes;
+  // sharded forward pass with an x-hat exchange: upward lists restricted to
+  // nodes that hold local rows (their x-hat is this rank's partial sum)
+  std::vector<std::pair<int, int>> upl_range;
+  DBuf upl_nodes;
   // apply workspace
   DBuf xp, yp, xhat, yhat, xdev, ydev;
   Index ws_m = 0;
@@ -1022,6 +1032,21 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     M.H_len = hoff;
     M.C_len = M.h2 ? static_cast<std::int64_t>(M.ncls) * M.P * M.P : 0;
     upload(M.cmeta, M.cmeta_h, st);
+    {
+      const char* e = std::getenv("PHM_CLASS_SUBSET");
+      const bool subset = H.cfg.shard_count > 1 && !(e && std::atoi(e) == 0);
+      std::vector<char> need(M.ncls, subset ? 0 : 1);
+      for (Index i = 0; i < static_cast<Index>(H.blocks.far.size()); ++i)
+        if (H.far_local[i]) need[H.far_key[i]] = 1;
+      std::vector<dev::ClassMeta> run;
+      for (int k = 0; k < M.ncls; ++k)
+        if (need[k]) run.push_back(M.cmeta_h[k]);
+      M.ncls_run = static_cast<int>(run.size());
+      if (M.ncls_run == M.ncls)
+        M.ncls_run = -1;  // all classes: use cmeta itself
+      else if (M.ncls_run > 0)
+        upload(M.cmeta_run, run, st);
+    }
     upload(M.class_mid, mid, st);
     upload(M.class_mid_dims, mdims, st);
     upload(M.class_L, L, st);
@@ -1179,23 +1204,28 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     upload(M.leaves_local, lloc, st);
     // level lists: upward = internal non-empty nodes per level (all);
     // downward = non-empty local non-root nodes per level
-    std::vector<std::int32_t> upn, dnn;
+    std::vector<std::int32_t> upn, dnn, upl;
     M.up_range.assign(T.l_max + 1, {0, 0});
     M.down_range.assign(T.l_max + 1, {0, 0});
+    M.upl_range.assign(T.l_max + 1, {0, 0});
     for (int l = 0; l <= T.l_max; ++l) {
       M.up_range[l].first = static_cast<int>(upn.size());
       M.down_range[l].first = static_cast<int>(dnn.size());
+      M.upl_range[l].first = static_cast<int>(upl.size());
       for (int id = 0; id < M.nnodes; ++id) {
         const TreeNode& nd = T.nodes[id];
         if (nd.level != l || nd.count == 0) continue;
         if (!nd.leaf()) upn.push_back(id);
+        if (!nd.leaf() && H.node_local[id]) upl.push_back(id);
         if (nd.parent >= 0 && H.node_local[id]) dnn.push_back(id);
       }
       M.up_range[l].second = static_cast<int>(upn.size());
       M.down_range[l].second = static_cast<int>(dnn.size());
+      M.upl_range[l].second = static_cast<int>(upl.size());
     }
     upload(M.up_nodes, upn, st);
     upload(M.down_nodes, dnn, st);
+    upload(M.upl_nodes, upl, st);
   } else {
     // H form: far blocks grouped per level, CSR by sigma, S/T payloads
     std::vector<dev::FarHItem> items;
@@ -1285,8 +1315,11 @@ void put_theta(DevMatrix& M, const std::vector<std::vector<double>>& v, const de
 
 void inst_classes(DevInstance& I, cudaStream_t s) {
   DevMatrix& M = *I.M;
+  const bool all = M.ncls_run < 0 || M.baseline;
+  if (!all && M.ncls_run == 0) return;  // a shard without far blocks
   M.ctx->run_on(s, "class_inst", [&] {
-    dev::launch_class_inst(s, M.cmeta.as<dev::ClassMeta>(), M.ncls, M.class_mid.as<double>(),
+    dev::launch_class_inst(s, all ? M.cmeta.as<dev::ClassMeta>() : M.cmeta_run.as<dev::ClassMeta>(),
+                           all ? M.ncls : M.ncls_run, M.class_mid.as<double>(),
                            M.class_mid_dims.as<std::int32_t>(), M.class_L.as<double>(), M.class_R.as<double>(),
                            M.theta_dev.as<dev::ThetaParams>(), M.P, M.h2, M.capA, M.capB, M.capT, M.capL,
                            I.H.as<double>(), I.C.as<double>());
@@ -1567,26 +1600,41 @@ namespace {
 
 // H^2 far-field chain on stream fs: forward (K3, K4), coupling (K5),
 // downward (K7 internal). Reads xp and C_k; writes yhat.
-void far_chain(DevInstance& I, Index m, cudaStream_t fs, int coupling_ctas) {
+void far_chain(DevInstance& I, Index m, cudaStream_t fs, int coupling_ctas, Comm* ex = nullptr) {
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   Context& ctx = *M.ctx;
   const int P = M.P;
   const int mm = static_cast<int>(m);
+  // On a row shard with an exchange, the forward pass covers only the local
+  // leaves and the nodes above them (x-hat of a node spanning ranks is this
+  // rank's partial sum; every other entry is zero), and one all-reduce of
+  // x-hat completes it: the transfer pass is linear, so the ranks' partial
+  // sums add up to the unsharded x-hat (to rounding). Replaces the forward
+  // pass every rank otherwise repeats in full.
+  static const bool split_env = [] {
+    const char* e = std::getenv("PHM_SPLIT_FORWARD");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool split = ex != nullptr && M.sharded && split_env;
+  if (split)
+    ctx.run_on(fs, "zero", [&] { dev::launch_zero(fs, M.xhat.as<double>(), static_cast<std::int64_t>(M.nnodes) * P * m); });
   ctx.run_on(fs, "leaf_fwd", [&] {
-    dev::launch_leaf_fwd(fs, M.leaves_all.as<std::int32_t>(), M.n_leaves_all, M.node_begin.as<std::int64_t>(),
+    dev::launch_leaf_fwd(fs, (split ? M.leaves_local : M.leaves_all).as<std::int32_t>(),
+                         split ? M.n_leaves_local : M.n_leaves_all, M.node_begin.as<std::int64_t>(),
                          M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, P, M.xp.as<double>(), mm,
                          M.xhat.as<double>());
   });
   for (int l = H.tree->l_max - 1; l >= 0; --l) {
-    const auto r = M.up_range[l];
+    const auto r = split ? M.upl_range[l] : M.up_range[l];
     if (r.second == r.first) continue;
     ctx.run_on(fs, "up", [&] {
-      dev::launch_up(fs, M.up_nodes.as<std::int32_t>() + r.first, r.second - r.first,
+      dev::launch_up(fs, (split ? M.upl_nodes : M.up_nodes).as<std::int32_t>() + r.first, r.second - r.first,
                      M.node_first_child.as<std::int32_t>(), M.node_count.as<std::int32_t>(), M.Etr.as<double>(), M.d,
                      M.ps, P, mm, M.xhat.as<double>());
     });
   }
+  if (split) ex->allreduce(M.xhat.as<double>(), static_cast<std::int64_t>(M.nnodes) * P * m, fs);
   // a kernel, not a memset: a memset node of a graph carries no priority and
   // would wait behind the near pass's CTAs
   ctx.run_on(fs, "zero", [&] { dev::launch_zero(fs, M.yhat.as<double>(), static_cast<std::int64_t>(M.nnodes) * P * m); });
@@ -1742,7 +1790,7 @@ void far_finish(DevInstance& I, Index m, cudaStream_t st) {
 // Computes this shard's rows of y in tree order into M.yp (n x m layout;
 // only rows [row_begin, row_end) are defined) from xp (tree order). The H^2
 // far chain runs on the side stream, concurrent with the near GEMV.
-void apply_tree_order(DevInstance& I, Index m) {
+void apply_tree_order(DevInstance& I, Index m, Comm* ex = nullptr) {
   DevMatrix& M = *I.M;
   Context& ctx = *M.ctx;
   static const int overlap = [] {
@@ -1750,20 +1798,20 @@ void apply_tree_order(DevInstance& I, Index m) {
     return e ? std::atoi(e) : 1;
   }();
   if (M.h2 && overlap == 0) {  // serial: far chain, then the near GEMV
-    far_chain(I, m, ctx.stream, 0);
+    far_chain(I, m, ctx.stream, 0, ex);
     near_product(I, m, ctx.stream);
     far_finish(I, m, ctx.stream);
     return;
   }
   if (M.h2 && overlap == 2) {  // serial: near GEMV first
     near_product(I, m, ctx.stream);
-    far_chain(I, m, ctx.stream, 0);
+    far_chain(I, m, ctx.stream, 0, ex);
     far_finish(I, m, ctx.stream);
     return;
   }
   if (M.h2) {
     ctx.fork();
-    far_chain(I, m, ctx.side, 0);
+    far_chain(I, m, ctx.side, 0, ex);
   }
   near_product(I, m, ctx.stream);
   if (M.h2) ctx.join();
@@ -1881,7 +1929,8 @@ void apply_host(DevInstance& I, const double* x, double* y, Index m) {
 // the side stream, the near stage (fused with the GEMV for one vector in
 // snapshot mode) on the main stream. It depends on theta only through
 // M.theta_dev, so it is graph-captured per (instance, x, m).
-void instantiate_apply_sequence(DevInstance& I, const double* x_dev, Index m, StageCounters* counters) {
+void instantiate_apply_sequence(DevInstance& I, const double* x_dev, Index m, StageCounters* counters,
+                                Comm* ex = nullptr) {
   DevMatrix& M = *I.M;
   Context& ctx = *M.ctx;
   cudaStream_t st = ctx.stream, fs = ctx.side;
@@ -1916,7 +1965,7 @@ void instantiate_apply_sequence(DevInstance& I, const double* x_dev, Index m, St
     const int per_sm = resident_env > 0 ? resident_env : std::min(fit, 1);
     coupling_ctas = per_sm * ctx.sms;
   }
-  far_chain(I, m, fs, coupling_ctas);
+  far_chain(I, m, fs, coupling_ctas, ex);
   bool fused = false;
   // Snapshot mode, one vector: K1 and K6 fused into one TMA pass over the
   // snapshots (k_near_tma) -- 10.8 ms at C3 against 9.8 + 1.6 ms for the
@@ -1958,7 +2007,7 @@ namespace {
 // graph). H form and direct mode run instantiate and apply one after the
 // other. y equals reinstantiate() + apply_device() to rounding (D bitwise).
 void instantiate_apply_tree(DevInstance& I, const double* theta, int n_theta, const double* x_dev, Index m,
-                            StageCounters* counters) {
+                            StageCounters* counters, Comm* ex = nullptr) {
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   PHM_CHECK(m >= 1, "apply: m must be >= 1");
@@ -1971,13 +2020,18 @@ void instantiate_apply_tree(DevInstance& I, const double* theta, int n_theta, co
     run_instantiate(I, theta, n_theta, counters);
     cudaStream_t st = M.st();
     M.ctx->run("gather", [&] { dev::launch_gather(st, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
-    apply_tree_order(I, m);
+    apply_tree_order(I, m, ex);
     return;
   }
   I.theta.assign(theta, theta + n_theta);
   Context& ctx = *M.ctx;
   put_theta(M, v, tv, ctx.stream);  // the only theta-dependent launch
-  run_graphed(I, 1, x_dev, m, [&] { instantiate_apply_sequence(I, x_dev, m, counters); });
+  if (ex == nullptr)
+    run_graphed(I, 1, x_dev, m, [&] { instantiate_apply_sequence(I, x_dev, m, counters); });
+  else if (ex->capturable())
+    run_graphed(I, 2, x_dev, m, [&] { instantiate_apply_sequence(I, x_dev, m, counters, ex); });
+  else
+    instantiate_apply_sequence(I, x_dev, m, counters, ex);
 }
 }  // namespace
 
@@ -1993,6 +2047,60 @@ void instantiate_apply_device(DevInstance& I, const double* theta, int n_theta, 
     dev::launch_scatter(M.st(), M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev);
   });
   M.ctx->print_stamps();
+}
+
+// The sharded HPO step as one library call: this rank's
+// instantiate + partial apply (its near blocks -- with symmetric storage also
+// the transposed products that land on other ranks' rows -- its far blocks,
+// its share of the forward pass), the x-hat all-reduce between the forward
+// pass and the coupling, the y all-reduce of the tree-order partials on the
+// context stream, and the un-permute into y (original point order, every
+// rank). With an NCCL comm the whole sequence is captured as one CUDA graph.
+void instantiate_apply_sharded(DevInstance& I, Comm& ex, const double* theta, int n_theta, const double* x_dev,
+                               double* y_dev, Index m, StageCounters* counters) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
+  NvtxRange nvtx("phm::instantiate_apply_sharded");
+  DevMatrix& M = *I.M;
+  PHM_CHECK(ex.world == M.hm->cfg.shard_count && ex.rank == M.hm->cfg.shard_rank,
+            "sharded step: communicator rank / world differ from the matrix's shard");
+  instantiate_apply_tree(I, theta, n_theta, x_dev, m, counters, &ex);
+  // world 1 still runs the (local) all-reduce: the same path as at N > 1
+  ex.allreduce(M.yp.as<double>(), M.n * m, M.st());
+  M.ctx->run("scatter", [&] {
+    dev::launch_scatter(M.st(), M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev);
+  });
+}
+
+void instantiate_apply_sharded_host(DevInstance& I, Comm& ex, const double* theta, int n_theta, const double* x,
+                                    double* y, Index m, StageCounters* counters) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
+  DevMatrix& M = *I.M;
+  CK(cudaSetDevice(M.ctx->device));
+  ensure_workspace(M, m);
+  cudaStream_t st = M.st();
+  CK(cudaMemcpyAsync(M.xdev.p, x, sizeof(double) * M.n * m, cudaMemcpyHostToDevice, st));
+  instantiate_apply_sharded(I, ex, theta, n_theta, M.xdev.as<double>(), M.ydev.as<double>(), m, counters);
+  CK(cudaMemcpyAsync(y, M.ydev.p, sizeof(double) * M.n * m, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+void apply_sharded(DevInstance& I, Comm& ex, const double* x_dev, double* y_dev, Index m) {
+  std::lock_guard<std::recursive_mutex> exec_lock(I.M->exec_mu());
+  NvtxRange nvtx("phm::apply_sharded");
+  DevMatrix& M = *I.M;
+  PHM_CHECK(ex.world == M.hm->cfg.shard_count && ex.rank == M.hm->cfg.shard_rank,
+            "sharded apply: communicator rank / world differ from the matrix's shard");
+  PHM_CHECK(m >= 1, "apply: m must be >= 1");
+  CK(cudaSetDevice(M.ctx->device));
+  ensure_workspace(M, m);
+  cudaStream_t st = M.st();
+  M.ctx->run("gather", [&] { dev::launch_gather(st, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
+  if (ex.capturable())
+    run_graphed(I, 3, nullptr, m, [&] { apply_tree_order(I, m, &ex); });
+  else
+    apply_tree_order(I, m, &ex);
+  ex.allreduce(M.yp.as<double>(), M.n * m, st);
+  M.ctx->run("scatter", [&] { dev::launch_scatter(st, M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev); });
 }
 
 void instantiate_apply_partial_device(DevInstance& I, const double* theta, int n_theta, const double* x_dev,

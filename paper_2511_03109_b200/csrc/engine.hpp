@@ -14,6 +14,7 @@ namespace phm {
 struct Context;     // device, stream, timers
 struct DevMatrix;   // parametric matrix resident on the GPU
 struct DevInstance; // matrix instantiated at one theta
+class Comm;         // rank-to-rank all-reduce (comm.hpp)
 
 std::shared_ptr<Context> context_create(int device);
 void context_set_stream(Context& ctx, void* stream);  // nullptr = own stream
@@ -25,6 +26,7 @@ void context_enable_timing(Context& ctx, bool on);
 void context_timer(Context& ctx, const std::string& name, double* ms, std::int64_t* count);
 void context_reset_timers(Context& ctx);
 std::int64_t context_launches(Context& ctx);  // kernels launched so far
+int context_device(const Context& ctx);
 
 // Offline build: host structure + TT-cross (host), upload, and for
 // NearMode::Snapshot the GPU snapshot generator (K11).
@@ -102,5 +104,14 @@ void apply_device_partial(DevInstance& inst, const double* x_dev, double* ypart_
 void instantiate_apply_partial_device(DevInstance& inst, const double* theta, int n_theta, const double* x_dev,
                                       double* ypart_dev, Index m, StageCounters* counters);
 void unpermute_device(DevMatrix& m, const double* yperm_dev, double* y_dev, Index mcols);
+// The row-sharded step as one call per rank: this rank's
+// partial instantiate + apply, the x-hat and y all-reduces over `comm`
+// (NCCL, or a callback), and the un-permute; y (original point order) is
+// complete on every rank. The matrix must be shard comm.rank of comm.world.
+void instantiate_apply_sharded(DevInstance& inst, Comm& comm, const double* theta, int n_theta, const double* x_dev,
+                               double* y_dev, Index m, StageCounters* counters);
+void instantiate_apply_sharded_host(DevInstance& inst, Comm& comm, const double* theta, int n_theta, const double* x,
+                                    double* y, Index m, StageCounters* counters);
+void apply_sharded(DevInstance& inst, Comm& comm, const double* x_dev, double* y_dev, Index m);
 
 }  // namespace phm

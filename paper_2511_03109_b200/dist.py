@@ -77,3 +77,61 @@ class PartialSum:
 
         dist.all_reduce(self.buf, op=dist.ReduceOp.SUM, group=group)
         return self.buf
+
+
+def nccl_comm(ctx, group=None):
+    """The library's own NCCL communicator for this rank (phm_comm_create_nccl):
+    rank 0's unique id is broadcast over the torch.distributed group, then
+    every rank joins. The sharded step then runs both exchanges inside the
+    library (phm_instantiate_apply_sharded), on the library's stream."""
+    import torch.distributed as dist
+
+    from . import Comm
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return Comm.nccl(ctx, obj[0], rank, world)
+
+
+def host_allreduce_comm(group=None):
+    """A library communicator whose all-reduce is torch.distributed on host
+    copies (gloo): drives the library's sharded step with ranks that share
+    one GPU, in tests. Synchronises the device, copies the buffer out,
+    all-reduces it, copies it back."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from . import Comm
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+    def fn(buf, count, stream):
+        torch.cuda.synchronize()
+        host = torch.from_numpy(np.empty(count, dtype=np.float64))
+        _memcpy(host.data_ptr(), buf, count * 8, 2)  # device -> host
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+        _memcpy(buf, host.data_ptr(), count * 8, 1)  # host -> device
+        # a pageable H2D cudaMemcpy may return before its DMA lands, and the
+        # library's streams are non-blocking (no implicit ordering with the
+        # legacy stream): wait for the device before the step continues
+        torch.cuda.synchronize()
+
+    return Comm.callback(fn, rank, world)
+
+
+_CUDART = None
+
+
+def _memcpy(dst, src, nbytes, kind):
+    """Synchronous cudaMemcpy on raw pointers (kind 1: H2D, 2: D2H)."""
+    import ctypes
+
+    global _CUDART
+    if _CUDART is None:
+        _CUDART = ctypes.CDLL("libcudart.so.12")
+        _CUDART.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+    err = _CUDART.cudaMemcpy(dst, src, nbytes, kind)
+    if err != 0:
+        raise RuntimeError(f"cudaMemcpy failed ({err})")
