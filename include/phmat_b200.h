@@ -262,6 +262,9 @@ typedef int (*phm_allreduce_fn)(double* buf_dev, int64_t count, void* cuda_strea
 int phm_comm_unique_id(uint8_t* id /* 128 bytes */);
 int phm_comm_create_nccl(phm_context ctx, const uint8_t* id /* 128 bytes */, int rank, int world, phm_comm* out);
 int phm_comm_create_callback(phm_allreduce_fn fn, void* user, int rank, int world, phm_comm* out);
+/* Single-GPU timing probe of one rank's sharded step: both exchanges are
+ * no-ops (the partials stay partial; y is NOT the product). Diagnostics only. */
+int phm_comm_create_probe(int rank, int world, phm_comm* out);
 int phm_comm_destroy(phm_comm comm);
 int phm_comm_info(phm_comm comm, int* rank, int* world, int* is_nccl);
 /* reinstantiate(theta) + apply(x) on this rank's shard, exchanges included;

@@ -69,6 +69,9 @@ _SIG = {
                           C.c_int, C.c_double, C.c_double, C.c_int, C.c_double, C.c_double, C.c_int64, C.c_int,
                           C.POINTER(_P)], C.c_int),
     "rfd_bench_destroy": ([_P], None),
+    "rfd_build_save": ([C.c_int64, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int, _DP, _DP, C.c_int, C.c_int,
+                        C.c_int, C.c_double, C.c_double, C.c_int, C.c_char_p, C.c_int], C.c_int),
+    "rfd_load": ([C.c_char_p, C.POINTER(_P)], C.c_int),
     "rfd_bench_info": ([_P, _DP], C.c_int),
     "rfd_bench_step": ([_P, C.c_int, _DP, _DP, C.c_int, _DP, _DP], C.c_int),
 }
@@ -167,6 +170,27 @@ def cheb_grid(lo: float, hi: float, p: int):
     nodes, w = np.empty(p), np.empty(p)
     _chk(lib().rfd_cheb_grid(lo, hi, p, _dp(nodes), _dp(w)))
     return nodes, w
+
+
+def build_save(path, n, d, seed, h2, family, boxes, l_max, p_s, p_theta, eps=1e-5, eta=1.0, near_tt=True,
+               threads=0):
+    """The reference's own offline build (offline_h / offline_h2 on its
+    generate_points) saved as an HMAT v1 artifact (save_parametric)."""
+    lo = np.array([b[0] for b in boxes], dtype=np.float64)
+    hi = np.array([b[1] for b in boxes], dtype=np.float64)
+    _chk(lib().rfd_build_save(n, d, seed, 1 if h2 else 0, family, len(boxes), _dp(lo), _dp(hi), l_max, p_s, p_theta,
+                              eps, eta, 1 if near_tt else 0, os.fsencode(path), threads))
+
+
+def load(path) -> "RefMatrix":
+    """load_parametric_h / _h2 of the reference into a RefMatrix."""
+    h = _P()
+    _chk(lib().rfd_load(os.fsencode(path), C.byref(h)))
+    R = RefMatrix.__new__(RefMatrix)
+    R._h = h
+    R._near_shape = None
+    R.n = int(R.nodes()["size"][0])  # the root holds every point
+    return R
 
 
 class RefInst:

@@ -518,6 +518,62 @@ int rfd_inst_to_dense(void* i, double* out, std::int64_t guard) {
   });
 }
 
+// ---- artifacts: the reference's own offline build, saved / loaded ---------
+// offline_h / offline_h2 of the reference itself (its TT-cross for the
+// couplings and, in TT near mode, for every near block; phmatrix.cpp:51-164)
+// on generate_points(n, d, seed), then save_parametric (serialize.cpp:108-
+// 177): the `phmat build --artifact` path (tools/phmat.cpp:155-171).
+int rfd_build_save(std::int64_t n, int d, std::uint64_t seed, int h2, int family, int d_theta, const double* lo,
+                   const double* hi, int l_max, int p_s, int p_theta, double eps, double eta, int near_tt,
+                   const char* path, int threads) {
+  return guarded([&] {
+    PHConfig cfg;
+    cfg.spec.family = static_cast<KernelFamily>(family);
+    for (int k = 0; k < d_theta; ++k) cfg.spec.theta_box.push_back({lo[k], hi[k]});
+    cfg.l_max = l_max;
+    cfg.p_s = p_s;
+    cfg.p_theta = p_theta;
+    cfg.eps = eps;
+    cfg.eta = eta;
+    cfg.near_mode = near_tt ? NearMode::TT : NearMode::Direct;
+    cfg.threads = threads;
+    StageCounters counters;
+    const Eigen::MatrixXd pts = generate_points(n, d, seed);
+    if (h2)
+      save_parametric(offline_h2(pts, cfg, counters), path);
+    else
+      save_parametric(offline_h(pts, cfg, counters), path);
+  });
+}
+
+// load_parametric_h / _h2 (serialize.cpp:180-269) into a driver handle
+// (instantiate / apply / near_d / far_h through the rfd_inst_* calls).
+int rfd_load(const char* path, void** out) {
+  return guarded([&] {
+    auto M = std::make_unique<RefMatrix>();
+    M->h2 = artifact_is_h2(path);
+    auto fill = [&](auto& pm) {
+      M->cfg = pm->config;
+      M->tree = std::const_pointer_cast<ClusterTree>(pm->tree);
+      M->blocks = pm->blocks;
+      M->grids = pm->theta_grids;
+      M->far_key = pm->far_key;
+      M->couplings = pm->couplings;
+      M->rep.assign(pm->couplings.size(), 0);
+      M->near = pm->near;
+    };
+    if (M->h2) {
+      M->ph2 = std::make_shared<ParametricH2Matrix>(load_parametric_h2(path));
+      fill(M->ph2);
+      M->basis = std::make_shared<NestedClusterBasis>(M->ph2->basis);
+    } else {
+      M->ph = std::make_shared<ParametricHMatrix>(load_parametric_h(path));
+      fill(M->ph);
+    }
+    *out = M.release();
+  });
+}
+
 // ---- per-block entry points (full-size sampled parity without a full build)
 int rfd_class_h(void* h, int k, const double* theta, double* out, std::int64_t* shape) {
   return guarded([&] {

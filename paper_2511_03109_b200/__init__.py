@@ -162,6 +162,7 @@ SIGNATURES = {
     "phm_comm_unique_id": ([C.c_char_p], C.c_int),
     "phm_comm_create_nccl": ([_P, C.c_char_p, C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
     "phm_comm_create_callback": ([_P, _P, C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
+    "phm_comm_create_probe": ([C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
     "phm_comm_destroy": ([_P], C.c_int),
     "phm_comm_info": ([_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
     "phm_instantiate_apply_sharded": ([_P, _P, _DP, C.c_int, _P, _P, C.c_int64], C.c_int),
@@ -641,6 +642,13 @@ class Comm:
         h = _P()
         _check(lib().phm_comm_create_callback(C.cast(cfn, _P), None, rank, world, C.byref(h)))
         return cls(h, keep=cfn)
+
+    @classmethod
+    def probe(cls, rank: int, world: int) -> "Comm":
+        """No-op exchanges: times one rank's sharded step on one GPU."""
+        h = _P()
+        _check(lib().phm_comm_create_probe(rank, world, C.byref(h)))
+        return cls(h)
 
     def info(self):
         r, w, k = C.c_int(), C.c_int(), C.c_int()

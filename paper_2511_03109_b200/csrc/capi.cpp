@@ -762,6 +762,14 @@ int phm_comm_create_callback(phm_allreduce_fn fn, void* user, int rank, int worl
     *out = c.release();
   });
 }
+int phm_comm_create_probe(int rank, int world, phm_comm* out) {
+  return guarded([&] {
+    need(out, "out");
+    auto c = std::make_unique<phm_comm_s>();
+    c->c = phm::comm_probe(rank, world);
+    *out = c.release();
+  });
+}
 int phm_comm_destroy(phm_comm c) {
   return guarded([&] { delete c; });
 }

@@ -95,6 +95,17 @@ class CallbackComm final : public Comm {
   void* user_;
 };
 
+class ProbeComm final : public Comm {
+ public:
+  ProbeComm(int rank_, int world_) {
+    rank = rank_;
+    world = world_;
+  }
+  void allreduce(double*, std::int64_t, void*) override {}
+  bool capturable() const override { return true; }
+  const char* kind() const override { return "probe"; }
+};
+
 }  // namespace
 
 void nccl_unique_id(void* out128) {
@@ -106,6 +117,11 @@ void nccl_unique_id(void* out128) {
 std::shared_ptr<Comm> comm_nccl(int device, const void* id128, int rank, int world) {
   if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("comm: bad rank / world");
   return std::make_shared<NcclComm>(device, id128, rank, world);
+}
+
+std::shared_ptr<Comm> comm_probe(int rank, int world) {
+  if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("comm: bad rank / world");
+  return std::make_shared<ProbeComm>(rank, world);
 }
 
 std::shared_ptr<Comm> comm_callback(AllreduceFn fn, void* user, int rank, int world) {

@@ -34,5 +34,8 @@ class Comm {
 void nccl_unique_id(void* out128);
 std::shared_ptr<Comm> comm_nccl(int device, const void* id128, int rank, int world);
 std::shared_ptr<Comm> comm_callback(AllreduceFn fn, void* user, int rank, int world);
+// Timing probe of one rank on one GPU: the exchanges are no-ops (the rank's
+// partials stay partial), capturable, so the rank's step replays as a graph.
+std::shared_ptr<Comm> comm_probe(int rank, int world);
 
 }  // namespace phm

@@ -215,3 +215,34 @@ def test_c4_form_largest_single_gpu_vs_reference(ph, pr, parity_log):
             assert e1 <= TOL_Y and e2 <= TOL_Y
             log("Y_rows_apply", e1)
             log("Y_rows_fused", e2)
+
+
+@pytest.mark.parametrize("h2,near_tt,family", [(True, True, "se"), (False, True, "se"), (True, False, "e"),
+                                               (False, False, "mc")])
+def test_reference_artifact_on_gpu(ph, pr, tmp_path, parity_log, h2, near_tt, family):
+    """The drop-in path `phmat build --artifact` -> GPU instantiate
+    (tools/phmat.cpp:155-204): the reference builds and saves its own
+    parametric matrix (its TT-cross; TT or Direct near mode), the product
+    loads the file onto the GPU (phm_matrix_load), and instantiate + apply
+    there equal the reference's instantiate + apply of the same file."""
+    log = lambda k, v: parity_log(f"reference_artifact_{'h2' if h2 else 'h'}_{'tt' if near_tt else 'direct'}", k, v)  # noqa: E731,E501
+    fam = {"se": pr.REF_SE, "e": pr.REF_E, "mc": pr.REF_MC}[family]
+    path = str(tmp_path / "ref.hmat")
+    pr.build_save(path, 2000, 3, 8, h2, fam, [(0.25, 1.0)], 2, 4, 6, eps=1e-6, eta=1.0, near_tt=near_tt,
+                  threads=THREADS)
+    R = pr.load(path)
+    pm = ph.load_parametric(path)
+    near, far, key = pm.blocks()
+    sizes = _sizes(pm)
+    x = pr.generate_normal(2000, 2)
+    for th in ([0.25], [0.61], [1.0]):
+        inst, ri = ph.instantiate(pm, th), R.instantiate(th)
+        wd = max(rel(inst.near_d(b, (sizes[near[b, 0]], sizes[near[b, 1]])), ri.near_d(b)) for b in range(len(near)))
+        wf = max(rel(inst.far_h(i), ri.far_h(i)) for i in range(0, len(far), 5))
+        y = ri.apply(x)
+        ey, ef = rel(inst.apply(x), y), rel(inst.instantiate_apply(th, x), y)
+        assert wd <= TOL_BLOCK and wf <= TOL_BLOCK and ey <= TOL_Y and ef <= TOL_Y
+        log("D_b", wd)
+        log("far_h", wf)
+        log("y_apply", ey)
+        log("y_fused", ef)

@@ -237,3 +237,33 @@ def test_reference_domain_error_and_grid(ph):
         R.instantiate([0.6])
     nodes, _ = R.theta_grid(0)
     assert np.array_equal(nodes, pm.theta_grid(0))
+
+
+@pytest.mark.parametrize("h2,near_tt", [(True, True), (False, True), (True, False)])
+def test_reference_written_artifact_loads_into_product(ph, po, tmp_path, h2, near_tt):
+    """the reference's own `phmat build --artifact` path
+    (offline_h / offline_h2 with its TT-cross for couplings and near blocks,
+    then save_parametric; tools/phmat.cpp:155-171) read by the product's
+    loader (phm_matrix_load_host). The loaded structure is the reference's,
+    and the oracle fed the loaded TT data reproduces the reference's own
+    instantiate + apply of the same file (load_parametric_h/_h2)."""
+    path = str(tmp_path / "ref.hmat")
+    pr.build_save(path, 900, 2, 3, h2, pr.REF_SE, [(0.25, 1.0)], 2, 5, 6, eps=1e-6, eta=1.0, near_tt=near_tt)
+    assert ph.artifact_is_h2(path) == h2
+    R = pr.load(path)
+    pm = ph.load_parametric_structure(path)
+    pts = pr.generate_points(900, 2, 3)
+    near, far, key = pm.blocks()
+    rn, rf, rk = R.blocks()
+    assert np.array_equal(near, rn) and np.array_equal(far, rf) and np.array_equal(key, rk)
+    assert np.array_equal(pm.perm(), R.perm())
+    if not near_tt:
+        return  # Direct mode: the near field is evaluated online (checked on the GPU)
+    om = po.from_product(pm, pts)
+    x = pr.generate_normal(900, 4)
+    for th in ([0.3], [0.77]):
+        ri, oi = R.instantiate(th), om.instantiate(th)
+        assert rel(oi.apply(x), ri.apply(x)) <= 1e-12
+        sizes = pm.nodes()[0][:, 3]
+        for b in range(0, len(near), 17):
+            assert rel(oi.near(b, (int(sizes[near[b, 0]]), int(sizes[near[b, 1]]))), ri.near_d(b)) <= 1e-12
