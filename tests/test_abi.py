@@ -72,6 +72,16 @@ int main() {
   phm_matrix_destroy(m);
   try { phmat_b200::Context ctx(0); std::printf("gpu\n"); }
   catch (const std::runtime_error& e) { std::printf("nogpu\n"); }
+  // the reference-shaped API: PHConfig / StageCounters / offline_h2 over a
+  // row-major point matrix (no Eigen here: the facade's own Matrix type)
+  phmat_b200::Matrix P(256, 2);
+  for (int i = 0; i < 256; ++i) { P(i, 0) = pts[2 * i]; P(i, 1) = pts[2 * i + 1]; }
+  phmat_b200::PHConfig rc;
+  rc.spec = phmat_b200::default_kernel_spec(phmat_b200::KernelFamily::SquaredExponential);
+  rc.l_max = 2; rc.p_s = 4; rc.p_theta = 5; rc.eps = 1e-3;
+  phmat_b200::StageCounters counters;
+  try { auto pm = phmat_b200::offline_h2(P, rc, counters); std::printf("built\n"); }
+  catch (const std::runtime_error&) { std::printf("nogpu-build\n"); }
   try { std::vector<double> th{3.0}; phm_instance i; phmat_b200::check(phm_instantiate(nullptr, th.data(), 1, &i)); }
   catch (const std::invalid_argument&) { std::printf("invalid\n"); }
   return 0;
@@ -79,7 +89,7 @@ int main() {
 ''')
     exe = tmp_path / "t"
     libdir = os.path.dirname(ph.library_path())
-    subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+    subprocess.run(["g++", "-std=c++20", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
                     "-L", libdir, "-lphmat_b200", f"-Wl,-rpath,{libdir}"], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
     assert "near=" in out and "invalid" in out

@@ -246,3 +246,21 @@ def test_reference_artifact_on_gpu(ph, pr, tmp_path, parity_log, h2, near_tt, fa
         log("far_h", wf)
         log("y_apply", ey)
         log("y_fused", ef)
+
+
+def test_cpp_facade_drop_in_against_reference(tmp_path):
+    """tests/cpp/dropin_check.cpp (built by oracle/ref_build.sh): the same C++
+    program text against the reference's API (namespace phmat, CPU) and the
+    product's facade (namespace phmat_b200, include/phmat_b200.hpp, GPU),
+    both on Eigen types: the reference builds + saves, the facade loads onto
+    the GPU, instantiate / apply / far_h / near_d / to_dense agree, the
+    facade's own offline_h2 has the reference's structure, and the exception
+    types match."""
+    import json
+    import subprocess
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_check")
+    assert os.path.exists(exe), "oracle/_ref/dropin_check not built (oracle/ref_build.sh)"
+    res = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    assert res.returncode == 0 and out["ok"], res.stdout + res.stderr
