@@ -64,9 +64,10 @@ int main() {
   std::vector<double> pts(2 * 256);
   phm_generate_points(256, 2, 3, pts.data());
   phmat_b200::PHConfig cfg;
-  cfg.c.l_max = 2; cfg.c.p_s = 4; cfg.c.p_theta[0] = 5; cfg.c.eps = 1e-3;
+  cfg.l_max = 2; cfg.p_s = 4; cfg.p_theta = 5; cfg.eps = 1e-3;
+  const phm_config cc = cfg.to_c(PHM_FORMAT_H2);
   phm_matrix m = nullptr;
-  phmat_b200::check(phm_matrix_build_host(pts.data(), 256, 2, &cfg.c, &m));
+  phmat_b200::check(phm_matrix_build_host(pts.data(), 256, 2, &cc, &m));
   phm_info info; phmat_b200::check(phm_matrix_info(m, &info));
   std::printf("near=%lld far=%lld\n", (long long)info.n_near, (long long)info.n_far);
   phm_matrix_destroy(m);
