@@ -64,6 +64,7 @@ int main() {
   std::vector<double> pts(2 * 256);
   phm_generate_points(256, 2, 3, pts.data());
   phmat_b200::PHConfig cfg;
+  cfg.spec = phmat_b200::default_kernel_spec(phmat_b200::KernelFamily::SquaredExponential);
   cfg.l_max = 2; cfg.p_s = 4; cfg.p_theta = 5; cfg.eps = 1e-3;
   const phm_config cc = cfg.to_c(PHM_FORMAT_H2);
   phm_matrix m = nullptr;
