@@ -722,7 +722,13 @@ __global__ void __maxnreg__(P >= 128 ? 128 : 88) k_coupling_mma(const CouplingIt
   constexpr int KS = P / 4;           // k-steps of the m16n8k4 MMA
   constexpr int NT = kGroupSlots / 8; // n-tiles of 8 slots
   constexpr int PANEL = kGroupSlots * LD;
-  constexpr int KH = KS / 2 > 0 ? KS / 2 : 1;  // k-steps per fragment load
+  // C_k fragments are loaded a quarter of the k-steps at a time into two
+  // ping-pong register buffers: the next quarter's (or the next class's
+  // first quarter's) L2 loads are in flight while this quarter's MMAs run
+  // (ncu, C3 apply: long-scoreboard stalls on these loads dominated)
+  constexpr int KH = KS >= 4 ? 4 : KS;        // k-steps per fragment load
+  constexpr int NQ = KS / KH;                 // loads per class
+  constexpr bool kCross = (NQ % 2) == 0;      // next class starts in buffer 0
   extern __shared__ double smem[];    // 2 stages of [32][LD]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t0 = lane & 3;
   const int row0 = warp * 16;
@@ -737,16 +743,24 @@ __global__ void __maxnreg__(P >= 128 ? 128 : 88) k_coupling_mma(const CouplingIt
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
 
-    auto gather = [&](int e, int buf) {
-      const std::int32_t* taus = cls_tau + static_cast<std::int64_t>(e) * kGroupSlots;
+    // X panel gather: thread t serves slot t / TPS (TPS = threads per
+    // slot) and 16-byte pairs t % TPS + TPS * j of that slot's x-hat column,
+    // so each thread needs ONE tau per class -- loaded a class ahead (ncu:
+    // the per-pair tau load in front of every cp.async was the hottest stall)
+    constexpr int TPS = (2 * P) / kGroupSlots;  // blockDim = 2P
+    constexpr int PPT = (P / 2) / TPS;          // pairs per thread
+    const int gslot = threadIdx.x / TPS, gsub = threadIdx.x % TPS;
+    auto tau_of = [&](int e) { return cls_tau[static_cast<std::int64_t>(e) * kGroupSlots + gslot]; };
+    auto gather = [&](int e, int buf, int tau) {
       const unsigned tiles = item_tiles[e];
-      double* X = smem + buf * PANEL;
-      for (int q2 = threadIdx.x; q2 < kGroupSlots * (P / 2); q2 += blockDim.x) {
-        const int slot = q2 / (P / 2), q = q2 % (P / 2);
-        if (!((tiles >> (slot >> 3)) & 1u)) continue;  // tile skipped by the MMAs
-        const int tau = taus[slot];
-        const double* src = xhat + (static_cast<std::int64_t>(tau < 0 ? 0 : tau) * m + col) * P + 2 * q;
-        cp_async16(X + slot * LD + 2 * q, src, tau >= 0);
+      double* X = smem + buf * PANEL + gslot * LD;
+      if ((tiles >> (gslot >> 3)) & 1u) {  // else the tile is skipped by the MMAs
+        const double* src = xhat + (static_cast<std::int64_t>(tau < 0 ? 0 : tau) * m + col) * P;
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const int q = gsub + TPS * j;
+          cp_async16(X + 2 * q, src + 2 * q, tau >= 0);
+        }
       }
       cp_async_commit();
     };
@@ -760,34 +774,44 @@ __global__ void __maxnreg__(P >= 128 ? 128 : 88) k_coupling_mma(const CouplingIt
       }
     };
     auto mma = [&](const double (&a)[KH][2], int h, const double* X, unsigned tiles) {
-      // tile-outer so an empty tile is a branch around its MMAs (a
-      // predicated MMA would still occupy the pipe)
+      // k-step outer, tile inner: the NT accumulators are independent
+      // chains in flight; an empty tile is a (warp-uniform) branch around
+      // its MMA (a predicated MMA would still occupy the pipe)
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        if (!((tiles >> j) & 1u)) continue;
+      for (int s2 = 0; s2 < KH; ++s2)
 #pragma unroll
-        for (int s2 = 0; s2 < KH; ++s2)
-          dmma_16x8x4(acc[j], a[s2][0], a[s2][1], X[(8 * j + g) * LD + 4 * (h * KH + s2) + t0]);
-      }
+        for (int j = 0; j < NT; ++j)
+          if ((tiles >> j) & 1u)
+            dmma_16x8x4(acc[j], a[s2][0], a[s2][1], X[(8 * j + g) * LD + 4 * (h * KH + s2) + t0]);
     };
 
     const int e0 = it.e_begin;
-    if (e0 < it.e_end) gather(e0, 0);
+    double a[2][KH][2];
+    int tau_next = 0;
+    if (e0 < it.e_end) {
+      gather(e0, 0, tau_of(e0));
+      load_a(e0, 0, a[0]);
+      if (e0 + 1 < it.e_end) tau_next = tau_of(e0 + 1);
+    }
     for (int e = e0; e < it.e_end; ++e) {
       const int buf = (e - e0) & 1;
       if (e + 1 < it.e_end) {
-        gather(e + 1, buf ^ 1);
+        gather(e + 1, buf ^ 1, tau_next);
+        if (e + 2 < it.e_end) tau_next = tau_of(e + 2);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncthreads();
       const unsigned tiles = item_tiles[e];
+      if (!kCross) load_a(e, 0, a[0]);
 #pragma unroll
-      for (int h = 0; h < KS / KH; ++h) {
-        double a[KH][2];
-        load_a(e, h, a);
-        mma(a, h, smem + buf * PANEL, tiles);
+      for (int h = 0; h < NQ; ++h) {
+        if (h + 1 < NQ)
+          load_a(e, h + 1, a[(h + 1) & 1]);
+        else if (kCross && e + 1 < it.e_end)
+          load_a(e + 1, 0, a[0]);
+        mma(a[h & 1], h, smem + buf * PANEL, tiles);
       }
       __syncthreads();  // X[buf] is refilled two classes later
     }
