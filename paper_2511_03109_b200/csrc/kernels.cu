@@ -774,15 +774,26 @@ __global__ void __maxnreg__(P >= 128 ? 128 : 88) k_coupling_mma(const CouplingIt
       }
     };
     auto mma = [&](const double (&a)[KH][2], int h, const double* X, unsigned tiles) {
-      // k-step outer, tile inner: the NT accumulators are independent
-      // chains in flight; an empty tile is a (warp-uniform) branch around
-      // its MMA (a predicated MMA would still occupy the pipe)
+      if (tiles == (1u << NT) - 1u) {
+        // every tile holds a partner: k-step outer, tile inner, so the NT
+        // accumulators are independent chains in flight
 #pragma unroll
-      for (int s2 = 0; s2 < KH; ++s2)
+        for (int s2 = 0; s2 < KH; ++s2)
 #pragma unroll
-        for (int j = 0; j < NT; ++j)
-          if ((tiles >> j) & 1u)
+          for (int j = 0; j < NT; ++j)
             dmma_16x8x4(acc[j], a[s2][0], a[s2][1], X[(8 * j + g) * LD + 4 * (h * KH + s2) + t0]);
+        return;
+      }
+      // tile outer: an empty tile is a (warp-uniform) branch around its
+      // MMAs; with the tile test inside the k loop the compiler predicates
+      // the MMAs instead, and a predicated MMA still occupies the pipe
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        if (!((tiles >> j) & 1u)) continue;
+#pragma unroll
+        for (int s2 = 0; s2 < KH; ++s2)
+          dmma_16x8x4(acc[j], a[s2][0], a[s2][1], X[(8 * j + g) * LD + 4 * (h * KH + s2) + t0]);
+      }
     };
 
     const int e0 = it.e_begin;
