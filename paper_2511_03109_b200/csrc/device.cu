@@ -1695,15 +1695,16 @@ void near_product(DevInstance& I, Index m, cudaStream_t st) {
   // runs on fp64 tensor cores (K9); single vectors stay on the HBM GEMV.
   // K9 computes rows sigma only, so a symmetric shard (whose transposed
   // products belong to other ranks' rows) keeps the two-sided GEMV.
-  static const bool two_sided = [] {
+  static const int two_sided_env = [] {  // 0: never, 2: also above 32 RHS unsharded (diagnostics)
     const char* e = std::getenv("PHM_K9_TWO_SIDED");
-    return !(e && std::atoi(e) == 0);
+    return e ? std::atoi(e) : 1;
   }();
+  const bool two_sided = two_sided_env != 0;
   // up to 32 RHS: each stored block read once, both products on DMMA
   // (k_near_mrhs3, TMA-staged: C3 at 10 RHS 3.5 ms against 6.4 for the
   // one-sided K9). At 64 RHS the one-sided K9 is faster (13.8 vs 16.8 ms +
   // 3.3 ms of gather), except on a symmetric shard, which needs both sides.
-  if (m >= kMrhsMin && M.n_sym_items > 0 && two_sided && (m <= 32 || (M.sym && M.sharded))) {
+  if (m >= kMrhsMin && M.n_sym_items > 0 && two_sided && (m <= 32 || (M.sym && M.sharded) || two_sided_env == 2)) {
     const size_t need = sizeof(double) * M.sym_pstride * m;
     if (M.sym_part_m.bytes < need) {
       M.sym_part_m.alloc(need);

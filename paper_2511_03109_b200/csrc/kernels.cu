@@ -1640,7 +1640,7 @@ __global__ void __maxnreg__(96) k_inst_tma(const double* __restrict__ G, std::in
 // lengths, k beyond the chunk, rows beyond the slice) are masked to zero
 // before they reach an MMA, so stale shared memory never contributes.
 template <int NC, int NST>
-__global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ items,
+__global__ void __maxnreg__(NC >= 64 ? 168 : 96) k_near_mrhs3(const SymRowItem* __restrict__ items,
                                               const SymBlock* __restrict__ blocks, const double* __restrict__ D,
                                               const double* __restrict__ X, std::int64_t n, int m,
                                               std::int64_t pstride, double* __restrict__ part, int dstage) {
@@ -1705,19 +1705,33 @@ __global__ void __maxnreg__(96) k_near_mrhs3(const SymRowItem* __restrict__ item
           src_d = col - sh;
           bytes_d = static_cast<unsigned>(((R + sh + 1) & ~1) * 8);
         }
-        if (lane < ncr) {
-          const double* xc = X + blk.x_col0 + j0 + static_cast<std::int64_t>(c0 + lane) * n;
-          const int sh = static_cast<int>((reinterpret_cast<std::uintptr_t>(xc) >> 3) & 1);
-          src_x = xc - sh;
-          bytes_x = static_cast<unsigned>(((kc + sh + 1) & ~1) * 8);
+        // RHS columns lane, lane + 32 (NC = 64)
+        constexpr int XC = NC > 32 ? NC / 32 : 1;
+        const double* src_xs[XC];
+        unsigned bytes_xs[XC];
+#pragma unroll
+        for (int u = 0; u < XC; ++u) {
+          const int cc = lane + 32 * u;
+          src_xs[u] = nullptr;
+          bytes_xs[u] = 0;
+          if (cc < ncr) {
+            const double* xc = X + blk.x_col0 + j0 + static_cast<std::int64_t>(c0 + cc) * n;
+            const int sh = static_cast<int>((reinterpret_cast<std::uintptr_t>(xc) >> 3) & 1);
+            src_xs[u] = xc - sh;
+            bytes_xs[u] = static_cast<unsigned>(((kc + sh + 1) & ~1) * 8);
+            bytes_x += bytes_xs[u];
+          }
         }
+        (void)src_x;
         unsigned total = bytes_d + bytes_x;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
         if (lane == 0) mbar_expect_tx(&full[slot], total);
         __syncwarp();
         if (bytes_d) bulk_g2s(Dc + lane * kK9bLd, src_d, bytes_d, &full[slot]);
-        if (bytes_x) bulk_g2s(Xt + lane * LDX, src_x, bytes_x, &full[slot]);
+#pragma unroll
+        for (int u = 0; u < XC; ++u)
+          if (bytes_xs[u]) bulk_g2s(Xt + (lane + 32 * u) * LDX, src_xs[u], bytes_xs[u], &full[slot]);
       }
     }
     return;
@@ -2496,11 +2510,13 @@ void launch_near_mrhs3(cudaStream_t st, const SymRowItem* items, int nitems, con
   auto bytes = [&](int nc, int nst) {
     return static_cast<size_t>(nc * kK9bLd + nst * (dstage + nc * (kK9bKc + 4))) * sizeof(double);
   };
-  const int nc = m <= 8 ? 8 : (m <= 16 ? 16 : 32);
-  // the deepest ring (<= 4) that keeps two CTAs per SM
+  // more than 32 RHS: one 64-column tile, so D is read once (one CTA per SM)
+  const int nc = m <= 8 ? 8 : (m <= 16 ? 16 : (m <= 32 ? 32 : 64));
+  // the deepest ring (<= 4) that keeps two CTAs per SM (one for 64 columns)
+  const size_t budget = nc == 64 ? 226 * 1024 : 113 * 1024;
   int nst = 2;
   for (int q = 4; q > 2; --q)
-    if (bytes(nc, q) + 2048 <= 113 * 1024) {
+    if (bytes(nc, q) + 2048 <= budget) {
       nst = q;
       break;
     }
@@ -2516,6 +2532,7 @@ void launch_near_mrhs3(cudaStream_t st, const SymRowItem* items, int nitems, con
   PHM_K9C(8, 2) PHM_K9C(8, 3) PHM_K9C(8, 4)
   PHM_K9C(16, 2) PHM_K9C(16, 3) PHM_K9C(16, 4)
   PHM_K9C(32, 2) PHM_K9C(32, 3) PHM_K9C(32, 4)
+  PHM_K9C(64, 2) PHM_K9C(64, 3) PHM_K9C(64, 4)
 #undef PHM_K9C
 }
 
