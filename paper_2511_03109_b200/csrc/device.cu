@@ -1810,9 +1810,13 @@ void apply_tree_order(DevInstance& I, Index m, Comm* ex = nullptr) {
     far_finish(I, m, ctx.stream);
     return;
   }
+  static const int apply_cp_per_sm = [] {  // diagnostics: coupling CTAs per SM in apply (0: full grid)
+    const char* e = std::getenv("PHM_APPLY_COUPLING_PER_SM");
+    return e ? std::atoi(e) : 0;
+  }();
   if (M.h2) {
     ctx.fork();
-    far_chain(I, m, ctx.side, 0, ex);
+    far_chain(I, m, ctx.side, apply_cp_per_sm * ctx.sms, ex);
   }
   near_product(I, m, ctx.stream);
   if (M.h2) ctx.join();

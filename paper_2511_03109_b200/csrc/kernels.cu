@@ -1339,13 +1339,29 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_near_tma(const SymRowItem* _
     const double* S = sm + slot * R * CH;
     const int nel = ncols * ld;
     double* Dg = D + d_off + static_cast<std::int64_t>(j0) * ld;
-    for (int e = tid; e < nel; e += 256) {
+    // D goes out in 256-bit stores: a scalar head up to the first 32-byte
+    // boundary of the chunk, aligned groups of four, a scalar tail (the
+    // same FMA order per element as before: D is unchanged bitwise)
+    auto form = [&](int e) {
       double v = 0.0;
 #pragma unroll
       for (int k = 0; k < R; ++k) v += S[k * CH + e] * wr[k];
       dc[e] = v;
-      Dg[e] = v;
+      return v;
+    };
+    const int head = min(nel, static_cast<int>((4 - ((reinterpret_cast<std::uintptr_t>(Dg) >> 3) & 3)) & 3));
+    const int nq = (nel - head) >> 2, tail0 = head + 4 * nq;
+    if (tid < head) Dg[tid] = form(tid);
+    for (int q = tid; q < nq; q += 256) {
+      const int e = head + 4 * q;
+      dbl4 v;
+      v.x = form(e);
+      v.y = form(e + 1);
+      v.z = form(e + 2);
+      v.w = form(e + 3);
+      st4(Dg + e, v);
     }
+    if (tid < nel - tail0) Dg[tail0 + tid] = form(tail0 + tid);
     consumers_sync();
     if (tid == 0) mbar_arrive(&empty[slot]);  // stage formed: the producer may refill it
     if (rg < ng) {
