@@ -242,6 +242,17 @@ struct StructureMetrics {
   Index n_near = 0;
 };
 
+// generate_points (harness.hpp:77-78, harness.cpp:174-181): the reference's
+// seeded U[0,1)^d stream, n x d.
+inline Matrix generate_points(Index n, int d, std::uint64_t seed) {
+  std::vector<double> p(static_cast<size_t>(n * d));
+  check(phm_generate_points(n, d, seed, p.data()));
+  Matrix out = make_matrix(n, d);
+  for (Index i = 0; i < n; ++i)
+    for (int k = 0; k < d; ++k) out(i, k) = p[static_cast<size_t>(i * d + k)];
+  return out;
+}
+
 // ----------------------------------------------------------------- context
 // One CUDA device + stream; shared by every matrix built on it.
 class Context {

@@ -264,3 +264,28 @@ def test_cpp_facade_drop_in_against_reference(tmp_path):
     res = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
     out = json.loads(res.stdout.strip().splitlines()[-1])
     assert res.returncode == 0 and out["ok"], res.stdout + res.stderr
+
+
+def test_c5_sweep_batch_and_10_rhs_vs_reference(ph, c3, parity_log):
+    """C5 (BASELINE configs[4]) = the C3 matrix, thetas instantiated 8 per
+    snapshot pass (phm_instantiate_batch) and applied to 10 RHS each (K9 +
+    multi-RHS coupling): probe rows of every RHS column against the
+    reference's rows, for every theta of one batch."""
+    log = lambda k, v: parity_log("c5_full_size_batch8_10rhs", k, v)  # noqa: E731
+    pm, R, c, pts = c3
+    b = _bench()
+    thetas = b.theta_vectors(b.CONFIGS["c5"], 8, 3)
+    insts = ph.instantiate_batch(pm, thetas)
+    X = np.stack([ph.generate_normal(c["n"], 40 + j) for j in range(10)], axis=1)
+    rows = np.sort(np.random.default_rng(9).choice(c["n"], 12, replace=False))
+    info = pm.info()
+    near_ids = np.sort(np.random.default_rng(4).choice(info["n_near"], 200, replace=False))
+    for q, (th, inst) in enumerate(zip(thetas, insts)):
+        th = list(th)
+        if q in (0, 7):
+            _check_blocks(ph, pm, inst, R, th, near_ids, range(0, info["n_classes"], 25), log=log)
+        Y = inst.apply(X)
+        yr = R.apply_rows(th, X, rows, threads=THREADS)
+        e = max(rel(Y[rows, j], yr[:, j]) for j in range(10))
+        assert e <= TOL_Y
+        log("Y_rows_10rhs", e)
