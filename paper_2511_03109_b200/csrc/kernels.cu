@@ -1339,29 +1339,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_near_tma(const SymRowItem* _
     const double* S = sm + slot * R * CH;
     const int nel = ncols * ld;
     double* Dg = D + d_off + static_cast<std::int64_t>(j0) * ld;
-    // D goes out in 256-bit stores: a scalar head up to the first 32-byte
-    // boundary of the chunk, aligned groups of four, a scalar tail (the
-    // same FMA order per element as before: D is unchanged bitwise)
-    auto form = [&](int e) {
+    // Coalesced 64-bit stores (a warp writes 256 contiguous bytes). A
+    // 256-bit-store variant (each thread forming four consecutive elements)
+    // read the stage with a stride of four doubles -- 4-way bank conflicts --
+    // and cost the fused C3 step 23% (115 -> 87 theta/s, round 2).
+    for (int e = tid; e < nel; e += 256) {
       double v = 0.0;
 #pragma unroll
       for (int k = 0; k < R; ++k) v += S[k * CH + e] * wr[k];
       dc[e] = v;
-      return v;
-    };
-    const int head = min(nel, static_cast<int>((4 - ((reinterpret_cast<std::uintptr_t>(Dg) >> 3) & 3)) & 3));
-    const int nq = (nel - head) >> 2, tail0 = head + 4 * nq;
-    if (tid < head) Dg[tid] = form(tid);
-    for (int q = tid; q < nq; q += 256) {
-      const int e = head + 4 * q;
-      dbl4 v;
-      v.x = form(e);
-      v.y = form(e + 1);
-      v.z = form(e + 2);
-      v.w = form(e + 3);
-      st4(Dg + e, v);
+      Dg[e] = v;
     }
-    if (tid < nel - tail0) Dg[tail0 + tid] = form(tail0 + tid);
     consumers_sync();
     if (tid == 0) mbar_arrive(&empty[slot]);  // stage formed: the producer may refill it
     if (rg < ng) {
@@ -1778,6 +1766,31 @@ __global__ void __maxnreg__(NC >= 64 ? 168 : 96) k_near_mrhs3(const SymRowItem* 
       };
       const int ksy = (kc + 3) >> 2;
       // Y_sigma += D(:, chunk) X_tau(chunk, :)
+      if (warp + 8 * (YQ - 1) < ypairs) {
+        // every pair of this warp is live: k-step outer, pair inner, so the
+        // YQ accumulators are independent DMMA chains (pair-outer made each
+        // a serial chain of ksy dependent MMAs: ncu "wait" stalls); the
+        // pairs share this lane's B column (nt = warp mod NTN)
+        const int nt = warp % NTN;
+        const int ncol_b = 8 * nt + g;
+        const bool bin = ncol_b < ncr;
+        const int xsh = bin ? static_cast<int>(((reinterpret_cast<std::uintptr_t>(
+                                   X + blk.x_col0 + j0 + static_cast<std::int64_t>(c0 + ncol_b) * n)) >> 3) & 1)
+                            : 0;
+        for (int s2 = 0; s2 < ksy; ++s2) {
+          const int k = 4 * s2 + t0;
+          const bool kin = k < kc;
+          const int sh = kin ? dsh(k) : 0;
+          const double b0 = (kin && bin) ? Xt[ncol_b * LDX + xsh + k] : 0.0;
+#pragma unroll
+          for (int q = 0; q < YQ; ++q) {
+            const int mt = (warp + 8 * q) / NTN;
+            const double a0 = kin ? Dc[k * cs + sh + 16 * mt + g] : 0.0;
+            const double a1 = kin ? Dc[k * cs + sh + 16 * mt + g + 8] : 0.0;
+            dmma_16x8x4(yacc[q], a0, a1, b0);
+          }
+        }
+      } else
 #pragma unroll
       for (int q = 0; q < YQ; ++q) {
         const int p = warp + 8 * q;

@@ -34,4 +34,23 @@ for k in k_near_mrhs3 k_coupling_mma; do
   ncu --set full --import-source on --clock-control none -k "regex:${k}\b" --launch-skip 3 -c 1 -o $out/apply_m10_full_$k -f \
     python tools/apply_probe.py --rhs 10 --steps 2 > $out/apply_m10_full_$k.log 2>&1
 done
+# keep what comes back under gpurun's 64 MiB: summaries of every capture, the
+# captures themselves only when small
+for r in $out/*.ncu-rep; do
+  python profiles/summarize_full.py $r > ${r%.ncu-rep}_summary.txt 2>&1
+  ncu -i $r --page source --csv --print-source sass > ${r%.ncu-rep}_sass.csv 2>/dev/null
+  python - "${r%.ncu-rep}_sass.csv" > ${r%.ncu-rep}_hot.txt <<'PY'
+import csv, sys
+rows = list(csv.reader(open(sys.argv[1])))
+hdr = rows[1]; data = rows[2:]
+i = hdr.index("Warp Stall Sampling (All Samples)")
+tot = sum(int(r[i]) for r in data if r[i].isdigit())
+print("warp stall samples", tot)
+for r in sorted(data, key=lambda r: -int(r[i]) if r[i].isdigit() else 0)[:25]:
+    print(r[i], r[0][-6:], r[1].strip()[:90])
+PY
+  rm -f ${r%.ncu-rep}_sass.csv
+  [ $(stat -c %s $r) -gt 6000000 ] && rm -f $r
+done
+du -sh $out
 echo done
