@@ -383,6 +383,7 @@ struct DevMatrix {
   // only those some local far block uses (the rest are never read)
   DBuf cmeta_run;
   int ncls_run = 0;
+  std::vector<char> cls_run;  // per class: instantiated by this matrix's class stage
   std::vector<dev::ClassMeta> cmeta_h;
   DBuf cmeta, class_mid, class_mid_dims, class_L, class_R;
   bool baseline = false;  // fixed far field (H-ACA / H^2-HCA at one theta)
@@ -1042,6 +1043,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
       for (int k = 0; k < M.ncls; ++k)
         if (need[k]) run.push_back(M.cmeta_h[k]);
       M.ncls_run = static_cast<int>(run.size());
+      M.cls_run = need;
       if (M.ncls_run == M.ncls)
         M.ncls_run = -1;  // all classes: use cmeta itself
       else if (M.ncls_run > 0)
@@ -1555,6 +1557,8 @@ void instance_far_h(DevInstance& I, Index far_index, std::vector<double>& out, I
   const DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   if (far_index < 0 || far_index >= static_cast<Index>(H.blocks.far.size())) throw std::out_of_range("far index");
+  if (!M.cls_run.empty() && !M.cls_run[H.far_key[far_index]])
+    throw std::logic_error("far_h: the block's class is not instantiated on this row shard (no local far block uses it)");
   const dev::ClassMeta& cm = M.cmeta_h[H.far_key[far_index]];
   rows = cm.rl;
   cols = cm.rr;
@@ -1589,6 +1593,8 @@ void instance_class_c(DevInstance& I, Index k, std::vector<double>& out) {
   const DevMatrix& M = *I.M;
   if (!M.h2) throw std::invalid_argument("explicit C_k exists only for the H2 format");
   if (k < 0 || k >= M.ncls) throw std::out_of_range("class index");
+  if (!M.cls_run.empty() && !M.cls_run[k])
+    throw std::logic_error("class_c: the class is not instantiated on this row shard (no local far block uses it)");
   out.resize(static_cast<size_t>(M.P) * M.P);
   CK(cudaMemcpyAsync(out.data(), I.C.as<double>() + k * static_cast<std::int64_t>(M.P) * M.P,
                      out.size() * sizeof(double), cudaMemcpyDeviceToHost, M.st()));
