@@ -1562,6 +1562,208 @@ __global__ void __maxnreg__(96) k_near_tma_apply(const SymRowItem* __restrict__ 
   }
 }
 
+// K6 lean (apply alone, one RHS; the default): the same TMA ring and item
+// double-buffering as k_near_tma_apply with a quarter of its SM footprint, so
+// that the H^2 coupling (DMMA pipe) runs on the same SMs at the same time as
+// this HBM stream instead of time-sharing CTA slots with it. 4 consumer
+// warps + 1 producer warp, one CTA per SM. Chunks are up to 64 columns of one
+// block (a whole 64 x 64 block = 32 KB). Warp w owns columns 16w .. 16w + 15
+// of a chunk, lane l rows l + 32q: per column two (or four) conflict-free
+// 8-byte shared loads feed the row product (D x_tau, kept in registers across
+// the item) and the column product (D^T x_sigma); the 16 column partials of a
+// warp are reduced with one 16-step transpose-reduce (one shuffle per column
+// and lane). Fixed summation order: deterministic.
+template <int NCW>
+__device__ __forceinline__ void lean_consumers_sync() { asm volatile("bar.sync 2, %0;" ::"n"(NCW * 32) : "memory"); }
+
+template <int NQ, int NCW, int CH, int NST>
+__device__ __forceinline__ void lean_item(const SymRowItem& it, const SymBlock* __restrict__ B,
+                                          const double* __restrict__ xsi, const double* __restrict__ stages,
+                                          std::uint64_t* full, std::uint64_t* empty, const double* __restrict__ xp,
+                                          double* __restrict__ part, int& c, int warp, int lane,
+                                          double (&racc)[2][4]) {
+  constexpr int kStage = CH + 2 + 66;
+  constexpr int CPW = 64 / NCW, NHB = CPW / 8;  // columns per warp, 8-column batches
+  const int ld = it.ld, nb = it.bend - it.bbeg, jc = min(64, CH / ld);
+  double xs[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) xs[q] = xsi[lane + 32 * q];  // zero past the item's rows
+  for (int b = 0; b < nb; ++b) {
+    const std::int64_t p_col = B[b].p_col, d_off = B[b].d_off, x_col0 = B[b].x_col0;
+    const int ncol = B[b].ncol;
+    for (int j0 = 0; j0 < ncol; j0 += jc, ++c) {
+      const int slot = c % NST;
+      const int ncols = min(jc, ncol - j0);
+      mbar_wait(&full[slot], (c / NST) & 1);
+      const double* st = stages + slot * kStage;
+      const double* Dc = st + ((d_off + static_cast<std::int64_t>(j0) * ld) & 1);
+      const double* Xc = st + CH + 2 + ((reinterpret_cast<std::uintptr_t>(xp + x_col0 + j0) >> 3) & 1);
+      // two batches of 8 columns; every load of a batch is issued before its
+      // FMAs (predicated, branch-free: one consumer warp per SMSP has only
+      // instruction-level parallelism to hide shared-memory latency)
+      double cp[NHB][8];
+#pragma unroll
+      for (int hb = 0; hb < NHB; ++hb) {
+        // unpredicated loads: a column past the chunk reads the chunk's last
+        // column with x_tau = 0, rows past ld read the next column's head
+        // (finite: stages hold only D, x and the initial zeros) against
+        // x_sigma = 0, and every read stays inside the stage
+        double v[8][NQ], xt[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int j = CPW * warp + 8 * hb + jj;
+          const bool jv = j < ncols;
+          xt[jj] = jv ? Xc[j] : 0.0;
+          const double* col = Dc + (jv ? j : ncols - 1) * ld + lane;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) v[jj][q] = col[32 * q];
+        }
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            racc[hb][q] = fma(v[jj][q], xt[jj], racc[hb][q]);
+            s = fma(v[jj][q], xs[q], s);
+          }
+          cp[hb][jj] = s;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the stage
+      if (p_col >= 0 && CPW * warp < ncols) {      // warp-uniform
+        // transpose-reduce per batch: after the xor-16/8/4 steps lane l holds
+        // the partial of column (l >> 2) & 7 over a quarter of the lanes;
+        // xor 2 and 1 complete it
+#pragma unroll
+        for (int hb = 0; hb < NHB; ++hb) {
+          double* c8 = cp[hb];
+#pragma unroll
+          for (int h = 4; h >= 1; h >>= 1) {
+            const bool up = lane & (4 * h);
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+              const double keep = up ? c8[i + h] : c8[i], send = up ? c8[i] : c8[i + h];
+              c8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4 * h);
+            }
+          }
+          c8[0] += __shfl_xor_sync(0xffffffffu, c8[0], 2);
+          c8[0] += __shfl_xor_sync(0xffffffffu, c8[0], 1);
+          const int j = CPW * warp + 8 * hb + ((lane >> 2) & 7);
+          if (!(lane & 3) && j < ncols) part[p_col + j0 + j] = c8[0];
+        }
+      }
+    }
+  }
+}
+
+template <int NCW, int CH, int NST>
+__global__ void __maxnreg__(96) k_near_gemv_lean(const SymRowItem* __restrict__ items, int nitems,
+                                                                   const SymBlock* __restrict__ blocks,
+                                                                   const double* __restrict__ D,
+                                                                   const double* __restrict__ xp,
+                                                                   double* __restrict__ part,
+                                                                   int* __restrict__ counter) {
+  static_assert(CH >= 128 * 16, "a chunk holds 16 columns of a 128-row leaf");
+  constexpr int kStage = CH + 2 + 66;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) std::uint64_t full[NST], empty[NST], ifull[2], iempty[2];
+  __shared__ SymBlock bl[2][kTmaMaxBlocks];
+  __shared__ SymRowItem itm[2];
+  __shared__ int iidx[2];
+  __shared__ double xs_item[2][128];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // the consumers read whole stages unpredicated: start from finite zeros
+  for (int e = tid; e < NST * kStage + NCW * 128; e += (NCW + 1) * 32) sm[e] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the bulk copies overwrite them
+  if (tid == 0) {
+    for (int q = 0; q < NST; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], NCW);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&ifull[q], 1);
+      mbar_init(&iempty[q], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NCW) {  // ------------------------------------------------ producer
+    int c = 0;
+    for (int n = 0;; ++n) {
+      const int ib = n & 1;
+      if (n >= 2) mbar_wait(&iempty[ib], ((n >> 1) - 1) & 1);
+      int idx = 0;
+      if (lane == 0) idx = atomicAdd(counter, 1);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      if (idx < nitems) {
+        const SymRowItem it = items[idx];
+        for (int t = lane; t < it.bend - it.bbeg; t += 32) bl[ib][t] = blocks[it.bbeg + t];
+        for (int t = lane; t < 128; t += 32) xs_item[ib][t] = t < it.rows ? xp[it.x_row0 + t] : 0.0;
+        if (lane == 0) itm[ib] = it;
+      }
+      if (lane == 0) iidx[ib] = idx;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ifull[ib]);
+      if (idx >= nitems) break;
+      if (lane == 0) {
+        const SymRowItem& it = itm[ib];
+        const int ld = it.ld, nb = it.bend - it.bbeg, jc = min(64, CH / ld);
+        for (int b = 0; b < nb; ++b) {
+          const std::int64_t d_off = bl[ib][b].d_off, x_col0 = bl[ib][b].x_col0;
+          const int ncol = bl[ib][b].ncol;
+          for (int j0 = 0; j0 < ncol; j0 += jc, ++c) {
+            const int slot = c % NST;
+            if (c >= NST) mbar_wait(&empty[slot], ((c / NST) - 1) & 1);
+            const int ncols = min(jc, ncol - j0);
+            const std::int64_t e0 = d_off + static_cast<std::int64_t>(j0) * ld;
+            const std::int64_t ea = e0 & ~std::int64_t(1);
+            const std::int64_t nbytes = (((e0 + static_cast<std::int64_t>(ncols) * ld - ea) + 1) & ~std::int64_t(1)) * 8;
+            PHM_DCHECK(ld <= 128 && it.rows == ld && nbytes <= (CH + 2) * 8 && ncols <= 64);
+            const double* xsrc = xp + x_col0 + j0;
+            const int xsh = static_cast<int>((reinterpret_cast<std::uintptr_t>(xsrc) >> 3) & 1);
+            const unsigned xbytes = static_cast<unsigned>(((ncols + xsh + 1) & ~1) * 8);
+            PHM_DCHECK(xbytes <= 66 * 8);
+            mbar_expect_tx(&full[slot], static_cast<unsigned>(nbytes) + xbytes);
+            bulk_g2s(sm + slot * kStage, D + ea, static_cast<unsigned>(nbytes), &full[slot]);
+            bulk_g2s(sm + slot * kStage + CH + 2, xsrc - xsh, xbytes, &full[slot]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  double* red = sm + NST * kStage;  // NCW x 128 row partials
+  int c = 0;
+  for (int n = 0;; ++n) {
+    const int ib = n & 1;
+    mbar_wait(&ifull[ib], (n >> 1) & 1);
+    if (iidx[ib] >= nitems) break;
+    const SymRowItem it = itm[ib];
+    double racc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+    if (it.ld <= 64)
+      lean_item<2, NCW, CH, NST>(it, bl[ib], xs_item[ib], sm, full, empty, xp, part, c, warp, lane, racc);
+    else if (it.ld <= 96)
+      lean_item<3, NCW, CH, NST>(it, bl[ib], xs_item[ib], sm, full, empty, xp, part, c, warp, lane, racc);
+    else
+      lean_item<4, NCW, CH, NST>(it, bl[ib], xs_item[ib], sm, full, empty, xp, part, c, warp, lane, racc);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&iempty[ib]);  // block list and x_sigma no longer read
+    lean_consumers_sync<NCW>();                    // the previous item's reads of red are done
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[warp * 128 + lane + 32 * q] = racc[0][q] + racc[1][q];
+    lean_consumers_sync<NCW>();
+    if (tid < it.rows) {
+      double t = red[tid];
+#pragma unroll
+      for (int w = 1; w < NCW; ++w) t += red[w * 128 + tid];
+      part[it.p_row + tid] = t;
+    }
+  }
+}
+
 // K1 over TMA (instantiate alone, snapshot mode): the flat stream of
 // k_inst_flat with the slabs moved by cp.async.bulk into an NST-deep ring
 // (one producer lane, 8 consumer warps, full/empty mbarriers), persistent
@@ -2388,6 +2590,40 @@ void launch_near_tma_apply(cudaStream_t st, const SymRowItem* items, int nitems,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaMemsetAsync(counter, 0, sizeof(int), st);
+  static const int lean = [] {  // PHM_NEAR_GEMV=0: the 8-consumer-warp kernel at two CTAs per SM
+    const char* e = std::getenv("PHM_NEAR_GEMV");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (lean) {
+    // one CTA per SM (a quarter of the SM's registers): the coupling's CTAs
+    // fill the rest of every SM while this stream runs
+    constexpr int LCH = 4096;
+    static const int lnst = [] {  // ring depth: 3 (two CTAs of the coupling beside it fit in 3, four in 2)
+      const char* e = std::getenv("PHM_NEAR_LEAN_NST");
+      const int k = e ? std::atoi(e) : 2;
+      return k == 2 || k == 4 ? k : 3;
+    }();
+    static const int lwarps = [] {  // consumer warps per CTA
+      const char* e = std::getenv("PHM_NEAR_LEAN_WARPS");
+      const int k = e ? std::atoi(e) : 4;
+      return k == 8 ? 8 : 4;
+    }();
+    static const int lean_per_sm = [] {
+      const char* e = std::getenv("PHM_NEAR_LEAN_PER_SM");
+      const int k = e ? std::atoi(e) : 2;
+      return k >= 1 && k <= 2 ? k : 1;
+    }();
+    const int grid = std::min(nitems, sms * lean_per_sm);
+#define PHM_LEAN(WW, NN)                                                                                    \
+  if (lnst == NN && lwarps == WW) {                                                                         \
+    const size_t lsmem = static_cast<size_t>(NN * (LCH + 2 + 66) + WW * 128) * sizeof(double);             \
+    smem_attr(reinterpret_cast<const void*>(k_near_gemv_lean<WW, LCH, NN>), static_cast<int>(lsmem), true); \
+    k_near_gemv_lean<WW, LCH, NN><<<grid, (WW + 1) * 32, lsmem, st>>>(items, nitems, blocks, D, xp, part, counter); \
+  }
+    PHM_LEAN(4, 2) PHM_LEAN(4, 3) PHM_LEAN(4, 4) PHM_LEAN(8, 2) PHM_LEAN(8, 3) PHM_LEAN(8, 4)
+#undef PHM_LEAN
+    return;
+  }
   const int grid = std::min(nitems, sms * per_sm);
   k_near_tma_apply<CH, NST><<<grid, kTmaThreads, smem, st>>>(items, nitems, blocks, D, xp, part, counter);
 }

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--rhs", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--save", default=None, help="np.save y (tree of the last apply) here")
     a = ap.parse_args()
     import torch
 
@@ -57,6 +58,8 @@ def main():
         t, cnt = ctx.timer(name)
         if cnt:
             kern[name] = round(t / a.steps, 4)
+    if a.save:
+        np.save(a.save, y.cpu().numpy())
     info = pm.info()
     print(json.dumps({"config": a.config, "rhs": m, "apply_ms": ms, "near_stored": info["near_stored"],
                       "kernels_ms_per_apply": kern}))
