@@ -41,7 +41,7 @@ CONFIGS = {
     # BASELINE.json configs[4] (C5): the C3 matrix, 4096 thetas sharded over
     # GPUs with no communication, each instantiated and applied to 10 vectors
     "c5": dict(n=262144, d=3, family="e", box=(0.05, 0.5), l_max=4, p_s=4, p_theta=8, eta=1.0, fmt="h2",
-               points="uniform", sweep=True, rhs=10, n_theta=4096, theta_batch=8),
+               points="uniform", sweep=True, rhs=10, n_theta=4096, theta_batch=16),
     # BASELINE.json configs[3] (C4, the 8-GPU DMMA case): n = 2^20 points from
     # a 16-Gaussian mixture, leaf 32, Matern-5/2 with theta = (l, sigma^2) on
     # an 8 x 6 grid, 64 right-hand sides. Fits 8 x B200 only with symmetric

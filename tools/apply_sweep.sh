@@ -9,7 +9,7 @@ run() {  # tag env...
   env "$@" timeout 600 python tools/apply_probe.py --save $out/y_$tag.npy $PROBE_ARGS > $out/$tag.json 2> $out/$tag.err
   echo "$tag $(cat $out/$tag.json | tail -1)"
 }
-run old PHM_NEAR_GEMV=0
+run old ${BASE_ENV:-PHM_NEAR_GEMV=0}
 while [ $# -gt 0 ]; do
   tag=$1; shift; envs=$1; shift
   run $tag $envs
