@@ -847,7 +847,13 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
       std::size_t total = 0;
       for (const auto& o : owned) total += o.size();
       const std::size_t target = 8 * 2 * 148;
-      kItemBlocks = std::min<std::size_t>(dev::kTmaMaxBlocks, std::max<std::size_t>(8, (total + target - 1) / target));
+      static const std::size_t floor_blocks = [] {  // tuning: smallest item run
+        const char* e = std::getenv("PHM_ITEM_MIN_BLOCKS");
+        const int k = e ? std::atoi(e) : 8;
+        return static_cast<std::size_t>(k >= 1 && k <= dev::kTmaMaxBlocks ? k : 8);
+      }();
+      kItemBlocks = std::min<std::size_t>(dev::kTmaMaxBlocks,
+                                          std::max<std::size_t>(floor_blocks, (total + target - 1) / target));
     }
     for (int s = 0; s < M.nnodes; ++s) {
       if (owned[s].empty()) continue;
@@ -884,6 +890,24 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
         poff += it.rows;
         items.push_back(it);
       }
+    }
+    // Longest items first (stable): the near passes take items in index
+    // order (one CTA per item, or a work counter), so the last wave is made
+    // of the shortest items instead of whichever leaves come last in tree
+    // order. Each item writes fixed partial segments: the order changes no
+    // result.
+    static const bool lpt = [] {
+      const char* e = std::getenv("PHM_ITEM_ORDER");
+      return !(e && std::atoi(e) == 0);
+    }();
+    if (lpt) {
+      auto work = [&](const dev::SymRowItem& it) {
+        std::int64_t w = 0;
+        for (int b = it.bbeg; b < it.bend; ++b) w += blocks[b].ncol;
+        return w * it.rows;
+      };
+      std::stable_sort(items.begin(), items.end(),
+                       [&](const dev::SymRowItem& a, const dev::SymRowItem& b) { return work(a) > work(b); });
     }
     upload(M.sym_blocks, blocks, st);
     std::vector<std::int64_t> lrow0;
