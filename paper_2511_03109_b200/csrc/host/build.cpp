@@ -244,11 +244,17 @@ std::unique_ptr<HostMatrix> build_host(const double* points, Index n, int d, con
   M.grids = make_theta_grids(cfg.spec, cfg.p_theta);
   M.stats.tree_s = now_s() - t0;
 
-  // Row sharding: contiguous leaf ranges balanced by near-field entries.
+  // Row sharding: contiguous leaf ranges balanced by the near-field entries
+  // each rank streams. With symmetric snapshot storage a rank streams the
+  // pairs whose owner leaf it holds (device.cu's parity rule), so only
+  // owned pairs count; otherwise every block of the leaf's rows.
   {
+    const bool sym = cfg.near_mode == NearMode::Snapshot && cfg.symmetric_near;
     std::vector<double> leaf_work(T.nodes.size(), 0.0);
-    for (const Block& b : M.blocks.near)
+    for (const Block& b : M.blocks.near) {
+      if (sym && b.sigma != b.tau && (b.sigma < b.tau) != (((b.sigma + b.tau) & 1) == 0)) continue;
       leaf_work[b.sigma] += static_cast<double>(T.nodes[b.sigma].count) * static_cast<double>(T.nodes[b.tau].count);
+    }
     std::vector<int> leaves;
     double total = 0.0;
     for (size_t id = 0; id < T.nodes.size(); ++id)
