@@ -679,3 +679,52 @@ def test_two_matrices_on_one_context_from_two_threads(ph, po):
     for t in ts:
         t.join()
     assert not errs
+
+
+_NEAR_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2511_03109_b200 as ph
+from oracle import pyoracle as po
+pts = ph.generate_points(12000, 3, 23)
+cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=3, p_s=4, p_theta=8, eta=1.0,
+                  near_mode=ph.NearMode.SNAPSHOT)
+pm = ph.offline_h2(pts, cfg)
+inst = ph.instantiate(pm, [0.21])
+x = ph.generate_normal(12000, 3)
+ys = [inst.apply(x) for _ in range(3)] + [inst.instantiate_apply([0.21], x)]
+ref = po.from_product(pm, pts).instantiate([0.21]).apply(x)
+np.save(sys.argv[2], np.stack(ys + [ref]))
+"""
+
+
+@pytest.mark.gpu
+def test_near_gemv_kernels_and_item_order(ph, tmp_path):
+    """apply's near GEMV: the lean kernel (default; 4 consumer warps, two
+    CTAs per SM beside the coupling) and the 8-warp kernel
+    (PHM_NEAR_GEMV=0) both match the oracle to 1e-13 and each other to
+    rounding; the longest-first item order (PHM_ITEM_ORDER=0 turns it off)
+    changes no bit of y, since every item writes fixed partial segments;
+    repeated applies (direct, captured, replayed) are bitwise equal."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "near.py"
+    script.write_text(_NEAR_SCRIPT)
+    outs = {}
+    for tag, env in (("lean", {}), ("old", {"PHM_NEAR_GEMV": "0"}), ("unordered", {"PHM_ITEM_ORDER": "0"}),
+                     ("lean1", {"PHM_NEAR_LEAN_PER_SM": "1", "PHM_NEAR_LEAN_NST": "3"})):
+        out = tmp_path / f"{tag}.npy"
+        subprocess.run([sys.executable, str(script), root, str(out)], check=True, timeout=600,
+                       env={**os.environ, **env})
+        outs[tag] = np.load(out)
+    for tag, ys in outs.items():
+        ref = ys[-1]
+        assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2]), tag
+        for y in ys[:4]:
+            assert rel(y, ref) <= 1e-13, tag
+    assert np.array_equal(outs["lean"][:4], outs["unordered"][:4])
+    assert np.array_equal(outs["lean"][:3], outs["lean1"][:3])  # same kernel, one CTA per SM
+    assert rel(outs["lean"][0], outs["old"][0]) <= 1e-14

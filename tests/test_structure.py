@@ -127,3 +127,42 @@ def test_metrics_relations(ph, po):
     assert mh["c_sp"] <= 216 and mh["rank"] >= 1.0
     assert 0 < mh2["coupling_ratio"] < mh2["ff_ratio"]
     assert mh["storage_gb"] == pytest.approx(mh["storage_entries"] * 8.0 / 1e9)
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_row_shards_balance_streamed_entries(ph, world):
+    """Row shards are contiguous leaf ranges balanced by the near entries each
+    rank streams: with symmetric snapshot storage a rank streams the pairs
+    whose owner leaf it holds (owner of {a, b}, a < b: a when a + b is even,
+    else b -- device.cu), each once. Every rank's share is within a few
+    leaves' worth of the mean, and the ranges tile the rows."""
+    pts = ph.generate_points(40000, 3, 2)
+    spec = ph.KernelSpec(ph.Family.E, [(0.05, 0.5)])
+    shares, ranges = [], []
+    for r in range(world):
+        cfg = ph.PHConfig(spec=spec, l_max=3, p_s=4, p_theta=8, eta=1.0, near_mode=ph.NearMode.SNAPSHOT,
+                          shard_rank=r, shard_count=world)
+        pm = ph.offline_structure(pts, cfg)
+        info = pm.info()
+        ints, _ = pm.nodes()
+        near, _, _ = pm.blocks()
+        lo, hi = info["row_begin"], info["row_end"]
+        ranges.append((lo, hi))
+        count = ints[:, 3]
+        # leaves own contiguous row ranges in leaf-id order (perm)
+        begin = np.full(len(ints), -1, dtype=np.int64)
+        leaves = np.flatnonzero(ints[:, 2] < 0)
+        begin[leaves] = np.concatenate([[0], np.cumsum(count[leaves])[:-1]])
+        w = 0
+        for s, t in near:
+            if not (lo <= begin[s] < hi):
+                continue
+            if s != t and (s < t) != ((s + t) % 2 == 0):
+                continue  # stored by the partner leaf
+            w += int(count[s]) * int(count[t])
+        shares.append(w)
+    assert ranges[0][0] == 0 and ranges[-1][1] == 40000
+    assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
+    mean = sum(shares) / world
+    leaf_max = max(shares) / (512 // world)  # ~leaves per rank at l_max 3
+    assert max(abs(s - mean) for s in shares) <= 2 * leaf_max, shares

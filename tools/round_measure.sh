@@ -26,7 +26,7 @@ for k in k_near_tma k_coupling_mma k_class_inst; do
   ncu --set full --import-source on --clock-control none -k "regex:${k}\b" -c 1 -o $out/c3_full_$k -f \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $out/c3_full_$k.log 2>&1
 done
-for k in k_near_tma_apply k_coupling_mma; do
+for k in k_near_gemv_lean k_coupling_mma; do
   ncu --set full --import-source on --clock-control none -k "regex:${k}\b" --launch-skip 3 -c 1 -o $out/apply_full_$k -f \
     python tools/apply_probe.py --steps 2 > $out/apply_full_$k.log 2>&1
 done
@@ -52,5 +52,8 @@ PY
   rm -f ${r%.ncu-rep}_sass.csv
   [ $(stat -c %s $r) -gt 6000000 ] && rm -f $r
 done
+# per-rank cost of the sharded step (C3 at 2/4/8 shards; C4 rank 0 of 8)
+timeout 900 python tools/shard_probe.py --n-shards 2 4 8 --ranks 0 -1 > $out/shard_probe_c3.txt 2>&1
+timeout 1500 python tools/shard_probe.py --config c4 --n-shards 8 --ranks 0 --steps 5 > $out/shard_probe_c4.txt 2>&1
 du -sh $out
 echo done
