@@ -2597,11 +2597,15 @@ void launch_near_tma_apply(cudaStream_t st, const SymRowItem* items, int nitems,
   if (lean) {
     // one CTA per SM (a quarter of the SM's registers): the coupling's CTAs
     // fill the rest of every SM while this stream runs
-    constexpr int LCH = 4096;
-    static const int lnst = [] {  // ring depth: 3 (two CTAs of the coupling beside it fit in 3, four in 2)
+    static const int lnst = [] {  // ring depth (two stages: room for the coupling's CTAs)
       const char* e = std::getenv("PHM_NEAR_LEAN_NST");
       const int k = e ? std::atoi(e) : 2;
-      return k == 2 || k == 4 ? k : 3;
+      return k == 3 || k == 4 ? k : 2;
+    }();
+    static const int lch = [] {  // chunk doubles: 4096 = a whole 64 x 64 block
+      const char* e = std::getenv("PHM_NEAR_LEAN_CH");
+      const int k = e ? std::atoi(e) : 4096;
+      return k == 3072 ? 3072 : 4096;
     }();
     static const int lwarps = [] {  // consumer warps per CTA
       const char* e = std::getenv("PHM_NEAR_LEAN_WARPS");
@@ -2614,14 +2618,21 @@ void launch_near_tma_apply(cudaStream_t st, const SymRowItem* items, int nitems,
       return k >= 1 && k <= 2 ? k : 1;
     }();
     const int grid = std::min(nitems, sms * lean_per_sm);
-#define PHM_LEAN(WW, NN)                                                                                    \
-  if (lnst == NN && lwarps == WW) {                                                                         \
+#define PHM_LEAN(WW, LCH, NN)                                                                               \
+  if (lnst == NN && lwarps == WW && lch == LCH) {                                                           \
     const size_t lsmem = static_cast<size_t>(NN * (LCH + 2 + 66) + WW * 128) * sizeof(double);             \
     smem_attr(reinterpret_cast<const void*>(k_near_gemv_lean<WW, LCH, NN>), static_cast<int>(lsmem), true); \
     k_near_gemv_lean<WW, LCH, NN><<<grid, (WW + 1) * 32, lsmem, st>>>(items, nitems, blocks, D, xp, part, counter); \
+    return;                                                                                                 \
   }
-    PHM_LEAN(4, 2) PHM_LEAN(4, 3) PHM_LEAN(4, 4) PHM_LEAN(8, 2) PHM_LEAN(8, 3) PHM_LEAN(8, 4)
+    PHM_LEAN(4, 4096, 2) PHM_LEAN(4, 3072, 2) PHM_LEAN(4, 4096, 3) PHM_LEAN(4, 3072, 3) PHM_LEAN(4, 4096, 4)
+    PHM_LEAN(8, 4096, 2) PHM_LEAN(8, 4096, 3) PHM_LEAN(8, 4096, 4)
 #undef PHM_LEAN
+    {  // any other PHM_NEAR_LEAN_* combination: the default kernel
+      const size_t lsmem = static_cast<size_t>(2 * (4096 + 2 + 66) + 4 * 128) * sizeof(double);
+      smem_attr(reinterpret_cast<const void*>(k_near_gemv_lean<4, 4096, 2>), static_cast<int>(lsmem), true);
+      k_near_gemv_lean<4, 4096, 2><<<grid, 5 * 32, lsmem, st>>>(items, nitems, blocks, D, xp, part, counter);
+    }
     return;
   }
   const int grid = std::min(nitems, sms * per_sm);
