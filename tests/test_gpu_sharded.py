@@ -91,6 +91,11 @@ def _worker(rank, world, port, fmt, sym, q):
             ref = ph.instantiate(full, th)
             errs.append(rel(inst.instantiate_apply_sharded(comm, th, x), ref.apply(x)))
             errs.append(rel(inst.instantiate_apply_sharded(comm, th, X), ref.apply(X)))
+        # above 32 RHS a symmetric shard runs the one-sided K9 for its own
+        # rows plus Z-only products for partner rows on the other rank
+        X40 = np.stack([ph.generate_normal(4000, 10 + j) for j in range(40)], axis=1)
+        ref = ph.instantiate(full, [0.47])  # same theta as the last step: apply_sharded below reuses it
+        errs.append(rel(inst.instantiate_apply_sharded(comm, [0.47], X40), ref.apply(X40)))
         xd = torch.from_numpy(x).cuda()
         yd = torch.zeros(4000, dtype=torch.float64, device="cuda")
         inst.apply_sharded_device(comm, xd.data_ptr(), yd.data_ptr(), 1)
