@@ -49,6 +49,11 @@ CONFIGS = {
     # rank); run under torchrun --nproc-per-node 8.
     "c4": dict(n=1048576, d=3, family="m52", box=(0.05, 0.5), boxes=[(0.05, 0.5), (0.5, 2.0)], amplitude=True,
                l_max=5, p_s=4, p_theta=[8, 6], eta=1.0, fmt="h2", points="mixture", rhs=64),
+    # profiling proxy of C4's near field on one GPU (not a BASELINE config):
+    # the same mixture and kernel at n = 2^18, l_max 4 -- clustered leaves of
+    # up to a few thousand rows, as in C4 -- small enough for ncu replays
+    "c4p": dict(n=262144, d=3, family="m52", box=(0.05, 0.5), boxes=[(0.05, 0.5), (0.5, 2.0)], amplitude=True,
+                l_max=4, p_s=4, p_theta=[8, 6], eta=1.0, fmt="h2", points="mixture", rhs=64),
 }
 
 
