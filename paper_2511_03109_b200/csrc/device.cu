@@ -34,7 +34,7 @@ void launch_snapshot(cudaStream_t, const SnapTile*, std::int64_t, const BlockGeo
                      int, int, const double*, double, double*);
 void launch_inst_flat(cudaStream_t, const double*, std::int64_t, int, const double*, double*);
 bool launch_inst_flat_batch(cudaStream_t, const double*, std::int64_t, int, int, const InstPtrs&);
-bool launch_inst_tma(cudaStream_t, const double*, std::int64_t, int, int, const InstPtrs&);
+bool launch_inst_tma(cudaStream_t, const double*, std::int64_t, int, int, const InstPtrs&, int per_sm = 2);
 void launch_inst_tiles(cudaStream_t, const InstTile*, std::int64_t, const double*, const double*, double*);
 void launch_near_w(cudaStream_t, const NearW*, std::int64_t, const double*, const std::int32_t*, const ThetaParams*,
                    double*);
@@ -46,6 +46,9 @@ void launch_class_inst(cudaStream_t, const ClassMeta*, int, const double*, const
                        const double*, const ThetaParams*, int, bool, int, int, int, int, double*, double*);
 void launch_gather(cudaStream_t, const double*, const std::int32_t*, std::int64_t, std::int64_t, double*);
 void launch_scatter(cudaStream_t, const double*, const std::int32_t*, std::int64_t, std::int64_t, double*);
+void launch_leaf_fwd_chunks(cudaStream_t, const LeafChunk*, int, const std::int32_t*, const std::int64_t*,
+                            const std::int32_t*, int, const std::int64_t*, const std::int32_t*, const double*,
+                            std::int64_t, int, int, const double*, int, double*, double*);
 void launch_leaf_fwd(cudaStream_t, const std::int32_t*, int, const std::int64_t*, const std::int32_t*, const double*,
                      std::int64_t, int, int, int, const double*, int, double*);
 void launch_up(cudaStream_t, const std::int32_t*, int, const std::int32_t*, const std::int32_t*, const double*, int,
@@ -405,6 +408,14 @@ struct DevMatrix {
   DBuf U, Etr;
   DBuf leaves_all, leaves_local;
   int n_leaves_all = 0, n_leaves_local = 0;
+  // split leaf forward pass (K3, m >= 4): per list (0 all, 1 local) the leaves
+  // of at most kLeafChunk points, the chunks of the bigger ones and their
+  // ordered reduction
+  struct LeafPlan {
+    DBuf small, chunks, red_leaf, red_slot, red_n;
+    int n_small = 0, n_chunks = 0, n_red = 0;
+  } lf[2];
+  DBuf lf_part;
   std::vector<std::pair<int, int>> up_range, down_range;  // per level into level_nodes arrays
   DBuf up_nodes, down_nodes;
   // sharded forward pass with an x-hat exchange: upward lists restricted to
@@ -1228,6 +1239,34 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     M.n_leaves_local = static_cast<int>(lloc.size());
     upload(M.leaves_all, lall, st);
     upload(M.leaves_local, lloc, st);
+    for (int li = 0; li < 2; ++li) {
+      const auto& lst = li == 0 ? lall : lloc;
+      std::vector<std::int32_t> small, rleaf, rn;
+      std::vector<dev::LeafChunk> ch;
+      std::vector<std::int64_t> rslot;
+      for (std::int32_t leaf : lst) {
+        const int cnt = static_cast<int>(T.nodes[leaf].count);
+        if (cnt <= dev::kLeafChunk) {
+          small.push_back(leaf);
+          continue;
+        }
+        rleaf.push_back(leaf);
+        rslot.push_back(static_cast<std::int64_t>(ch.size()));
+        int k = 0;
+        for (int p0 = 0; p0 < cnt; p0 += dev::kLeafChunk, ++k)
+          ch.push_back({leaf, p0, std::min(dev::kLeafChunk, cnt - p0), 0, static_cast<std::int64_t>(ch.size())});
+        rn.push_back(k);
+      }
+      auto& L = M.lf[li];
+      L.n_small = static_cast<int>(small.size());
+      L.n_chunks = static_cast<int>(ch.size());
+      L.n_red = static_cast<int>(rleaf.size());
+      upload(L.small, small, st);
+      upload(L.chunks, ch, st);
+      upload(L.red_leaf, rleaf, st);
+      upload(L.red_slot, rslot, st);
+      upload(L.red_n, rn, st);
+    }
     // level lists: upward = internal non-empty nodes per level (all);
     // downward = non-empty local non-root nodes per level
     std::vector<std::int32_t> upn, dnn, upl;
@@ -1372,7 +1411,12 @@ bool k1_tma() {
 }
 
 // Near stage of instantiate: every stored D_b(theta) (K1).
-void inst_near(DevInstance& I, const double* theta, cudaStream_t s, StageCounters* counters) {
+// k1_per_sm: CTAs per SM of the TMA K1 stream -- 1 when the far chain runs
+// beside it on the side stream (instantiate + block apply), so the class
+// stage, the leaf forward pass and the coupling get SM room during K1
+// instead of queueing behind its persistent grid (C4 rank 0 of 8: 71.3 vs
+// 74.2 ms per step)
+void inst_near(DevInstance& I, const double* theta, cudaStream_t s, StageCounters* counters, int k1_per_sm = 2) {
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   Context& ctx = *M.ctx;
@@ -1385,7 +1429,7 @@ void inst_near(DevInstance& I, const double* theta, cudaStream_t s, StageCounter
       // the TMA ring pays off on large snapshot sets; small ones (C1: 160 MB)
       // run faster as the plain 256-bit stream
       const bool big = static_cast<double>(M.E) * M.R_snap * 8.0 > 1e9;
-      if (!big || !k1_tma() || !dev::launch_inst_tma(s, M.G.as<double>(), M.E, M.R_snap, 1, tab))
+      if (!big || !k1_tma() || !dev::launch_inst_tma(s, M.G.as<double>(), M.E, M.R_snap, 1, tab, k1_per_sm))
         dev::launch_inst_flat(s, M.G.as<double>(), M.E, M.R_snap, I.w.as<double>(), I.D.as<double>());
     });
   } else if (M.mode == NearMode::TT) {
@@ -1649,12 +1693,31 @@ void far_chain(DevInstance& I, Index m, cudaStream_t fs, int coupling_ctas, Comm
   const bool split = ex != nullptr && M.sharded && split_env;
   if (split)
     ctx.run_on(fs, "zero", [&] { dev::launch_zero(fs, M.xhat.as<double>(), static_cast<std::int64_t>(M.nnodes) * P * m); });
-  ctx.run_on(fs, "leaf_fwd", [&] {
-    dev::launch_leaf_fwd(fs, (split ? M.leaves_local : M.leaves_all).as<std::int32_t>(),
-                         split ? M.n_leaves_local : M.n_leaves_all, M.node_begin.as<std::int64_t>(),
-                         M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, P, M.xp.as<double>(), mm,
-                         M.xhat.as<double>());
-  });
+  const auto& LP = M.lf[split ? 1 : 0];
+  if (LP.n_chunks > 0 && P == 64 && m >= 4 && M.d * M.ps <= 48) {
+    // big (clustered) leaves split into chunks of kLeafChunk points
+    const size_t need = sizeof(double) * LP.n_chunks * m * P;
+    if (M.lf_part.bytes < need) {
+      M.lf_part.alloc(need);
+      ++M.ws_gen;  // captured graphs hold the old pointer
+    }
+    ctx.run_on(fs, "leaf_fwd", [&] {
+      dev::launch_leaf_fwd_chunks(fs, LP.chunks.as<dev::LeafChunk>(), LP.n_chunks, LP.red_leaf.as<std::int32_t>(),
+                                  LP.red_slot.as<std::int64_t>(), LP.red_n.as<std::int32_t>(), LP.n_red,
+                                  M.node_begin.as<std::int64_t>(), M.node_count.as<std::int32_t>(), M.U.as<double>(),
+                                  M.n, M.d, M.ps, M.xp.as<double>(), mm, M.lf_part.as<double>(), M.xhat.as<double>());
+      dev::launch_leaf_fwd(fs, LP.small.as<std::int32_t>(), LP.n_small, M.node_begin.as<std::int64_t>(),
+                           M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, P, M.xp.as<double>(),
+                           mm, M.xhat.as<double>());
+    });
+  } else {
+    ctx.run_on(fs, "leaf_fwd", [&] {
+      dev::launch_leaf_fwd(fs, (split ? M.leaves_local : M.leaves_all).as<std::int32_t>(),
+                           split ? M.n_leaves_local : M.n_leaves_all, M.node_begin.as<std::int64_t>(),
+                           M.node_count.as<std::int32_t>(), M.U.as<double>(), M.n, M.d, M.ps, P, M.xp.as<double>(),
+                           mm, M.xhat.as<double>());
+    });
+  }
   for (int l = H.tree->l_max - 1; l >= 0; --l) {
     const auto r = split ? M.upl_range[l] : M.up_range[l];
     if (r.second == r.first) continue;
@@ -2026,7 +2089,7 @@ void instantiate_apply_sequence(DevInstance& I, const double* x_dev, Index m, St
     }
   }
   if (!fused) {
-    inst_near(I, nullptr, st, counters);
+    inst_near(I, nullptr, st, counters, M.h2 ? 1 : 2);
     CK(cudaStreamWaitEvent(st, ctx.aux_ev, 0));  // xp gathered
     near_product(I, m, st);
   }

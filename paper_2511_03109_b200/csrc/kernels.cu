@@ -535,18 +535,24 @@ __global__ void k_scatter(const double* __restrict__ yp, const std::int32_t* __r
 // once for all of them, and the factor rows are staged once per leaf instead
 // of once per column. Products and sums run in k_leaf_fwd's order, so every
 // column equals the single-vector result bit for bit.
+// chunks (non-null): CTA x takes points [p0, p0 + len) of leaf `leaf` and
+// writes its partial x-hat to xhat + slot (m x P); a leaf of more than
+// kLeafChunk points is split this way (k_leaf_fwd_reduce sums the chunks in
+// order), so a clustered leaf of thousands of points is not one CTA's
+// serial loop.
 template <int MC>
 __global__ void __launch_bounds__(256) k_leaf_fwd_m(const std::int32_t* __restrict__ leaves,
                                                     const std::int64_t* __restrict__ begin,
                                                     const std::int32_t* __restrict__ count,
                                                     const double* __restrict__ U, std::int64_t n, int d, int ps,
-                                                    const double* __restrict__ xp, int m, double* __restrict__ xhat) {
+                                                    const double* __restrict__ xp, int m, double* __restrict__ xhat,
+                                                    const LeafChunk* __restrict__ chunks = nullptr) {
   constexpr int P = 64, CH = 32;
   __shared__ double su[CH * 3 * 16];  // CH points x d x ps (d * ps <= 48)
   __shared__ double sx[CH * 4 * MC];  // CH points x the tile's columns
-  const int leaf = leaves[blockIdx.x];
-  const std::int64_t b0 = begin[leaf];
-  const int cnt = count[leaf];
+  const int leaf = chunks ? chunks[blockIdx.x].leaf : leaves[blockIdx.x];
+  const std::int64_t b0 = begin[leaf] + (chunks ? chunks[blockIdx.x].p0 : 0);
+  const int cnt = chunks ? chunks[blockIdx.x].len : count[leaf];
   const int c0 = blockIdx.y * 4 * MC;
   const int ncol = min(4 * MC, m - c0);
   const int a = threadIdx.x & 63, cg = threadIdx.x >> 6;
@@ -592,7 +598,25 @@ __global__ void __launch_bounds__(256) k_leaf_fwd_m(const std::int32_t* __restri
 #pragma unroll
   for (int j = 0; j < MC; ++j) {
     const int c = cg + 4 * j;
-    if (c < ncol) xhat[(static_cast<std::int64_t>(leaf) * m + c0 + c) * P + a] = acc[j];
+    if (c < ncol) {
+      if (chunks)
+        xhat[(chunks[blockIdx.x].slot * m + c0 + c) * P + a] = acc[j];
+      else
+        xhat[(static_cast<std::int64_t>(leaf) * m + c0 + c) * P + a] = acc[j];
+    }
+  }
+}
+
+// x-hat of a split leaf: the sum of its chunk partials in chunk order.
+__global__ void k_leaf_fwd_reduce(const std::int32_t* __restrict__ red_leaf, const std::int64_t* __restrict__ red_slot,
+                                  const std::int32_t* __restrict__ red_n, int P, int m, const double* __restrict__ part,
+                                  double* __restrict__ xhat) {
+  const int r = blockIdx.x, leaf = red_leaf[r], ns = red_n[r];
+  const std::int64_t s0 = red_slot[r] * m * P;
+  for (int e = threadIdx.x; e < m * P; e += blockDim.x) {
+    double t = part[s0 + e];
+    for (int q = 1; q < ns; ++q) t += part[s0 + static_cast<std::int64_t>(q) * m * P + e];
+    xhat[static_cast<std::int64_t>(leaf) * m * P + e] = t;
   }
 }
 
@@ -2444,19 +2468,24 @@ bool launch_inst_flat_batch(cudaStream_t st, const double* G, std::int64_t E, in
     default: return false;
   }
 }
-bool launch_inst_tma(cudaStream_t st, const double* G, std::int64_t E, int R, int B, const InstPtrs& tab) {
+bool launch_inst_tma(cudaStream_t st, const double* G, std::int64_t E, int R, int B, const InstPtrs& tab, int per_sm) {
   if (E == 0) return true;
   if (B < 1 || B > kInstBatchMax) return false;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static const int k1_env = [] {  // A/B override of the caller's choice
+    const char* e = std::getenv("PHM_K1_TMA_PER_SM");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int k1_per_sm = k1_env == 1 || k1_env == 2 ? k1_env : (per_sm == 1 ? 1 : 2);
 #define PHM_K1T(RR)                                                                                           \
   case RR: {                                                                                                  \
     constexpr int CH = ((5120 / RR) & ~63) < 256 ? 256 : (((5120 / RR) & ~63) > 1024 ? 1024 : ((5120 / RR) & ~63)); \
     constexpr int NST = 2;                                                                                    \
     const size_t smem = static_cast<size_t>(NST * RR * CH) * sizeof(double);                                 \
     smem_attr(reinterpret_cast<const void*>(k_inst_tma<RR, CH, NST>), static_cast<int>(smem), true);          \
-    const int grid = static_cast<int>(std::min<std::int64_t>((E + CH - 1) / CH, 2 * sms));                   \
+    const int grid = static_cast<int>(std::min<std::int64_t>((E + CH - 1) / CH, k1_per_sm * sms));           \
     k_inst_tma<RR, CH, NST><<<grid, kTmaThreads, smem, st>>>(G, E, B, tab);                                   \
     return true;                                                                                              \
   }
@@ -2559,6 +2588,21 @@ void launch_leaf_fwd(cudaStream_t st, const std::int32_t* leaves, int nleaves, c
   const size_t smem = (64 * d * ps + 64) * sizeof(double);
   if (smem > 48 * 1024) smem_attr(reinterpret_cast<const void*>(k_leaf_fwd), static_cast<int>(smem), false);
   k_leaf_fwd<<<dim3(nleaves, m), threads_for(P), smem, st>>>(leaves, begin, count, U, n, d, ps, P, xp, m, xhat);
+}
+// The big leaves of a list (more than kLeafChunk points, m >= 4, P = 64):
+// chunk partials, then the ordered sum per leaf.
+void launch_leaf_fwd_chunks(cudaStream_t st, const LeafChunk* chunks, int nchunks, const std::int32_t* red_leaf,
+                            const std::int64_t* red_slot, const std::int32_t* red_n, int nred,
+                            const std::int64_t* begin, const std::int32_t* count, const double* U, std::int64_t n,
+                            int d, int ps, const double* xp, int m, double* part, double* xhat) {
+  if (nchunks == 0) return;
+  if (m <= 16)
+    k_leaf_fwd_m<4><<<dim3(nchunks, (m + 15) / 16), 256, 0, st>>>(nullptr, begin, count, U, n, d, ps, xp, m, part,
+                                                                   chunks);
+  else
+    k_leaf_fwd_m<16><<<dim3(nchunks, (m + 63) / 64), 256, 0, st>>>(nullptr, begin, count, U, n, d, ps, xp, m, part,
+                                                                    chunks);
+  k_leaf_fwd_reduce<<<nred, 256, 0, st>>>(red_leaf, red_slot, red_n, 64, m, part, xhat);
 }
 void launch_up(cudaStream_t st, const std::int32_t* nodes, int cnt, const std::int32_t* first_child,
                const std::int32_t* count, const double* E, int d, int ps, int P, int m, double* xhat) {

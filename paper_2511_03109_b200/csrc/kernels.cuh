@@ -84,6 +84,14 @@ struct ClassMeta {
 // same child parity (so their far partners share translation classes); an
 // item is a contiguous range of that group's classes. cls_tau[e*32 + slot] is
 // the tau node of (sigma slot, class item_cls[e]) or -1.
+// Chunk of a leaf for the split leaf forward pass (K3): points [p0, p0 + len)
+// of `leaf`, partial x-hat at chunk ordinal `slot` (m x P doubles each).
+constexpr int kLeafChunk = 256;
+struct LeafChunk {
+  std::int32_t leaf, p0, len, pad;
+  std::int64_t slot;
+};
+
 constexpr int kGroupSlots = 32;
 struct CouplingItem {
   std::int32_t group, e_begin, e_end, pad;

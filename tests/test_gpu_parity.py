@@ -728,3 +728,26 @@ def test_near_gemv_kernels_and_item_order(ph, tmp_path):
     assert np.array_equal(outs["lean"][:4], outs["unordered"][:4])
     assert np.array_equal(outs["lean"][:3], outs["lean1"][:3])  # same kernel, one CTA per SM
     assert rel(outs["lean"][0], outs["old"][0]) <= 1e-14
+
+
+@pytest.mark.gpu
+def test_split_leaf_forward_big_clustered_leaves(ph, po):
+    """Leaves of more than kLeafChunk (256) points -- clustered points at a
+    shallow l_max -- run the leaf forward pass split into chunks with an
+    ordered per-leaf sum (K3 for m >= 4); y of block right-hand sides matches
+    the oracle and the column-by-column apply, and repeats bitwise."""
+    pts = ph.generate_mixture_points(12000, 3, 16, 0.05, 3)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT)
+    pm = ph.offline_h2(pts, cfg)
+    sizes = _node_sizes(pm)
+    ints, _ = pm.nodes()
+    assert sizes[ints[:, 2] < 0].max() > 256  # the split path is exercised
+    om = po.from_product(pm, pts)
+    inst = ph.instantiate(pm, [0.19])
+    for m in (6, 24):
+        X = np.stack([ph.generate_normal(12000, 40 + j) for j in range(m)], axis=1)
+        Y = inst.apply(X)
+        assert np.array_equal(Y, inst.apply(X))
+        assert rel(Y, om.instantiate([0.19]).apply(X)) <= 1e-12
+        assert rel(Y[:, 1], inst.apply(X[:, 1])) <= 1e-13
