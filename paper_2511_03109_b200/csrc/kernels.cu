@@ -1257,6 +1257,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// The same bulk copy with an L2 evict-first policy: a stream read once
+// (apply's D) should not push out the L2-resident operands of kernels running
+// beside it (the coupling's C_k, 83 MB at C3).
+__device__ __forceinline__ std::uint64_t l2_evict_first_policy() {
+  std::uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_ef(void* dst, const void* src, unsigned bytes, std::uint64_t* bar,
+                                            std::uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
   unsigned ok = 0;
   do {
@@ -1687,7 +1703,7 @@ __global__ void __maxnreg__(96) k_near_gemv_lean(const SymRowItem* __restrict__ 
                                                                    const double* __restrict__ D,
                                                                    const double* __restrict__ xp,
                                                                    double* __restrict__ part,
-                                                                   int* __restrict__ counter) {
+                                                                   int* __restrict__ counter, bool evict_first) {
   static_assert(CH >= 128 * 16, "a chunk holds 16 columns of a 128-row leaf");
   constexpr int kStage = CH + 2 + 66;
   extern __shared__ __align__(128) double sm[];
@@ -1713,6 +1729,7 @@ __global__ void __maxnreg__(96) k_near_gemv_lean(const SymRowItem* __restrict__ 
   }
   __syncthreads();
   if (warp == NCW) {  // ------------------------------------------------ producer
+    const std::uint64_t pol = l2_evict_first_policy();
     int c = 0;
     for (int n = 0;; ++n) {
       const int ib = n & 1;
@@ -1749,7 +1766,10 @@ __global__ void __maxnreg__(96) k_near_gemv_lean(const SymRowItem* __restrict__ 
             const unsigned xbytes = static_cast<unsigned>(((ncols + xsh + 1) & ~1) * 8);
             PHM_DCHECK(xbytes <= 66 * 8);
             mbar_expect_tx(&full[slot], static_cast<unsigned>(nbytes) + xbytes);
-            bulk_g2s(sm + slot * kStage, D + ea, static_cast<unsigned>(nbytes), &full[slot]);
+            if (evict_first)
+              bulk_g2s_ef(sm + slot * kStage, D + ea, static_cast<unsigned>(nbytes), &full[slot], pol);
+            else
+              bulk_g2s(sm + slot * kStage, D + ea, static_cast<unsigned>(nbytes), &full[slot]);
             bulk_g2s(sm + slot * kStage + CH + 2, xsrc - xsh, xbytes, &full[slot]);
           }
         }
@@ -2662,11 +2682,15 @@ void launch_near_tma_apply(cudaStream_t st, const SymRowItem* items, int nitems,
       return k >= 1 && k <= 2 ? k : 1;
     }();
     const int grid = std::min(nitems, sms * lean_per_sm);
+    static const bool lef = [] {  // D by evict-first bulk copies (C_k stays in L2 for the coupling beside)
+      const char* e = std::getenv("PHM_GEMV_EVICT_FIRST");
+      return !(e && std::atoi(e) == 0);
+    }();
 #define PHM_LEAN(WW, LCH, NN)                                                                               \
   if (lnst == NN && lwarps == WW && lch == LCH) {                                                           \
     const size_t lsmem = static_cast<size_t>(NN * (LCH + 2 + 66) + WW * 128) * sizeof(double);             \
     smem_attr(reinterpret_cast<const void*>(k_near_gemv_lean<WW, LCH, NN>), static_cast<int>(lsmem), true); \
-    k_near_gemv_lean<WW, LCH, NN><<<grid, (WW + 1) * 32, lsmem, st>>>(items, nitems, blocks, D, xp, part, counter); \
+    k_near_gemv_lean<WW, LCH, NN><<<grid, (WW + 1) * 32, lsmem, st>>>(items, nitems, blocks, D, xp, part, counter, lef); \
     return;                                                                                                 \
   }
     PHM_LEAN(4, 4096, 2) PHM_LEAN(4, 3072, 2) PHM_LEAN(4, 4096, 3) PHM_LEAN(4, 3072, 3) PHM_LEAN(4, 4096, 4)
@@ -2675,7 +2699,7 @@ void launch_near_tma_apply(cudaStream_t st, const SymRowItem* items, int nitems,
     {  // any other PHM_NEAR_LEAN_* combination: the default kernel
       const size_t lsmem = static_cast<size_t>(2 * (4096 + 2 + 66) + 4 * 128) * sizeof(double);
       smem_attr(reinterpret_cast<const void*>(k_near_gemv_lean<4, 4096, 2>), static_cast<int>(lsmem), true);
-      k_near_gemv_lean<4, 4096, 2><<<grid, 5 * 32, lsmem, st>>>(items, nitems, blocks, D, xp, part, counter);
+      k_near_gemv_lean<4, 4096, 2><<<grid, 5 * 32, lsmem, st>>>(items, nitems, blocks, D, xp, part, counter, lef);
     }
     return;
   }
