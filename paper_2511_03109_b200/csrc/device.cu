@@ -1001,7 +1001,17 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     M.C_len = M.h2 ? static_cast<std::int64_t>(M.ncls) * M.P * M.P : 0;
     upload(M.cmeta, M.cmeta_h, st);
     upload(M.fixed_H, B.fixed_h, st);
-    if (M.h2) upload(M.fixed_C, B.fixed_c, st);
+    if (M.h2) {
+      if (M.P == 64) {  // C_k in DMMA fragment order (kernels.cuh cfrag64)
+        std::vector<double> fc(B.fixed_c.size());
+        for (std::size_t k = 0; k * 4096 < fc.size(); ++k)
+          for (int j = 0; j < 64; ++j)
+            for (int i = 0; i < 64; ++i) fc[k * 4096 + dev::cfrag64(i, j)] = B.fixed_c[k * 4096 + i + j * 64];
+        upload(M.fixed_C, fc, st);
+      } else {
+        upload(M.fixed_C, B.fixed_c, st);
+      }
+    }
   } else {
     M.ncls = static_cast<int>(H.couplings.size());
     std::vector<double> mid, L, R;
@@ -1667,6 +1677,12 @@ void instance_class_c(DevInstance& I, Index k, std::vector<double>& out) {
   CK(cudaMemcpyAsync(out.data(), I.C.as<double>() + k * static_cast<std::int64_t>(M.P) * M.P,
                      out.size() * sizeof(double), cudaMemcpyDeviceToHost, M.st()));
   CK(cudaStreamSynchronize(M.st()));
+  if (M.P == 64) {  // stored in DMMA fragment order (kernels.cuh cfrag64)
+    std::vector<double> cm(out.size());
+    for (int j = 0; j < 64; ++j)
+      for (int i = 0; i < 64; ++i) cm[i + j * 64] = out[dev::cfrag64(i, j)];
+    out.swap(cm);
+  }
 }
 
 // ------------------------------------------------------------------ apply

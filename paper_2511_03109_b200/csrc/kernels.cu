@@ -481,12 +481,12 @@ __global__ void k_class_inst(const ClassMeta* __restrict__ meta, int ncls, const
     const int c = 8 * warp + 2 * t0;
     double* Cb = C + M.c_off;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
+    for (int mt = 0; mt < 4; ++mt) {  // fragment order (cfrag64)
       const int r = 16 * mt + g;
-      Cb[r + c * 64] = acc[mt][0];
-      Cb[r + (c + 1) * 64] = acc[mt][1];
-      Cb[r + 8 + c * 64] = acc[mt][2];
-      Cb[r + 8 + (c + 1) * 64] = acc[mt][3];
+      Cb[cfrag64(r, c)] = acc[mt][0];
+      Cb[cfrag64(r, c + 1)] = acc[mt][1];
+      Cb[cfrag64(r + 8, c)] = acc[mt][2];
+      Cb[cfrag64(r + 8, c + 1)] = acc[mt][3];
     }
     return;
   }
@@ -504,7 +504,7 @@ __global__ void k_class_inst(const ClassMeta* __restrict__ meta, int ncls, const
       const int a = e % P, bb = e / P;
       double s = 0.0;
       for (int i = 0; i < rl; ++i) s += Lm[M.l_off + a + static_cast<std::int64_t>(i) * P] * Tt[i + bb * rl];
-      C[M.c_off + a + static_cast<std::int64_t>(b0 + bb) * P] = s;
+      C[M.c_off + (P == 64 ? cfrag64(a, b0 + bb) : a + static_cast<std::int64_t>(b0 + bb) * P)] = s;
     }
   }
 }
@@ -790,11 +790,21 @@ __global__ void __maxnreg__(P >= 128 ? 128 : 88) k_coupling_mma(const CouplingIt
     };
     auto load_a = [&](int e, int h, double (&a)[KH][2]) {
       const double* Ck = C + static_cast<std::int64_t>(item_cls[e]) * P * P;
+      if constexpr (P == 64) {  // fragment order: one 16-byte load per k-step
+        const double2* F = reinterpret_cast<const double2*>(Ck);
 #pragma unroll
-      for (int s2 = 0; s2 < KH; ++s2) {
-        const std::int64_t k = 4 * (h * KH + s2) + t0;
-        a[s2][0] = __ldg(Ck + (row0 + g) + k * P);
-        a[s2][1] = __ldg(Ck + (row0 + g + 8) + k * P);
+        for (int s2 = 0; s2 < KH; ++s2) {
+          const double2 v = __ldg(F + ((h * KH + s2) * 4 + warp) * 32 + lane);
+          a[s2][0] = v.x;
+          a[s2][1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int s2 = 0; s2 < KH; ++s2) {
+          const std::int64_t k = 4 * (h * KH + s2) + t0;
+          a[s2][0] = __ldg(Ck + (row0 + g) + k * P);
+          a[s2][1] = __ldg(Ck + (row0 + g + 8) + k * P);
+        }
       }
     };
     auto mma = [&](const double (&a)[KH][2], int h, const double* X, unsigned tiles) {

@@ -92,6 +92,16 @@ struct LeafChunk {
   std::int64_t slot;
 };
 
+// C_k with P = 64 is stored in DMMA fragment order: element (i, j) (row i of
+// sigma's basis, column j of tau's) at cfrag64(i, j), so that the coupling's
+// m16n8k4 A fragment of (k-step s, m-tile mt) is 32 lanes x 16 contiguous
+// bytes -- one coalesced 16-byte load per lane, and a contiguous 8 KB per
+// quarter of k-steps.
+__host__ __device__ inline int cfrag64(int i, int j) {
+  const int mt = i >> 4, r = i & 15, s = j >> 2, t0 = j & 3;
+  return (((s * 4 + mt) * 32 + ((r & 7) << 2) + t0) << 1) + (r >> 3);
+}
+
 constexpr int kGroupSlots = 32;
 struct CouplingItem {
   std::int32_t group, e_begin, e_end, pad;
