@@ -217,7 +217,7 @@ int phm_instance_destroy(phm_instance inst);
 int phm_instance_sync(phm_instance inst);
 int phm_instance_far_h(phm_instance inst, int64_t far_index, double* out, int64_t* rows, int64_t* cols);
 int phm_instance_near_d(phm_instance inst, int64_t near_block, double* out);
-int phm_instance_class_c(phm_instance inst, int64_t cls, double* out /* P x P */);
+int phm_instance_class_c(phm_instance inst, int64_t cls, double* out /* P x P, column-major (the device keeps P = 64 in DMMA fragment order and converts here) */);
 /* y = K(theta) x, host buffers, n_rows must equal n (length check before
  * any launch, phmatrix.cpp:228); m right-hand sides, column-major. */
 int phm_apply(phm_instance inst, const double* x, int64_t n_rows, double* y, int64_t m);
