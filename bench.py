@@ -444,6 +444,13 @@ def run_ours(args):
 
     # phase split of the same step (same stream, CUDA events)
     inst_ms = time_loop(lambda s: inst.reinstantiate(theta_of(s)))
+    # The MVM phase starts after 1 s of idle GPU: right behind the step and
+    # instantiate loops it inherits their transient sw_power_cap clock dips
+    # (C3: 1.94 ms per apply straight after 25 fused steps, 1.69 ms after a
+    # 1 s pause, the same as a fresh process; tools/apply_probe.py --idle).
+    if not row_shard:
+        torch.cuda.synchronize()
+        time.sleep(1.0)
     apply_ms = (time_loop(lambda s: inst.apply_device(x_dev.data_ptr(), y_dev.data_ptr(), m))
                 if not row_shard else None)
     # per-kernel split of the apply phase (separate loop: the timers add events)

@@ -43,7 +43,7 @@ void launch_put_theta(cudaStream_t, const ThetaParams&, ThetaParams*);
 void launch_stamp(cudaStream_t, unsigned long long*, int);
 void launch_zero(cudaStream_t, double*, std::int64_t);
 void launch_class_inst(cudaStream_t, const ClassMeta*, int, const double*, const std::int32_t*, const double*,
-                       const double*, const ThetaParams*, int, bool, int, int, int, int, double*, double*);
+                       const double*, const ThetaParams*, int, bool, int, int, int, int, int, int, double*, double*);
 void launch_gather(cudaStream_t, const double*, const std::int32_t*, std::int64_t, std::int64_t, double*);
 void launch_scatter(cudaStream_t, const double*, const std::int32_t*, std::int64_t, std::int64_t, double*);
 void launch_leaf_fwd_chunks(cudaStream_t, const LeafChunk*, int, const std::int32_t*, const std::int64_t*,
@@ -392,7 +392,7 @@ struct DevMatrix {
   bool baseline = false;  // fixed far field (H-ACA / H^2-HCA at one theta)
   DBuf fixed_H, fixed_C;
   std::int64_t H_len = 0, C_len = 0;
-  int capA = 0, capB = 0, capT = 0, capL = 0;
+  int capA = 0, capB = 0, capT = 0, capL = 0, capR = 0;  // capR > 0: k_class_inst_pf
   // H^2 coupling CSR by sigma node
   DBuf cp_sig, cp_beg, cp_tau, cp_cls;
   int n_cp_sig = 0;
@@ -1017,7 +1017,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     std::vector<double> mid, L, R;
     std::vector<std::int32_t> mdims;
     std::int64_t hoff = 0;
-    int maxrl = 1, maxrr = 1, maxA = 1, maxB = 1, maxs1 = 1;
+    int maxrl = 1, maxrr = 1, maxA = 1, maxB = 1, maxs1 = 1, maxdt = 0;
     for (int k = 0; k < M.ncls; ++k) {
       const Coupling& c = H.couplings[k];
       dev::ClassMeta cm{};
@@ -1027,6 +1027,7 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
       cm.mid_off = static_cast<std::int64_t>(mid.size());
       cm.dims_off = static_cast<std::int32_t>(mdims.size());
       int cur = 1;
+      maxdt = std::max(maxdt, c.d_theta);
       for (int q = 0; q < c.d_theta; ++q) {
         const TTCore& g = c.tt.cores[c.d + q];
         mdims.push_back(static_cast<std::int32_t>(g.r0));
@@ -1073,8 +1074,28 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
       const int rl4 = (mrl + 3) & ~3, rr4 = (mrr + 3) & ~3;
       M.capT = std::max(M.capT, ldT * 64);
       M.capL = 68 * std::max(rl4, rr4);  // L, and R before it
+      // every class on the DMMA path: k_class_inst_pf (all loads of a class
+      // in flight at once; its own region sizes, each a multiple of two
+      // doubles for the 16-byte cp.async destinations)
+      static const bool pf_env = [] {
+        const char* e = std::getenv("PHM_CLASS_PF");
+        return !(e && std::atoi(e) == 0);
+      }();
+      bool all_dmma = true;
+      for (const auto& cm : M.cmeta_h) all_dmma = all_dmma && cm.rl <= 64;
+      // one theta core (the chain of two or more measured slower with it:
+      // C4 proxy 0.43 -> 0.60 ms)
+      if (pf_env && all_dmma && maxdt == 1) {
+        auto even = [](int v) { return (v + 1) & ~1; };
+        M.capA = even(std::max(maxA, maxrl * maxs1));
+        M.capB = even(maxB);
+        M.capT = even(maxrl * maxs1);               // theta-chain scratch
+        M.capR = even(std::max(68 * rr4, ldT * 64));  // R, then T
+        M.capL = 68 * rl4;                          // L
+      }
     }
-    PHM_CHECK((M.capA + M.capB + M.capT + M.capL) * 8 <= 227 * 1024, "class instantiate shared memory over 227 KB");
+    PHM_CHECK((M.capA + M.capB + M.capT + M.capR + M.capL) * 8 <= 227 * 1024,
+              "class instantiate shared memory over 227 KB");
     M.H_len = hoff;
     M.C_len = M.h2 ? static_cast<std::int64_t>(M.ncls) * M.P * M.P : 0;
     upload(M.cmeta, M.cmeta_h, st);
@@ -1388,7 +1409,10 @@ void put_theta(DevMatrix& M, const std::vector<std::vector<double>>& v, const de
   M.ctx->run_on(s, "put_theta", [&] { dev::launch_put_theta(s, p, M.theta_dev.as<dev::ThetaParams>()); });
 }
 
-void inst_classes(DevInstance& I, cudaStream_t s) {
+// ctas > 0 caps the grid of k_class_inst_pf (a persistent loop over the
+// classes): beside the fused near pass, one class CTA per SM leaves room for
+// a near CTA from the start instead of holding every slot until its last wave.
+void inst_classes(DevInstance& I, cudaStream_t s, int ctas = 0) {
   DevMatrix& M = *I.M;
   const bool all = M.ncls_run < 0 || M.baseline;
   if (!all && M.ncls_run == 0) return;  // a shard without far blocks
@@ -1396,7 +1420,7 @@ void inst_classes(DevInstance& I, cudaStream_t s) {
     dev::launch_class_inst(s, all ? M.cmeta.as<dev::ClassMeta>() : M.cmeta_run.as<dev::ClassMeta>(),
                            all ? M.ncls : M.ncls_run, M.class_mid.as<double>(),
                            M.class_mid_dims.as<std::int32_t>(), M.class_L.as<double>(), M.class_R.as<double>(),
-                           M.theta_dev.as<dev::ThetaParams>(), M.P, M.h2, M.capA, M.capB, M.capT, M.capL,
+                           M.theta_dev.as<dev::ThetaParams>(), M.P, M.h2, M.capA, M.capB, M.capT, M.capL, M.capR, ctas,
                            I.H.as<double>(), I.C.as<double>());
   });
 }
@@ -2054,7 +2078,18 @@ void instantiate_apply_sequence(DevInstance& I, const double* x_dev, Index m, St
   ctx.run_on(fs, "gather", [&] { dev::launch_gather(fs, x_dev, M.perm.as<std::int32_t>(), M.n, m, M.xp.as<double>()); });
   ctx.stamp(fs, 9);
   CK(cudaEventRecord(ctx.aux_ev, fs));
-  inst_classes(I, fs);
+  // PHM_CLASS_PER_SM=k: k class CTAs per SM beside the fused near pass
+  // (k_class_inst_pf as a persistent loop) instead of one CTA per class.
+  // Measured on row shard 8 of 8 at C3 and not the default: with k = 1 the
+  // near pass starts at once but runs a CTA short per SM while the class
+  // stage takes 2x longer (1.277 -> 1.314 ms per step); k = 2 equals the
+  // full grid (1.274).
+  static const int class_per_sm = [] {
+    const char* e = std::getenv("PHM_CLASS_PER_SM");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool fuse_near = M.near_tma && M.mode == NearMode::Snapshot && m == 1;
+  inst_classes(I, fs, fuse_near && class_per_sm > 0 ? class_per_sm * ctx.sms : 0);
   ctx.stamp(fs, 2);
   // The coupling as a capped grid that stays resident beside the fused near
   // pass (one CTA per SM where it fits next to the pass's two) instead of
@@ -2183,6 +2218,7 @@ void instantiate_apply_sharded(DevInstance& I, Comm& ex, const double* theta, in
   M.ctx->run("scatter", [&] {
     dev::launch_scatter(M.st(), M.yp.as<double>(), M.perm.as<std::int32_t>(), M.n, m, y_dev);
   });
+  M.ctx->print_stamps();
 }
 
 void instantiate_apply_sharded_host(DevInstance& I, Comm& ex, const double* theta, int n_theta, const double* x,

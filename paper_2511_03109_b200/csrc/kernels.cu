@@ -350,6 +350,18 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
                : "d"(a0), "d"(a1), "d"(b0));
 }
 
+// cp.async (16-byte, L2 only) into shared memory
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int sz = valid ? 16 : 0;  // src-size 0 zero-fills (missing partner)
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ----------------------------------------------------------------- K2
 // One CTA per translation class. H = prod_i contract(G_{d+i}, v_i)
 // (farfield.cpp:149-155); for H^2 also C = L H R^T in 32-column tiles.
@@ -506,6 +518,167 @@ __global__ void k_class_inst(const ClassMeta* __restrict__ meta, int ncls, const
       for (int i = 0; i < rl; ++i) s += Lm[M.l_off + a + static_cast<std::int64_t>(i) * P] * Tt[i + bb * rl];
       C[M.c_off + (P == 64 ? cfrag64(a, b0 + bb) : a + static_cast<std::int64_t>(b0 + bb) * P)] = s;
     }
+  }
+}
+
+// K2 with every global load of a class issued up front (H^2, P = 64, all
+// left ranks <= 64): L_k and R_k go to shared memory by cp.async at the start
+// and stay in flight during the theta-core contraction, whose loads are
+// issued for four H entries per thread before their sums; T = H R^T then
+// reuses R's region. One DRAM round trip per class instead of three. Same
+// arithmetic, in the same order, as k_class_inst: H and C are bitwise equal.
+__global__ void __launch_bounds__(256, 2)
+    k_class_inst_pf(const ClassMeta* __restrict__ meta, int ncls, const double* __restrict__ mid,
+                    const std::int32_t* __restrict__ mid_dims, const double* __restrict__ Lm,
+                    const double* __restrict__ Rm, const ThetaParams* __restrict__ tp, int capA, int capB, int capS,
+                    int capR, double* __restrict__ H, double* __restrict__ C) {
+  constexpr int nt = 256, ldL = 68;
+  const ThetaV& tv = tp->tv;
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x;
+  // one class per CTA, or a capped persistent grid looping over the classes
+  for (int cls = blockIdx.x; cls < ncls; cls += gridDim.x) {
+  if (cls != static_cast<int>(blockIdx.x)) __syncthreads();  // the previous class is done with every region
+  const ClassMeta M = meta[cls];
+  const int rl = M.rl, rr = M.rr;
+  const int rl4 = (rl + 3) & ~3, rr4 = (rr + 3) & ~3;
+  double* A = sm;          // rl x r (running product), ld rl
+  double* B = A + capA;    // next contracted core (theta chains of two or more)
+  double* S = B + capB;    // A B scratch
+  double* Rs = S + capS;   // R (64 x rr4, ld 68), then T (rl4 x 64, ld ldT)
+  double* Ls = Rs + capR;  // L (64 x rl4, ld 68)
+  for (int e = tid; e < 32 * rr; e += nt) {
+    const int c = e >> 5, h = (e & 31) * 2;
+    cp_async16(Rs + h + c * ldL, Rm + M.r_off + h + static_cast<std::int64_t>(c) * 64, true);
+  }
+  for (int e = tid; e < 32 * rl; e += nt) {
+    const int c = e >> 5, h = (e & 31) * 2;
+    cp_async16(Ls + h + c * ldL, Lm + M.l_off + h + static_cast<std::int64_t>(c) * 64, true);
+  }
+  cp_async_commit();
+  for (int e = tid; e < 64 * (rr4 - rr); e += nt) Rs[(e & 63) + (rr + (e >> 6)) * ldL] = 0.0;
+  for (int e = tid; e < 64 * (rl4 - rl); e += nt) Ls[(e & 63) + (rl + (e >> 6)) * ldL] = 0.0;
+  // first theta core: A[a, c] = sum_j v_j G[a, j, c], zero weights skipped
+  std::int64_t off = M.mid_off;
+  {
+    const int r0 = mid_dims[M.dims_off + 0], m0 = mid_dims[M.dims_off + 1], r1 = mid_dims[M.dims_off + 2];
+    const int n = r0 * r1;
+    for (int e0 = tid; e0 < n; e0 += 4 * nt) {
+      const double* src[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = min(e0 + i * nt, n - 1);
+        src[i] = mid + off + (e % r0) + static_cast<std::int64_t>(e / r0) * r0 * m0;
+      }
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int j0 = 0; j0 < m0; j0 += 8) {
+        double x[4][8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) x[i][jj] = (j0 + jj < m0) ? src[i][(j0 + jj) * r0] : 0.0;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const double vj = (j0 + jj < m0) ? tv.v[0][j0 + jj] : 0.0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (vj != 0.0) s[i] += vj * x[i][jj];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (e0 + i * nt < n) A[e0 + i * nt] = s[i];
+    }
+    off += static_cast<std::int64_t>(r0) * m0 * r1;
+  }
+  for (int q = 1; q < tv.dt; ++q) {
+    const int s0 = mid_dims[M.dims_off + 3 * q], sm_ = mid_dims[M.dims_off + 3 * q + 1],
+              s1 = mid_dims[M.dims_off + 3 * q + 2];
+    __syncthreads();
+    for (int e = tid; e < s0 * s1; e += nt) {
+      const int a = e % s0, c = e / s0;
+      double s = 0.0;
+#pragma unroll 8
+      for (int j = 0; j < sm_; ++j) {
+        const double vj = tv.v[q][j];
+        const double x = mid[off + a + j * s0 + static_cast<std::int64_t>(c) * s0 * sm_];
+        if (vj != 0.0) s += vj * x;
+      }
+      B[e] = s;
+    }
+    off += static_cast<std::int64_t>(s0) * sm_ * s1;
+    __syncthreads();
+    for (int e = tid; e < rl * s1; e += nt) {
+      const int a = e % rl, c = e / rl;
+      double s = 0.0;
+      for (int k = 0; k < s0; ++k) s += A[a + k * rl] * B[k + c * s0];
+      S[e] = s;
+    }
+    __syncthreads();
+    for (int e = tid; e < rl * s1; e += nt) A[e] = S[e];
+  }
+  __syncthreads();
+  for (int e = tid; e < rl * rr; e += nt) H[M.h_off + e] = A[e];
+  cp_async_wait<0>();
+  __syncthreads();  // R and L landed
+  const int ldT = rl4 + ((4 - rl4) & 15);  // the least ld >= rl4 with ld = 4 mod 16
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t0 = lane & 3;
+  const int mts = (rl + 15) >> 4;
+  {
+    double acc[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.0;
+    for (int s2 = 0; s2 < (rr4 >> 2); ++s2) {
+      const int k = 4 * s2 + t0;
+      const double b0 = Rs[(8 * warp + g) + k * ldL];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        if (mt >= mts) break;  // warp-uniform
+        const int r = 16 * mt + g;
+        const double a0 = (r < rl && k < rr) ? A[r + k * rl] : 0.0;
+        const double a1 = (r + 8 < rl && k < rr) ? A[r + 8 + k * rl] : 0.0;
+        dmma_16x8x4(acc[mt], a0, a1, b0);
+      }
+    }
+    __syncthreads();  // every warp done with R: T takes its region
+    double* Ts = Rs;
+    const int c = 8 * warp + 2 * t0;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      if (mt >= mts) break;
+      const int r = 16 * mt + g;  // rows in [rl, rl4) come out zero (zero A rows)
+      if (r < rl4) {
+        Ts[r + c * ldT] = acc[mt][0];
+        Ts[r + (c + 1) * ldT] = acc[mt][1];
+      }
+      if (r + 8 < rl4) {
+        Ts[r + 8 + c * ldT] = acc[mt][2];
+        Ts[r + 8 + (c + 1) * ldT] = acc[mt][3];
+      }
+    }
+  }
+  __syncthreads();  // T complete
+  const double* Ts = Rs;
+  double acc[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.0;
+  for (int s2 = 0; s2 < (rl4 >> 2); ++s2) {
+    const int k = 4 * s2 + t0;
+    const double b0 = Ts[k + (8 * warp + g) * ldT];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+      dmma_16x8x4(acc[mt], Ls[(16 * mt + g) + k * ldL], Ls[(16 * mt + g + 8) + k * ldL], b0);
+  }
+  const int c = 8 * warp + 2 * t0;
+  double* Cb = C + M.c_off;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {  // fragment order (cfrag64)
+    const int r = 16 * mt + g;
+    Cb[cfrag64(r, c)] = acc[mt][0];
+    Cb[cfrag64(r, c + 1)] = acc[mt][1];
+    Cb[cfrag64(r + 8, c)] = acc[mt][2];
+    Cb[cfrag64(r + 8, c + 1)] = acc[mt][3];
+  }
   }
 }
 
@@ -712,17 +885,6 @@ __global__ void k_coupling(const std::int32_t* __restrict__ sig, const std::int6
 // shared memory by cp.async, double-buffered against the MMAs of the
 // previous class. Per-item partial sums are reduced in a fixed order by
 // k_coupling_reduce: deterministic, no atomics.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int sz = valid ? 16 : 0;  // src-size 0 zero-fills (missing partner)
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 // One (item, RHS column) pair per CTA iteration; X is the gathered 32-slot
 // panel of the column, double-buffered. item_tiles[e] has bit j set when
 // n-tile j (slots 8j .. 8j + 7) holds any partner of class item_cls[e];
@@ -2583,8 +2745,15 @@ void launch_put_theta(cudaStream_t st, const ThetaParams& p, ThetaParams* dst) {
 
 void launch_class_inst(cudaStream_t st, const ClassMeta* meta, int ncls, const double* mid, const std::int32_t* dims,
                        const double* L, const double* R, const ThetaParams* tp, int P, bool want_c, int capA,
-                       int capB, int capT, int capL, double* H, double* C) {
+                       int capB, int capT, int capL, int capR, int ctas, double* H, double* C) {
   if (ncls == 0) return;
+  if (capR > 0) {  // k_class_inst_pf: capT is its theta-chain scratch, capR the R / T region
+    const size_t smem = static_cast<size_t>(capA + capB + capT + capR + capL) * sizeof(double);
+    smem_attr(reinterpret_cast<const void*>(k_class_inst_pf), 227 * 1024, false);
+    const int grid = ctas > 0 ? std::min(ctas, ncls) : ncls;
+    k_class_inst_pf<<<grid, 256, smem, st>>>(meta, ncls, mid, dims, L, R, tp, capA, capB, capT, capR, H, C);
+    return;
+  }
   const size_t smem = static_cast<size_t>(capA + capB + capT + capL) * sizeof(double);
   smem_attr(reinterpret_cast<const void*>(k_class_inst), 227 * 1024, false);
   k_class_inst<<<ncls, 256, smem, st>>>(meta, ncls, mid, dims, L, R, tp, P, want_c ? 1 : 0, capA, capB, capT, H, C);

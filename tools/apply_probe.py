@@ -20,6 +20,11 @@ def main():
     ap.add_argument("--rhs", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--save", default=None, help="np.save y (tree of the last apply) here")
+    ap.add_argument("--pre-steps", type=int, default=0,
+                    help="run this many fused instantiate+apply steps (and reinstantiates) first, as bench.py does")
+    ap.add_argument("--pre-fused", type=int, default=None, help="fused steps first (default: --pre-steps)")
+    ap.add_argument("--pre-inst", type=int, default=None, help="reinstantiates first (default: --pre-steps)")
+    ap.add_argument("--idle", type=float, default=0.0, help="seconds of idle GPU between the pre-steps and the timing")
     a = ap.parse_args()
     import torch
 
@@ -37,6 +42,15 @@ def main():
     inst = ph.instantiate(pm, bench.theta_vectors(c, 1, 0)[0])
     x = torch.from_numpy(np.stack([ph.generate_normal(c["n"], 1 + j) for j in range(m)])).cuda()
     y = torch.empty_like(x)
+    thetas = bench.theta_vectors(c, 32, 0)
+    for s in range(a.pre_steps if a.pre_fused is None else a.pre_fused):
+        inst.instantiate_apply_device(thetas[s % 32], x.data_ptr(), y.data_ptr(), m)
+    for s in range(a.pre_steps if a.pre_inst is None else a.pre_inst):
+        inst.reinstantiate(thetas[s % 32])
+    torch.cuda.synchronize()
+    if a.idle > 0:
+        import time
+        time.sleep(a.idle)
     for _ in range(5):
         inst.apply_device(x.data_ptr(), y.data_ptr(), m)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -61,7 +75,8 @@ def main():
     if a.save:
         np.save(a.save, y.cpu().numpy())
     info = pm.info()
-    print(json.dumps({"config": a.config, "rhs": m, "apply_ms": ms, "near_stored": info["near_stored"],
+    print(json.dumps({"config": a.config, "rhs": m, "pre_fused": a.pre_steps if a.pre_fused is None else a.pre_fused,
+                      "pre_inst": a.pre_steps if a.pre_inst is None else a.pre_inst, "idle_s": a.idle, "apply_ms": ms, "near_stored": info["near_stored"],
                       "kernels_ms_per_apply": kern}))
 
 

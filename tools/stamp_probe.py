@@ -19,6 +19,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c3")
     ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--shards", type=int, default=0, help="time row shard --rank of N through the sharded step")
+    ap.add_argument("--rank", type=int, default=0)
     a = ap.parse_args()
     import torch
 
@@ -34,11 +36,18 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
-    pm = ph.offline_h2(pts, bench.make_cfg(ph, c), ctx)
+    if a.shards:
+        pm = ph.offline_h2(pts, bench.make_cfg(ph, c, a.rank, a.shards), ctx)
+        comm = ph.Comm.probe(a.rank, a.shards)
+    else:
+        pm = ph.offline_h2(pts, bench.make_cfg(ph, c), ctx)
     inst = ph.instantiate(pm, thetas[0])
     for s in range(a.steps):
         print("step", s, file=sys.stderr, flush=True)
-        inst.instantiate_apply_device(thetas[s % 32], x.data_ptr(), y.data_ptr(), 1)
+        if a.shards:
+            inst.instantiate_apply_sharded_device(comm, thetas[s % 32], x.data_ptr(), y.data_ptr(), 1)
+        else:
+            inst.instantiate_apply_device(thetas[s % 32], x.data_ptr(), y.data_ptr(), 1)
     torch.cuda.synchronize()
 
 
