@@ -176,8 +176,11 @@ struct Context {
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (join_ev) cudaEventDestroy(join_ev);
     if (aux_ev) cudaEventDestroy(aux_ev);
+    if (leaf_ev) cudaEventDestroy(leaf_ev);
+    if (up_ev) cudaEventDestroy(up_ev);
     if (stamps) cudaFree(stamps);
     if (side) cudaStreamDestroy(side);
+    if (side2) cudaStreamDestroy(side2);
     if (own) cudaStreamDestroy(own);
   }
   cudaEvent_t ev() {
@@ -261,6 +264,11 @@ struct Context {
   // GEMV (compute-bound DMMA next to an HBM stream); fork/join by events.
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, aux_ev = nullptr;
+  // Third stream (same priority as side): in apply, the transfer pass and the
+  // upper-level coupling run here while the leaf-level coupling, which needs
+  // only the leaf x-hat, already runs on side (far_chain).
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t leaf_ev = nullptr, up_ev = nullptr;
   void fork() {
     CK(cudaEventRecord(fork_ev, stream));
     CK(cudaStreamWaitEvent(side, fork_ev, 0));
@@ -307,7 +315,10 @@ std::shared_ptr<Context> context_create(int device) {
     const char* e = std::getenv("PHM_SIDE_PRIORITY");
     const bool prio = !(e && std::atoi(e) == 0);
     CK(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio ? hi : lo));
+    CK(cudaStreamCreateWithPriority(&ctx->side2, cudaStreamNonBlocking, prio ? hi : lo));
   }
+  CK(cudaEventCreateWithFlags(&ctx->leaf_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->up_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->aux_ev, cudaEventDisableTiming));
@@ -400,6 +411,13 @@ struct DevMatrix {
   bool cp_mma = false;
   DBuf cg_items, cg_order, cg_cls, cg_tiles, cg_tau, cg_grp_sigma, cg_grp_items, cg_partial;
   int n_cg_items = 0, n_cg_groups = 0;
+  // cg_order lists the items of levels above the leaf level first: the first
+  // cg_n_upper entries need the transfer pass, the rest only the leaf x-hat
+  // (-1: order not by level)
+  int cg_n_upper = -1;
+  // lowest level (nearest the root) holding far blocks, over ALL ranks' blocks
+  // (class keys): x-hat / y-hat of the levels above it are never used
+  int far_min_level = 0;
   // H form far CSR by level
   DBuf fh_items, fh_tb, fh_tn, fh_cls, fh_soff, fh_toff, fh_S, fh_T, fh_bitem, fh_poff, fh_part;
   std::vector<dev::FarHItem> fh_items_h;
@@ -1223,6 +1241,12 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
         }();
         if (!ordered)
           for (size_t i = 0; i < items.size(); ++i) order[i] = static_cast<std::int32_t>(i);
+        M.cg_n_upper = -1;
+        if (ordered) {
+          M.cg_n_upper = 0;
+          for (std::int32_t i : order)
+            if (grp_level[items[i].group] < T.l_max) ++M.cg_n_upper;
+        }
         upload(M.cg_order, order, st);
       }
       upload(M.cg_items, items, st);
@@ -1322,6 +1346,16 @@ std::shared_ptr<DevMatrix> matrix_upload(std::shared_ptr<Context> ctx, std::uniq
     upload(M.up_nodes, upn, st);
     upload(M.down_nodes, dnn, st);
     upload(M.upl_nodes, upl, st);
+    // Levels above the first one with far blocks take no part in the product
+    // (chebyshev.cpp:223-298 runs them; their x-hat / y-hat are never read).
+    // Class keys cover every rank's far blocks, so shards agree on the level.
+    M.far_min_level = T.l_max;
+    for (const auto& key : H.class_keys) M.far_min_level = std::min<int>(M.far_min_level, static_cast<int>(key[0]));
+    if (H.class_keys.empty()) M.far_min_level = 0;
+    {
+      const char* e = std::getenv("PHM_SKIP_TOP_LEVELS");
+      if (e && std::atoi(e) == 0) M.far_min_level = 0;
+    }
   } else {
     // H form: far blocks grouped per level, CSR by sigma, S/T payloads
     std::vector<dev::FarHItem> items;
@@ -1714,7 +1748,8 @@ namespace {
 
 // H^2 far-field chain on stream fs: forward (K3, K4), coupling (K5),
 // downward (K7 internal). Reads xp and C_k; writes yhat.
-void far_chain(DevInstance& I, Index m, cudaStream_t fs, int coupling_ctas, Comm* ex = nullptr) {
+void far_chain(DevInstance& I, Index m, cudaStream_t fs, int coupling_ctas, Comm* ex = nullptr,
+               bool leaf_level_first = false) {
   DevMatrix& M = *I.M;
   const HostMatrix& H = *M.hm;
   Context& ctx = *M.ctx;
@@ -1758,32 +1793,63 @@ void far_chain(DevInstance& I, Index m, cudaStream_t fs, int coupling_ctas, Comm
                            mm, M.xhat.as<double>());
     });
   }
-  for (int l = H.tree->l_max - 1; l >= 0; --l) {
-    const auto r = split ? M.upl_range[l] : M.up_range[l];
-    if (r.second == r.first) continue;
-    ctx.run_on(fs, "up", [&] {
-      dev::launch_up(fs, (split ? M.upl_nodes : M.up_nodes).as<std::int32_t>() + r.first, r.second - r.first,
-                     M.node_first_child.as<std::int32_t>(), M.node_count.as<std::int32_t>(), M.Etr.as<double>(), M.d,
-                     M.ps, P, mm, M.xhat.as<double>());
-    });
-  }
-  if (split) ex->allreduce(M.xhat.as<double>(), static_cast<std::int64_t>(M.nnodes) * P * m, fs);
-  // a kernel, not a memset: a memset node of a graph carries no priority and
-  // would wait behind the near pass's CTAs
-  ctx.run_on(fs, "zero", [&] { dev::launch_zero(fs, M.yhat.as<double>(), static_cast<std::int64_t>(M.nnodes) * P * m); });
+  // PHM_LEAF_LEVEL_FIRST=1 (diagnostic, off by default): leaf-level blocks
+  // (2.02M of 2.16M at C3) read only the leaf x-hat, so in apply their
+  // coupling launch can start right after K3 while the transfer pass and the
+  // upper levels' coupling run on a second side stream. Items write disjoint
+  // partial slots and the reduction order is per item, so y is bitwise the
+  // same. Measured at C3: no gain (1.691 vs 1.677 ms) -- the MVM is bound by
+  // the SM time the GEMV and the coupling share, not by the K3 -> K4 -> K5
+  // dependency chain; the earlier coupling just overlaps more of the GEMV
+  // and both slow down (profiles/r02d_apply_level_split_sweep.txt).
+  static const bool llf_env = [] {
+    const char* e = std::getenv("PHM_LEAF_LEVEL_FIRST");
+    return e && std::atoi(e) == 1;
+  }();
+  const bool llf = leaf_level_first && llf_env && !split && M.cp_mma && coupling_ctas == 0 && M.cg_n_upper > 0 &&
+                   M.cg_n_upper < M.n_cg_items;
+  cudaStream_t us = llf ? ctx.side2 : fs;  // transfer pass (and upper-level coupling)
   if (M.cp_mma) {
     const size_t need = sizeof(double) * std::max(1, M.n_cg_items) * m * dev::kGroupSlots * P;
     if (M.cg_partial.bytes < need) {
       M.cg_partial.alloc(need);
       ++M.ws_gen;  // captured graphs hold the old pointer
     }
-    ctx.stamp(fs, 5);
-    ctx.run_on(fs, "coupling", [&] {
-      dev::launch_coupling_mma(fs, M.cg_items.as<dev::CouplingItem>(), M.cg_order.as<std::int32_t>(), M.n_cg_items,
-                               M.cg_cls.as<std::int32_t>(),
-                               M.cg_tiles.as<std::uint8_t>(), M.cg_tau.as<std::int32_t>(), I.C.as<double>(), P,
-                               M.xhat.as<double>(), mm, M.cg_partial.as<double>(), coupling_ctas);
+  }
+  auto coupling_launch = [&](cudaStream_t s, int first, int count) {
+    ctx.run_on(s, "coupling", [&] {
+      dev::launch_coupling_mma(s, M.cg_items.as<dev::CouplingItem>(), M.cg_order.as<std::int32_t>() + first, count,
+                               M.cg_cls.as<std::int32_t>(), M.cg_tiles.as<std::uint8_t>(),
+                               M.cg_tau.as<std::int32_t>(), I.C.as<double>(), P, M.xhat.as<double>(), mm,
+                               M.cg_partial.as<double>(), coupling_ctas);
     });
+  };
+  // a kernel, not a memset: a memset node of a graph carries no priority and
+  // would wait behind the near pass's CTAs
+  ctx.run_on(fs, "zero", [&] { dev::launch_zero(fs, M.yhat.as<double>(), static_cast<std::int64_t>(M.nnodes) * P * m); });
+  if (llf) {
+    CK(cudaEventRecord(ctx.leaf_ev, fs));
+    CK(cudaStreamWaitEvent(us, ctx.leaf_ev, 0));
+    coupling_launch(fs, M.cg_n_upper, M.n_cg_items - M.cg_n_upper);
+  }
+  for (int l = H.tree->l_max - 1; l >= M.far_min_level; --l) {
+    const auto r = split ? M.upl_range[l] : M.up_range[l];
+    if (r.second == r.first) continue;
+    ctx.run_on(us, "up", [&] {
+      dev::launch_up(us, (split ? M.upl_nodes : M.up_nodes).as<std::int32_t>() + r.first, r.second - r.first,
+                     M.node_first_child.as<std::int32_t>(), M.node_count.as<std::int32_t>(), M.Etr.as<double>(), M.d,
+                     M.ps, P, mm, M.xhat.as<double>());
+    });
+  }
+  if (llf) {
+    coupling_launch(us, 0, M.cg_n_upper);
+    CK(cudaEventRecord(ctx.up_ev, us));
+    CK(cudaStreamWaitEvent(fs, ctx.up_ev, 0));
+  }
+  if (split) ex->allreduce(M.xhat.as<double>(), static_cast<std::int64_t>(M.nnodes) * P * m, fs);
+  if (M.cp_mma) {
+    ctx.stamp(fs, 5);
+    if (!llf) coupling_launch(fs, 0, M.n_cg_items);
     ctx.stamp(fs, 6);
     ctx.run_on(fs, "coupling_reduce", [&] {
       dev::launch_coupling_reduce(fs, M.cg_grp_sigma.as<std::int32_t>(), M.cg_grp_items.as<std::int32_t>(),
@@ -1796,7 +1862,7 @@ void far_chain(DevInstance& I, Index m, cudaStream_t fs, int coupling_ctas, Comm
                            M.xhat.as<double>(), M.yhat.as<double>());
     });
   }
-  for (int l = 1; l <= H.tree->l_max; ++l) {
+  for (int l = std::max(1, M.far_min_level + 1); l <= H.tree->l_max; ++l) {
     const auto r = M.down_range[l];
     if (r.second == r.first) continue;
     ctx.run_on(fs, "down", [&] {
@@ -1949,7 +2015,7 @@ void apply_tree_order(DevInstance& I, Index m, Comm* ex = nullptr) {
   }();
   if (M.h2) {
     ctx.fork();
-    far_chain(I, m, ctx.side, apply_cp_per_sm * ctx.sms, ex);
+    far_chain(I, m, ctx.side, apply_cp_per_sm * ctx.sms, ex, /*leaf_level_first=*/true);
   }
   near_product(I, m, ctx.stream);
   if (M.h2) ctx.join();
