@@ -552,6 +552,8 @@ def run_ours(args):
         dmma_peak = dmma_peak_tflops()
         cp_tf = (2.0 * info["n_far"] * info["P"] ** 2 * m / (cp["ms_per_launch"] * 1e-3) / 1e12) if cp else None
         k9_tf = (2.0 * info["near_entries"] * m / (k9["ms_per_launch"] * 1e-3) / 1e12) if k9 else None
+        mvm_gflop = ((2.0 * info["n_far"] * info["P"] ** 2 if c["fmt"] == "h2" else 0.0)
+                     + 2.0 * info["near_entries"]) * m / 1e9
         dmma = {
             "note": ("useful fp64 flop over each kernel's event-timed duration inside the step, where it "
                      "time-shares the SMs with the near pass (the fused step's coupling is a capped grid "
@@ -589,7 +591,13 @@ def run_ours(args):
                        "instantiate_GB_s": b_inst / (inst_ms * 1e-3) / 1e9},
             "mvm": {"ms": mvm_ms, "algorithmic_bytes": b_mvm,
                     "GB_s": b_mvm / (mvm_ms * 1e-3) / 1e9 if mvm_ms else None,
-                    "frac_of_hbm": (b_mvm / (mvm_ms * 1e-3) / 1e9) / peak if mvm_ms else None},
+                    "frac_of_hbm": (b_mvm / (mvm_ms * 1e-3) / 1e9) / peak if mvm_ms else None,
+                    # the MVM's second resource: fp64 flop of the coupling (2 |far| P^2 m, only for
+                    # H^2) and of the near product (2 per entry and RHS), against the measured
+                    # fp64 peak (DMMA and DFMA share one pipe on this part)
+                    "fp64_gflop": mvm_gflop,
+                    "fp64_ms_at_peak": (mvm_gflop / dmma_peak) if dmma_peak else None,
+                    "hbm_ms_at_peak": b_mvm / peak / 1e6},
             "near_gemv": near_gemv,
             "apply_kernels": apply_timers,
             "dmma": dmma,

@@ -193,6 +193,27 @@ def test_block_rhs_dmma_near_field(ph, po, sym, m):
     assert rel(Y, Yo) <= TOL_Y
 
 
+@pytest.mark.parametrize("sym,m", [(True, 10), (True, 17), (False, 10), (True, 18)])
+def test_block_rhs_tail_columns_on_gemv(ph, po, sym, m):
+    """H^2 with m = 8k + (1 or 2) right-hand sides (BASELINE config 5: m =
+    10): K9 takes the first 8k columns, the tail columns run on the HBM GEMV
+    (K6). Every column against the oracle; the tail columns are the
+    single-vector path bit for bit."""
+    pts = ph.generate_points(2300, 3, 33)
+    cfg = ph.PHConfig(spec=ph.KernelSpec(ph.Family.E, [(0.05, 0.5)]), l_max=2, p_s=4, p_theta=8, eta=1.0,
+                      near_mode=ph.NearMode.SNAPSHOT, symmetric_near=sym)
+    pm, om = _build(ph, po, pts, cfg, ph.Format.H2)
+    inst = ph.instantiate(pm, [0.19])
+    rng = np.random.default_rng(100 + m)
+    X = rng.standard_normal((2300, m))
+    Y = inst.apply(X)
+    Yo = om.instantiate([0.19]).apply(X)
+    for c in range(m):
+        assert rel(Y[:, c], Yo[:, c]) <= TOL_Y
+        assert rel(Y[:, c], inst.apply(X[:, c])) <= 1e-14
+    assert np.array_equal(inst.apply(X), Y)  # deterministic
+
+
 def test_two_parameter_amplitude_kernel(ph, po):
     """theta = (l, sigma^2) with an 8 x 6 tensor grid (BASELINE config 4 form)."""
     pts = ph.generate_mixture_points(3000, 3, 16, 0.05, 0)

@@ -22,7 +22,7 @@ python tools/apply_probe.py > $out/apply_probe.json 2>&1
 python tools/apply_probe.py --rhs 10 > $out/apply_probe_m10.json 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/c3_launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $out/c3_launches.log 2>&1
-for k in k_near_tma k_coupling_mma k_class_inst; do
+for k in k_near_tma k_coupling_mma k_class_inst_pf; do
   ncu --set full --import-source on --clock-control none -k "regex:${k}\b" -c 1 -o $out/c3_full_$k -f \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $out/c3_full_$k.log 2>&1
 done
