@@ -564,6 +564,26 @@ def run_ours(args):
             "near_mrhs_tflops_in_step": k9_tf,
             "near_mrhs_frac_of_peak": k9_tf / dmma_peak if k9_tf and dmma_peak else None,
         }
+        timing_note = ("kernel launch times from CUDA events around each launch, over a second pass "
+                       "of the same K steps (value's pass runs without them, as CUDA graphs)")
+        roofline = {"bound": "hbm", "kernel": k1_desc, "achieved": achieved,
+                    "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                    "traffic_source": traffic_src, "peak_kind": peak_kind, "bytes_per_launch": k1_bytes,
+                    "avg_launch_ms": k1_avg, "timing": timing_note,
+                    "ms_per_step_event_pass": ms_timed_loop / args.steps}
+        extra = {}
+        if cp and dmma_peak and cp["ms_per_launch"] * cp["launches"] > k1_ms:
+            # block right-hand sides (C5): the coupling's fp64 DMMA GEMMs outweigh the snapshot
+            # stream, so the dominant kernel is tensor-bound; the HBM line of K1 stays beside it
+            cp_flop = 2.0 * info["n_far"] * info["P"] ** 2 * m
+            extra["roofline_hbm"] = roofline
+            roofline = {"bound": "tensor", "kernel": "k_coupling_mma (K5: C_k x-hat on fp64 mma.sync m16n8k4)",
+                        "achieved": cp_tf, "peak": dmma_peak, "unit": "TFLOP/s", "frac": cp_tf / dmma_peak,
+                        "traffic": None,
+                        "peak_kind": "measured fp64 DMMA peak, profiles/dmma_peak.json (tools/dmma_probe.cu); "
+                                     "MEASURED_PEAKS.json holds bf16 only, and sm_100 has no tcgen05 f64 kind",
+                        "flops_per_launch": cp_flop, "avg_launch_ms": cp["ms_per_launch"], "timing": timing_note,
+                        "ms_per_step_event_pass": ms_timed_loop / args.steps}
         what, config = describe(args, c, m, tb, world)
         line = {
             "metric": what,
@@ -580,13 +600,7 @@ def run_ours(args):
             "dtype": "f64",
             "data": "synthetic (seeded uniform points, harness theta draws, x~N(0,1))",
             "config": config,
-            "roofline": {"bound": "hbm", "kernel": k1_desc, "achieved": achieved,
-                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "traffic_source": traffic_src, "peak_kind": peak_kind, "bytes_per_launch": k1_bytes,
-                         "avg_launch_ms": k1_avg,
-                         "timing": "kernel launch times from CUDA events around each launch, over a second pass "
-                                   "of the same K steps (value's pass runs without them, as CUDA graphs)",
-                         "ms_per_step_event_pass": ms_timed_loop / args.steps},
+            "roofline": roofline,
             "phases": {"instantiate_ms": inst_ms, "apply_ms": apply_ms,
                        "instantiate_GB_s": b_inst / (inst_ms * 1e-3) / 1e9},
             "mvm": {"ms": mvm_ms, "algorithmic_bytes": b_mvm,
@@ -598,6 +612,7 @@ def run_ours(args):
                     "fp64_gflop": mvm_gflop,
                     "fp64_ms_at_peak": (mvm_gflop / dmma_peak) if dmma_peak else None,
                     "hbm_ms_at_peak": b_mvm / peak / 1e6},
+            **extra,
             "near_gemv": near_gemv,
             "apply_kernels": apply_timers,
             "dmma": dmma,
