@@ -895,7 +895,11 @@ __global__ void k_coupling(const std::int32_t* __restrict__ sig, const std::int6
 // occupancy; each half still feeds every tile). Prefetching the next class's
 // fragments instead made the capped grid beside the near pass faster
 // (6.0 vs 8.1 ms) but slowed the near pass more (9.4 vs 8.9 ms).
-template <int P>
+// DIAG (schedule diagnostics only, results invalid; PHM_COUPLING_DIAG): 1 =
+// the C_k fragment loads stay but no MMAs and no x-hat gathers run (L2
+// traffic of C_k alone), 2 = MMAs and gathers stay but the C_k fragments are
+// constants (fp64 pipe and x-hat traffic alone). 0 is the product kernel.
+template <int P, int DIAG = 0>
 __global__ void __maxnreg__(P >= 128 ? 128 : 88) k_coupling_mma(const CouplingItem* __restrict__ items,
                                                               const std::int32_t* __restrict__ order,
                                                               const std::int32_t* __restrict__ item_cls,
@@ -937,8 +941,9 @@ __global__ void __maxnreg__(P >= 128 ? 128 : 88) k_coupling_mma(const CouplingIt
     constexpr int PPT = (P / 2) / TPS;          // pairs per thread
     const int gslot = threadIdx.x / TPS, gsub = threadIdx.x % TPS;
     auto tau_of = [&](int e) { return cls_tau[static_cast<std::int64_t>(e) * kGroupSlots + gslot]; };
+    [[maybe_unused]] unsigned sink = 0;  // DIAG 1: keeps the fragment loads alive
     auto gather = [&](int e, int buf, int tau) {
-      const unsigned tiles = item_tiles[e];
+      const unsigned tiles = DIAG == 1 ? 0u : item_tiles[e];
       double* X = smem + buf * PANEL + gslot * LD;
       if ((tiles >> (gslot >> 3)) & 1u) {  // else the tile is skipped by the MMAs
         const double* src = xhat + (static_cast<std::int64_t>(tau < 0 ? 0 : tau) * m + col) * P;
@@ -952,6 +957,11 @@ __global__ void __maxnreg__(P >= 128 ? 128 : 88) k_coupling_mma(const CouplingIt
     };
     auto load_a = [&](int e, int h, double (&a)[KH][2]) {
       const double* Ck = C + static_cast<std::int64_t>(item_cls[e]) * P * P;
+      if constexpr (DIAG == 2) {
+#pragma unroll
+        for (int s2 = 0; s2 < KH; ++s2) a[s2][0] = a[s2][1] = 1.0 + h;
+        return;
+      }
       if constexpr (P == 64) {  // fragment order: one 16-byte load per k-step
         const double2* F = reinterpret_cast<const double2*>(Ck);
 #pragma unroll
@@ -970,6 +980,11 @@ __global__ void __maxnreg__(P >= 128 ? 128 : 88) k_coupling_mma(const CouplingIt
       }
     };
     auto mma = [&](const double (&a)[KH][2], int h, const double* X, unsigned tiles) {
+      if constexpr (DIAG == 1) {
+#pragma unroll
+        for (int s2 = 0; s2 < KH; ++s2) sink ^= __double2loint(a[s2][0]) ^ __double2hiint(a[s2][1]);
+        return;
+      }
       if (tiles == (1u << NT) - 1u) {
         // every tile holds a partner: k-step outer, tile inner, so the NT
         // accumulators are independent chains in flight
@@ -1023,6 +1038,7 @@ __global__ void __maxnreg__(P >= 128 ? 128 : 88) k_coupling_mma(const CouplingIt
       __syncthreads();  // X[buf] is refilled two classes later
     }
     double* out = partial + (static_cast<std::int64_t>(item) * m + col) * kGroupSlots * P;
+    if constexpr (DIAG == 1) acc[0][0] = __hiloint2double(0, static_cast<int>(sink));
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       const int n0 = 8 * j + 2 * t0;
@@ -3108,6 +3124,22 @@ void launch_coupling_mma(cudaStream_t st, const CouplingItem* items, const std::
   const size_t smem = 2 * kGroupSlots * (P + 4) * sizeof(double);
   const std::int64_t nvb = static_cast<std::int64_t>(nitems) * m;
   const int grid = static_cast<int>(max_ctas > 0 && max_ctas < nvb ? max_ctas : nvb);
+  static const int diag = [] {  // schedule diagnostics (results invalid), P = 64 only
+    const char* e = std::getenv("PHM_COUPLING_DIAG");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (P == 64 && (diag == 1 || diag == 2)) {
+    if (diag == 1) {
+      smem_attr(reinterpret_cast<const void*>(k_coupling_mma<64, 1>), 200 * 1024, false);
+      k_coupling_mma<64, 1><<<grid, 128, smem, st>>>(items, order, item_cls, item_tiles, cls_tau, C, xhat, m, partial,
+                                                     nitems);
+    } else {
+      smem_attr(reinterpret_cast<const void*>(k_coupling_mma<64, 2>), 200 * 1024, false);
+      k_coupling_mma<64, 2><<<grid, 128, smem, st>>>(items, order, item_cls, item_tiles, cls_tau, C, xhat, m, partial,
+                                                     nitems);
+    }
+    return;
+  }
 #define PHM_CASE(PP)                                                                                        \
   if (P == PP) {                                                                                            \
     smem_attr(reinterpret_cast<const void*>(k_coupling_mma<PP>), 200 * 1024, false);                       \
